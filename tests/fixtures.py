@@ -1,0 +1,70 @@
+"""Hand-built tiny workloads for pins and parity cases (inputs only — no method arithmetic).
+
+Output lengths are forced through the cap: with a point-mass eCDF at 60000 the sampler's
+l_out = min(X, y, l_max - l_in) equals y whenever y <= l_max - l_in.
+"""
+import numpy as np
+
+import samu_workloads as W
+
+NB = 9  # coeff buckets 1, 2, 4, ..., 256
+
+
+def spec(L=1, h=8, c=10, l_max=4096, tp_values=(1,), weight_bytes=1, kv_bytes_per_token=1):
+    mask = 0
+    for t in tp_values:
+        mask |= 1 << int(np.log2(t))
+    return dict(arch="tiny", L=L, h=h, c=c, l_max=l_max, tp_mask=mask, weight_bytes=weight_bytes,
+                kv_bytes_per_token=kv_bytes_per_token)
+
+
+def coeff(kind="const", value=1.0):
+    """[5][3][2][9] coefficient buckets.  const: lat = value; B: lat = B; S: lat = S."""
+    cf = np.zeros((W.N_TP_SLOTS, 3, 2, NB))
+    Bv = np.array([1, 2, 4, 8, 16, 32, 64, 128, 256], dtype=np.float64)
+    if kind == "const":
+        cf[:, 0, 1, :] = value
+    elif kind == "B":
+        cf[:, 0, 1, :] = Bv
+    elif kind == "S":
+        cf[:, 2, 0, :] = 1.0
+    elif kind == "flops":
+        cf[:, 0, 0, :] = value
+    else:
+        raise ValueError(kind)
+    return cf
+
+
+def zero_load():
+    return np.zeros((W.N_TP_SLOTS, W.MAX_DP))
+
+
+def engine(max_num_seqs=256, block_size=16, min_batched_tokens=2048, kv_cap=10 ** 15, n_gpus=1,
+           mem=10 ** 15):
+    return dict(max_num_seqs=max_num_seqs, block_size=block_size, min_batched_tokens=min_batched_tokens,
+                mem_util_permille=1000, mem_bytes_per_gpu=mem, kv_cap_bytes_per_gpu=kv_cap, n_gpus=n_gpus)
+
+
+def tiny(l_in, l_out, eng=None, sp=None, cf="const", load=None, pred=None, chain=None, n_trials=1):
+    """One node, requests with forced output lengths."""
+    sp = sp or spec()
+    cfa = coeff(cf) if isinstance(cf, str) else cf
+    return W.custom_workload(
+        [sp], [dict(l_in=l_in, cap=l_out, pred=pred, chain=chain)], n_trials=n_trials,
+        engine=eng or engine(), ecdfs=[(np.array([60000]), np.array([1]))], coeff=[cfa],
+        load=[load if load is not None else zero_load()])
+
+
+def multi(node_specs, eng=None, n_trials=1):
+    """Several nodes.  node_specs: list of dict(sp=..., l_in=..., l_out=..., cf=..., load=...,
+    pred=..., chain=..., ecdf=(values, cum) or None)."""
+    sps, reqs, ecdfs, cfs, loads = [], [], [], [], []
+    for ns in node_specs:
+        sps.append(ns.get("sp") or spec())
+        reqs.append(dict(l_in=ns["l_in"], cap=ns["l_out"], pred=ns.get("pred"), chain=ns.get("chain")))
+        ecdfs.append(ns.get("ecdf") or (np.array([60000]), np.array([1])))
+        c = ns.get("cf", "const")
+        cfs.append(coeff(c) if isinstance(c, str) else c)
+        loads.append(ns.get("load") if ns.get("load") is not None else zero_load())
+    return W.custom_workload(sps, reqs, n_trials=n_trials, engine=eng or engine(), ecdfs=ecdfs,
+                             coeff=cfs, load=loads)
