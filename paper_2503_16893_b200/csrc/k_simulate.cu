@@ -1,0 +1,617 @@
+// K2: iteration-level continuous-batching simulation (readings c3-c9,
+// c13, c15, c18, c19, c24, c25), one warp per (candidate, trial, dp replica).
+//
+// Design (B200-first, not a translation of the per-request oracle loop):
+//  * persistent grid, one work item per warp, pulled from an atomic counter over a host-sorted
+//    longest-first item list (replica-sims differ ~100x in length);
+//  * the running set lives in shared memory: 256 slots, lane L owns slots L + 32 j, so slot
+//    scans are bank-conflict free;
+//  * the per-iteration state is O(1): B, S = sum(l), s = d + max(l - d), the exact KV-block need
+//    of decode step d comes from a histogram over (l - 1 - d) mod bs (every running request
+//    advances one token per decode, so its phase is fixed at admission); finishes are events at
+//    the minimum finish decode-index — a uniform decode iteration touches no request;
+//  * admission is a warp prefix-scan over the next 32 queue heads (tokens and KV blocks), retire
+//    is a slot scan + REDUX reductions only at finish events;
+//  * Eq. prefill / decode FLOPs are exact u64 (u128 sums); the latency is evaluated in fp64 with
+//    explicit round-to-nearest intrinsics (no contraction) in the contract's order (c24).
+#include "samu_internal.cuh"
+
+#include <math_constants.h>
+
+namespace {
+
+constexpr uint32_t FULL = 0xFFFFFFFFu;
+constexpr int SLOTS = 256;
+
+struct WarpSm {
+  uint32_t s_req[SLOTS];     // request id, SAMU_EMPTY if free
+  uint32_t s_fin[SLOTS];     // decode index at which it finishes
+  int32_t s_o[SLOTS];        // l - d (constant while running)
+  uint32_t s_meta[SLOTS];    // admission rank << 5 | phase  (phase = (o - 1) mod bs)
+  uint32_t stk_req[SLOTS];   // preempted stack, top = front of W
+  uint32_t stk_g[SLOTS];
+  uint32_t tmp[SLOTS];       // finished requests of the current iteration / radix histogram
+  uint32_t tmp2[SLOTS];      // released successors
+  uint32_t hist[32];         // running requests per phase
+  uint32_t adm_req[32], adm_fin[32], adm_meta[32];
+  int32_t adm_o[32];
+};
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t n = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v += n;
+  }
+  return v;
+}
+
+__device__ __forceinline__ uint64_t dkey(double x) {   // order-preserving double -> u64
+  const uint64_t b = (uint64_t)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double kdouble(uint64_t k) {
+  const uint64_t b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+
+__device__ __forceinline__ uint32_t cdiv(uint32_t a, uint32_t b) { return (a + b - 1) / b; }
+
+__device__ __forceinline__ uint32_t posmod(int32_t a, uint32_t m) {
+  const int32_t r = a % (int32_t)m;
+  return (uint32_t)(r < 0 ? r + (int32_t)m : r);
+}
+
+// Eq. per-iter cost, reading c24: ((fma_c + fma_p) + fma_s), exact integer -> RN
+__device__ __forceinline__ double iter_cost(const double* __restrict__ coef, uint32_t ms, uint32_t B, uint64_t F,
+                                            uint32_t Bs, uint32_t S) {
+  const double* cb = coef + (B - 1);
+  const double tc = __fma_rn(__ldg(cb), __ull2double_rn(F), __ldg(cb + ms));
+  const double tp = __fma_rn(__ldg(cb + 2 * ms), __uint2double_rn(Bs), __ldg(cb + 3 * ms));
+  const double ts = __fma_rn(__ldg(cb + 4 * ms), __uint2double_rn(S), __ldg(cb + 5 * ms));
+  return __dadd_rn(__dadd_rn(tc, tp), ts);
+}
+
+__device__ __forceinline__ void set_error(int32_t* e, int32_t code) { atomicCAS(e, 0, code); }
+
+struct Sim {
+  // uniform scalar state
+  double t, tau, next_ready;
+  uint64_t fl_lo, fl_hi, reqit;
+  uint32_t iter, d, needidx, B, S, next_fin, next_rank;
+  int32_t F, maxO;
+  uint32_t stack_cnt, q_head, q_tail, n_heads, pend_ptr, n_pend;
+  int32_t err;
+};
+
+__device__ __forceinline__ void add_flops(Sim& m, uint64_t f) {
+  const uint64_t lo = m.fl_lo + f;
+  m.fl_hi += (lo < m.fl_lo) ? 1ull : 0ull;
+  m.fl_lo = lo;
+}
+
+// rescan the running set: next finish index and max(l - d)
+__device__ __forceinline__ void rescan(WarpSm& W, Sim& m, int lane) {
+  uint32_t mn = FULL;
+  int32_t mx = INT_MIN;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int s = lane + 32 * j;
+    if (W.s_req[s] != SAMU_EMPTY) {
+      mn = min(mn, W.s_fin[s]);
+      mx = max(mx, W.s_o[s]);
+    }
+  }
+  m.next_fin = __reduce_min_sync(FULL, mn);
+  m.maxO = __reduce_max_sync(FULL, mx);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunch P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpSm& W = reinterpret_cast<WarpSm*>(smem_raw)[warp];
+  const int gw = blockIdx.x * SAMU_WARPS_PER_BLOCK + warp;
+  uint32_t* q = P.scratch_q + (size_t)gw * P.max_q;
+  uint64_t* pkey = P.scratch_key + (size_t)gw * 2 * P.max_p;
+  uint32_t* pidx = P.scratch_idx + (size_t)gw * 2 * P.max_p;
+  const DevApp& A = P.app;
+  const int n = A.n_req;
+
+  for (;;) {
+    uint32_t item = 0;
+    if (lane == 0) item = atomicAdd(P.next_item, 1u);
+    item = __shfl_sync(FULL, item, 0);
+    if (item >= (uint32_t)P.n_items) break;
+    const uint2 it = P.items[item];
+    const uint32_t ci = it.x, k = it.y >> 4, j = it.y & 15u;
+    const DevCand& C = P.cands[ci];
+    const size_t tb = (size_t)k * n;
+    const uint16_t* __restrict__ lo = P.l_out + tb;
+    const uint16_t* __restrict__ li = P.l_in + tb;
+    uint32_t* st = P.st ? P.st + tb : nullptr;
+    uint16_t* gst = P.g ? P.g + tb : nullptr;
+    double* ft = P.fin_t ? P.fin_t + tb : nullptr;
+    const double* sfin = C.src_fin ? C.src_fin + tb : nullptr;
+    double* fto = C.fin_t_out ? C.fin_t_out + tb : nullptr;
+    uint32_t* fio = C.fin_iter_out ? C.fin_iter_out + tb : nullptr;
+    double* over = P.over ? P.over + ((size_t)k * A.n_nodes + C.node) * 16 : nullptr;
+    const uint32_t r0 = C.rep_off[j], r1 = C.rep_off[j + 1];
+    const uint32_t bs = C.bs, ms = C.max_seqs;
+    const bool commit = C.commit && st;
+
+    Sim m;
+    m.t = C.resume ? (over ? over[j] : 0.0) : C.load_s;
+    m.tau = C.tau ? C.tau[k] : (C.tau_rec ? C.tau_rec[k].t_end : CUDART_INF);
+    m.fl_lo = m.fl_hi = m.reqit = 0;
+    m.iter = 0; m.d = 0; m.needidx = 0; m.B = 0; m.S = 0; m.next_rank = 0;
+    m.F = C.blocks; m.maxO = INT_MIN; m.next_fin = FULL;
+    m.stack_cnt = 0; m.q_head = 0; m.q_tail = 0; m.n_heads = 0; m.pend_ptr = 0; m.n_pend = 0;
+    m.err = 0;
+
+    for (int s = lane; s < SLOTS; s += 32) W.s_req[s] = SAMU_EMPTY;
+    W.hist[lane] = 0;
+    __syncwarp();
+
+    // ---- initial state from the carried WorkloadState (c18, c27) ----
+    uint32_t n_run = 0, n_pre = 0, n_q = 0;
+    bool all_done = true;
+    for (uint32_t base = r0; base < r1; base += 32) {
+      const uint32_t idx = base + lane;
+      const bool valid = idx < r1;
+      const uint32_t r = valid ? __ldg(C.rep_req + idx) : 0u;
+      const uint32_t w = (valid && st) ? st[r] : 0u;
+      const uint32_t s = w >> 28;
+      const int32_t pr = valid ? __ldg(A.pred + r) : -1;
+      const bool cross = valid && pr >= 0 && __ldg(A.cross + r);
+      const bool fresh = valid && s == SAMU_ST_FRESH;
+      const bool head = fresh && pr < 0;
+      const bool pend = fresh && cross;
+      const bool succ_wait = fresh && pr >= 0 && !cross;
+      if (succ_wait && st && (st[pr] >> 28) == SAMU_ST_DONE) m.err = SAMU_E_STATE;
+      if (valid && s > SAMU_ST_DONE) m.err = SAMU_E_STATE;
+      const uint32_t bh = __ballot_sync(FULL, head);
+      if (head) q[m.q_tail + __popc(bh & lanemask_lt())] = r;
+      m.q_tail += __popc(bh);
+      const uint32_t bp = __ballot_sync(FULL, pend);
+      if (pend) {
+        double ready;
+        if (st && (st[pr] >> 28) == SAMU_ST_DONE && ft) ready = ft[pr];
+        else if (sfin) ready = sfin[pr];
+        else ready = CUDART_INF;
+        const uint32_t pos = m.n_pend + __popc(bp & lanemask_lt());
+        if (pos < (uint32_t)P.max_p) { pkey[pos] = dkey(ready); pidx[pos] = r; }
+      }
+      m.n_pend += __popc(bp);
+      n_run += __popc(__ballot_sync(FULL, valid && s == SAMU_ST_RUNNING));
+      n_pre += __popc(__ballot_sync(FULL, valid && s == SAMU_ST_PREEMPTED));
+      n_q += __popc(__ballot_sync(FULL, valid && s == SAMU_ST_QUEUED));
+      if (__ballot_sync(FULL, valid && s != SAMU_ST_DONE)) all_done = false;
+    }
+    m.err = __reduce_max_sync(FULL, (uint32_t)(-m.err)) ? SAMU_E_STATE : 0;
+    m.n_heads = m.q_tail;
+    if (m.n_pend > (uint32_t)P.max_p || m.q_tail + n_q > (uint32_t)P.max_q) m.err = SAMU_E_STATE;
+    const uint32_t n_stack0 = C.resume ? n_pre : n_run + n_pre;
+    if ((C.resume && n_run > ms) || n_stack0 > SLOTS) m.err = SAMU_E_STATE;
+    if (!m.err && (n_run | n_pre | n_q)) {
+      int32_t used = 0;
+      uint32_t S0 = 0;
+      for (uint32_t base = r0; base < r1; base += 32) {
+        const uint32_t idx = base + lane;
+        const bool valid = idx < r1;
+        const uint32_t r = valid ? __ldg(C.rep_req + idx) : 0u;
+        const uint32_t w = valid ? st[r] : 0u;
+        const uint32_t s = w >> 28, rk = w & 0x0FFFFFFFu;
+        if (valid && s == SAMU_ST_RUNNING) {
+          const uint32_t g = gst[r];
+          if (rk >= n_run) { m.err = SAMU_E_STATE; }
+          else if (C.resume) {
+            const uint32_t lin = li[r];
+            const uint32_t Lr = max((uint32_t)lo[r], 1u);
+            const int32_t o = (int32_t)(lin + g);
+            const uint32_t ph = posmod(o - 1, bs);
+            W.s_req[rk] = r;
+            W.s_fin[rk] = Lr - g;
+            W.s_o[rk] = o;
+            W.s_meta[rk] = (rk << 5) | ph;
+            atomicAdd(&W.hist[ph], 1u);
+            used += (int32_t)cdiv(lin + g - 1, bs);
+            S0 += lin + g;
+          } else {
+            const uint32_t pos = n_stack0 - 1 - rk;
+            W.stk_req[pos] = r;
+            W.stk_g[pos] = g;
+          }
+        } else if (valid && s == SAMU_ST_PREEMPTED) {
+          const uint32_t p = (C.resume ? 0u : n_run) + rk;
+          if (p >= n_stack0) m.err = SAMU_E_STATE;
+          else { W.stk_req[n_stack0 - 1 - p] = r; W.stk_g[n_stack0 - 1 - p] = gst[r]; }
+        } else if (valid && s == SAMU_ST_QUEUED) {
+          if (rk >= n_q) m.err = SAMU_E_STATE;
+          else q[m.n_heads + rk] = r;
+        }
+      }
+      used = (int32_t)__reduce_add_sync(FULL, (uint32_t)used);
+      S0 = __reduce_add_sync(FULL, S0);
+      m.err = __reduce_max_sync(FULL, (uint32_t)(-m.err)) ? SAMU_E_STATE : 0;
+      if (C.resume) {
+        m.B = n_run;
+        m.S = S0;
+        m.F -= used;
+        m.next_rank = n_run;
+        if (m.F < 0) m.err = SAMU_E_STATE;
+      }
+      m.stack_cnt = n_stack0;
+      m.q_tail = m.n_heads + n_q;
+    }
+    __syncwarp();
+    if (m.B) rescan(W, m, lane);
+
+    // ---- sort pending cross-node arrivals by (ready, index): stable LSD radix (8 x 8 bits) ----
+    if (!m.err && m.n_pend > 1) {
+      uint64_t* ka = pkey;
+      uint64_t* kb = pkey + P.max_p;
+      uint32_t* ia = pidx;
+      uint32_t* ib = pidx + P.max_p;
+      for (int pass = 0; pass < 8; ++pass) {
+        const int sh = pass * 8;
+        for (int b = lane; b < 256; b += 32) W.tmp[b] = 0;
+        __syncwarp();
+        for (uint32_t i = lane; i < m.n_pend; i += 32) atomicAdd(&W.tmp[(ka[i] >> sh) & 255u], 1u);
+        __syncwarp();
+        // exclusive scan of the 256 bins: lane handles 8 consecutive bins
+        uint32_t loc[8], sum = 0;
+        bool one_bin = false;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) { loc[b] = W.tmp[lane * 8 + b]; sum += loc[b]; one_bin |= loc[b] == m.n_pend; }
+        if (__any_sync(FULL, one_bin)) { __syncwarp(); continue; }   // one bin holds every key: no-op pass
+        const uint32_t incl = warp_incl_scan(sum, lane);
+        uint32_t run = incl - sum;
+        __syncwarp();
+#pragma unroll
+        for (int b = 0; b < 8; ++b) { W.tmp[lane * 8 + b] = run; run += loc[b]; }
+        __syncwarp();
+        for (uint32_t base = 0; base < m.n_pend; base += 32) {
+          const uint32_t i = base + lane;
+          const bool v = i < m.n_pend;
+          const uint32_t act = __ballot_sync(FULL, v);
+          if (v) {
+            const uint64_t key = ka[i];
+            const uint32_t dg = (uint32_t)(key >> sh) & 255u;
+            const uint32_t peers = __match_any_sync(act, dg);
+            const uint32_t pos = W.tmp[dg] + __popc(peers & lanemask_lt());
+            kb[pos] = key;
+            ib[pos] = ia[i];
+            __syncwarp(act);
+            if ((peers & lanemask_lt()) == 0) W.tmp[dg] += __popc(peers);
+          }
+          __syncwarp();
+        }
+        uint64_t* tk = ka; ka = kb; kb = tk;
+        uint32_t* ti = ia; ia = ib; ib = ti;
+      }
+      if (ka != pkey) {   // odd number of effective passes: copy back
+        for (uint32_t i = lane; i < m.n_pend; i += 32) { pkey[i] = ka[i]; pidx[i] = ia[i]; }
+        __syncwarp();
+      }
+    }
+    m.next_ready = m.n_pend ? kdouble(pkey[0]) : CUDART_INF;
+    const uint64_t K1 = 2ull * C.L * C.h_tp;
+    bool cut = false;
+
+    // ---- main loop (c25) ----
+    while (!m.err) {
+      if (m.t >= m.tau) { cut = true; break; }
+      // (2) pending cross-node arrivals with ready <= t join the back of W
+      while (m.pend_ptr < m.n_pend && m.next_ready <= m.t) {
+        const uint32_t i = m.pend_ptr + lane;
+        const bool ok = i < m.n_pend && kdouble(pkey[i]) <= m.t;
+        const uint32_t b = __ballot_sync(FULL, ok);
+        const uint32_t cnt = (b == FULL) ? 32u : (uint32_t)(__ffs(~b) - 1);
+        if (lane < cnt) q[m.q_tail + lane] = pidx[i];
+        m.q_tail += cnt;
+        m.pend_ptr += cnt;
+        m.next_ready = m.pend_ptr < m.n_pend ? kdouble(pkey[m.pend_ptr]) : CUDART_INF;
+      }
+      const bool wnon = m.stack_cnt > 0 || m.q_head < m.q_tail;
+      if (m.B == 0 && !wnon) {
+        if (m.pend_ptr < m.n_pend && m.next_ready != CUDART_INF) { m.t = m.next_ready; continue; }
+        break;
+      }
+      // head of W fits? (slots, token budget, blocks)
+      bool fits = false;
+      if (wnon && m.B < ms) {
+        uint32_t hr, hg;
+        if (m.stack_cnt) { hr = W.stk_req[m.stack_cnt - 1]; hg = W.stk_g[m.stack_cnt - 1]; }
+        else { hr = q[m.q_head]; hg = 0; }
+        const uint32_t p = (uint32_t)li[hr] + hg;
+        fits = p <= C.budget && (int32_t)cdiv(p, bs) <= m.F;
+      }
+      uint32_t n_fin = 0;
+      if (fits) {
+        // ================= prefill iteration (c8): admit a strict FCFS prefix of W =========
+        uint32_t k_adm = 0, tok = 0, smaxp = 0, S_add = 0, n_stay = 0;
+        int32_t blk = 0, freed = 0;
+        for (;;) {
+          const uint32_t avail = m.stack_cnt + (m.q_tail - m.q_head);
+          if (avail == 0) break;
+          const bool valid = (uint32_t)lane < avail;
+          uint32_t r = 0, g = 0;
+          if ((uint32_t)lane < m.stack_cnt) { r = W.stk_req[m.stack_cnt - 1 - lane]; g = W.stk_g[m.stack_cnt - 1 - lane]; }
+          else if (valid) r = q[m.q_head + lane - m.stack_cnt];
+          const uint32_t p = valid ? (uint32_t)li[r] + g : 0u;
+          const uint32_t nb = valid ? cdiv(p, bs) : 0u;
+          const uint32_t sp = warp_incl_scan(p, lane), sb = warp_incl_scan(nb, lane);
+          const bool ok = valid && (m.B + k_adm + lane + 1 <= ms) && (tok + sp <= C.budget) &&
+                          ((int32_t)(blk + sb) <= m.F);
+          const uint32_t bal = __ballot_sync(FULL, ok);
+          const uint32_t mm = (bal == FULL) ? 32u : (uint32_t)(__ffs(~bal) - 1);
+          if (mm == 0) break;
+          const bool adm = (uint32_t)lane < mm;
+          const uint32_t Lr = adm ? max((uint32_t)lo[r], 1u) : 0u;
+          const bool finish_now = adm && g + 1 >= Lr;
+          const bool stay = adm && !finish_now;
+          // stage stays (admission order) and immediate finishers
+          const uint32_t bst = __ballot_sync(FULL, stay);
+          const uint32_t bfn = __ballot_sync(FULL, finish_now);
+          if (stay) {
+            const uint32_t a = __popc(bst & lanemask_lt());
+            const int32_t o = (int32_t)(p + 1) - (int32_t)m.d;
+            const uint32_t ph = posmod((int32_t)p - (int32_t)m.d, bs);
+            W.adm_req[a] = r;
+            W.adm_fin[a] = m.d + (Lr - (g + 1));
+            W.adm_o[a] = o;
+            W.adm_meta[a] = ((m.next_rank + k_adm + lane) << 5) | ph;
+            atomicAdd(&W.hist[ph], 1u);
+          }
+          if (finish_now) W.tmp[n_fin + __popc(bfn & lanemask_lt())] = r;
+          n_fin += __popc(bfn);
+          const uint32_t ns = __popc(bst);
+          freed += (int32_t)__reduce_add_sync(FULL, finish_now ? nb : 0u);
+          S_add += __reduce_add_sync(FULL, stay ? p + 1 : 0u);
+          smaxp = max(smaxp, __reduce_max_sync(FULL, adm ? p : 0u));
+          __syncwarp();
+          // insert stays into free slots: lane L fills admitted ordinals [ex, ex + nfree)
+          if (ns) {
+            uint32_t freemask = 0;
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj)
+              if (W.s_req[lane + 32 * jj] == SAMU_EMPTY) freemask |= 1u << jj;
+            const uint32_t nf = __popc(freemask);
+            const uint32_t ex = warp_incl_scan(nf, lane) - nf;
+            uint32_t a = ex;
+            while (freemask && a < ns) {
+              const int jj = __ffs(freemask) - 1;
+              freemask &= freemask - 1;
+              const int s = lane + 32 * jj;
+              W.s_req[s] = W.adm_req[a];
+              W.s_fin[s] = W.adm_fin[a];
+              W.s_o[s] = W.adm_o[a];
+              W.s_meta[s] = W.adm_meta[a];
+              ++a;
+            }
+            __syncwarp();
+          }
+          n_stay += ns;
+          tok += __shfl_sync(FULL, sp, mm - 1);
+          blk += (int32_t)__shfl_sync(FULL, sb, mm - 1);
+          k_adm += mm;
+          const uint32_t take = min(mm, m.stack_cnt);
+          m.stack_cnt -= take;
+          m.q_head += mm - take;
+          if (mm < 32) break;
+        }
+        m.F -= blk;
+        // Eq. prefill FLOPs: L (c B s + 2 B h s^2 / tp)
+        const uint64_t Bp = k_adm, sp64 = smaxp;
+        const uint64_t fl = (uint64_t)C.L * (C.c * Bp * sp64 + 2ull * Bp * C.h_tp * sp64 * sp64);
+        const double lat = iter_cost(C.coef, ms, k_adm, fl, k_adm * smaxp, tok);
+        m.t = __dadd_rn(m.t, lat);
+        add_flops(m, fl);
+        m.reqit += k_adm;
+        m.iter += 1;
+        m.F += freed;
+        m.B += n_stay;
+        m.S += S_add;
+        m.next_rank += k_adm;
+        if (n_stay) rescan(W, m, lane);
+      } else {
+        if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; break; }
+        // ================= decode run (c9): uniform iterations until an event ===============
+        uint32_t B = m.B;
+        uint64_t K0 = (uint64_t)C.L * C.c * B;
+        uint32_t smax = (uint32_t)((int32_t)m.d + m.maxO);
+        const double stop_t = fmin(m.tau, m.next_ready);
+        bool event = false;
+        for (;;) {
+          uint32_t need = W.hist[m.needidx];
+          if ((int32_t)need > m.F) {
+            // recompute preemption of the last admitted request (c7)
+            while ((int32_t)need > m.F) {
+              uint32_t best = 0;
+              int bslot = -1;
+#pragma unroll
+              for (int jj = 0; jj < 8; ++jj) {
+                const int s = lane + 32 * jj;
+                if (W.s_req[s] != SAMU_EMPTY && (bslot < 0 || W.s_meta[s] > best)) { best = W.s_meta[s]; bslot = s; }
+              }
+              const uint32_t vmeta = __reduce_max_sync(FULL, bslot >= 0 ? best : 0u);
+              const uint32_t own = __ballot_sync(FULL, bslot >= 0 && best == vmeta);
+              const int ol = __ffs(own) - 1;
+              const int vs = __shfl_sync(FULL, bslot, ol);
+              const uint32_t vr = W.s_req[vs];
+              const int32_t vo = W.s_o[vs];
+              const uint32_t vph = vmeta & 31u;
+              const uint32_t l = (uint32_t)(vo + (int32_t)m.d);
+              m.F += (int32_t)cdiv(l - 1, bs);
+              if (vph == m.needidx) --need;
+              __syncwarp();
+              if (lane == 0) {
+                W.hist[vph] -= 1;
+                W.s_req[vs] = SAMU_EMPTY;
+                W.stk_req[m.stack_cnt] = vr;
+                W.stk_g[m.stack_cnt] = l - (uint32_t)li[vr];
+              }
+              __syncwarp();
+              m.stack_cnt += 1;
+              m.B -= 1;
+              m.S -= l;
+              if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; break; }
+            }
+            if (m.err) break;
+            rescan(W, m, lane);
+            B = m.B;
+            K0 = (uint64_t)C.L * C.c * B;
+            smax = (uint32_t)((int32_t)m.d + m.maxO);
+            event = true;   // W changed: re-check admission after this iteration
+          }
+          m.F -= (int32_t)need;
+          // Eq. decode FLOPs: L (c B + 2 h S / tp)
+          const uint64_t fl = K0 + K1 * (uint64_t)m.S;
+          const double lat = iter_cost(C.coef, ms, B, fl, B * smax, m.S);
+          m.t = __dadd_rn(m.t, lat);
+          add_flops(m, fl);
+          m.reqit += B;
+          m.iter += 1;
+          m.S += B;
+          smax += 1;
+          m.d += 1;
+          m.needidx = m.needidx == 0 ? bs - 1 : m.needidx - 1;
+          if (m.d == m.next_fin) {
+            // retire the finishers (ballot / REDUX over the slot scan)
+            uint32_t mn = FULL, cnt = 0, sfin_l = 0;
+            int32_t mx = INT_MIN, fr = 0;
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+              const int s = lane + 32 * jj;
+              const uint32_t rq = W.s_req[s];
+              if (rq != SAMU_EMPTY) {
+                const uint32_t f = W.s_fin[s];
+                const int32_t o = W.s_o[s];
+                if (f == m.d) {
+                  const uint32_t l_now = (uint32_t)(o + (int32_t)m.d);
+                  fr += (int32_t)cdiv(l_now - 1, bs);
+                  sfin_l += l_now;
+                  atomicSub(&W.hist[W.s_meta[s] & 31u], 1u);
+                  W.s_req[s] = SAMU_EMPTY;
+                  W.tmp2[cnt * 32 + lane] = rq;   // staged per lane (<= 8 each)
+                  ++cnt;
+                } else {
+                  mn = min(mn, f);
+                  mx = max(mx, o);
+                }
+              }
+            }
+            // compact finished ids into tmp in lane-major order
+            const uint32_t ex = warp_incl_scan(cnt, lane) - cnt;
+            for (uint32_t c2 = 0; c2 < cnt; ++c2) W.tmp[ex + c2] = W.tmp2[c2 * 32 + lane];
+            n_fin = __reduce_add_sync(FULL, cnt);
+            m.F += (int32_t)__reduce_add_sync(FULL, (uint32_t)fr);
+            m.S -= __reduce_add_sync(FULL, sfin_l);
+            m.B -= n_fin;
+            m.next_fin = __reduce_min_sync(FULL, mn);
+            m.maxO = __reduce_max_sync(FULL, mx);
+            __syncwarp();
+            event = true;
+          }
+          if (event || m.t >= stop_t) break;
+        }
+        if (m.err) break;
+      }
+      // ---- finish records + chain successor release (c19), for this iteration's finishers ----
+      if (n_fin) {
+        const uint32_t itx = m.iter - 1;
+        uint32_t nrel = 0;
+        for (uint32_t base = 0; base < n_fin; base += 32) {
+          const uint32_t i = base + lane;
+          const bool v = i < n_fin;
+          const uint32_t r = v ? W.tmp[i] : 0u;
+          int32_t sr = -1;
+          if (v) {
+            if (fio) fio[r] = itx;
+            if (fto) fto[r] = m.t;
+            if (commit) { st[r] = SAMU_ST_DONE << 28; ft[r] = m.t; }
+            sr = __ldg(A.succ + r);
+          }
+          const uint32_t br = __ballot_sync(FULL, sr >= 0);
+          if (sr >= 0) W.tmp2[nrel + __popc(br & lanemask_lt())] = (uint32_t)sr;
+          nrel += __popc(br);
+        }
+        __syncwarp();
+        if (nrel) {
+          // append in index order: rank of each released id among the released set
+          for (uint32_t i = lane; i < nrel; i += 32) {
+            const uint32_t x = W.tmp2[i];
+            uint32_t rank = 0;
+            for (uint32_t jj = 0; jj < nrel; ++jj) rank += W.tmp2[jj] < x ? 1u : 0u;
+            q[m.q_tail + rank] = x;
+          }
+          m.q_tail += nrel;
+          __syncwarp();
+        }
+      }
+    }
+
+    // ---- write back (commit) and the per-replica record ----
+    const bool done = !m.err && m.B == 0 && m.stack_cnt == 0 && m.q_head == m.q_tail && m.pend_ptr == m.n_pend;
+    if (m.err) set_error(P.error, m.err);
+    if (commit && !m.err) {
+      for (int s = lane; s < SLOTS; s += 32) {
+        const uint32_t rq = W.s_req[s];
+        if (rq != SAMU_EMPTY) {
+          const uint32_t me = W.s_meta[s];
+          uint32_t rank = 0;
+          for (int s2 = 0; s2 < SLOTS; ++s2)
+            if (W.s_req[s2] != SAMU_EMPTY && W.s_meta[s2] < me) ++rank;
+          st[rq] = (SAMU_ST_RUNNING << 28) | rank;
+          gst[rq] = (uint16_t)((uint32_t)(W.s_o[s] + (int32_t)m.d) - (uint32_t)li[rq]);
+        }
+      }
+      for (uint32_t i = lane; i < m.stack_cnt; i += 32) {
+        const uint32_t rq = W.stk_req[i];
+        st[rq] = (SAMU_ST_PREEMPTED << 28) | (m.stack_cnt - 1 - i);
+        gst[rq] = (uint16_t)W.stk_g[i];
+      }
+      const uint32_t qbase = max(m.q_head, m.n_heads);
+      for (uint32_t pos = m.q_head + lane; pos < m.q_tail; pos += 32) {
+        const uint32_t rq = q[pos];
+        if (pos >= m.n_heads) st[rq] = (SAMU_ST_QUEUED << 28) | (pos - qbase);
+        gst[rq] = 0;
+      }
+      if (over && lane == 0) over[j] = (done || !cut) ? 0.0 : __dsub_rn(m.t, m.tau);
+    }
+    if (lane == 0) {
+      samu_trial_rec rec;
+      rec.t_end = m.t;
+      rec.flops_lo = m.fl_lo;
+      rec.flops_hi = m.fl_hi;
+      rec.req_iters = m.reqit;
+      rec.iters = m.iter;
+      rec.flags = (done ? 1u : 0u) | (cut ? 2u : 0u) | (all_done ? 4u : 0u);
+      P.rep_rec[((size_t)ci * P.n_trials + k) * 16 + j] = rec;
+    }
+    __syncwarp();
+  }
+}
+
+int32_t simulate_smem_bytes() { return (int32_t)(sizeof(WarpSm) * SAMU_WARPS_PER_BLOCK); }
+
+cudaError_t simulate_prepare(int* blocks_per_sm) {
+  const int smem = simulate_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(k_simulate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_simulate, 32 * SAMU_WARPS_PER_BLOCK, smem);
+}
+
+cudaError_t launch_simulate(const SimLaunch& L, int32_t n_blocks, cudaStream_t s) {
+  k_simulate<<<n_blocks, 32 * SAMU_WARPS_PER_BLOCK, simulate_smem_bytes(), s>>>(L);
+  return cudaGetLastError();
+}

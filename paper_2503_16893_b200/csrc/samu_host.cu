@@ -1,0 +1,1063 @@
+// libsamu host runtime: the C ABI of include/samu.h.  Registries, validation, device uploads,
+// batched simulation launches (K1/K2/K3), NCCL trial sharding and the Algorithm 1 control loop
+// whose scoring runs on the device (K4).  No simulation arithmetic runs here.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "samu_internal.cuh"
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void release() { if (p) cudaFree(p); p = nullptr; n = 0; }
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= n && p) return cudaSuccess;
+    release();
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(bytes, 16));
+    if (e != cudaSuccess) { p = nullptr; return e; }
+    n = std::max<size_t>(bytes, 16);
+    return cudaSuccess;
+  }
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+struct ModelReg {
+  bool spec_set = false, ecdf_set = false;
+  samu_model_spec spec{};
+  std::vector<uint32_t> bucket_B;
+  std::vector<double> coeff;   // [5][3][2][nb]
+  std::vector<double> load;    // [5][16]
+  std::vector<uint32_t> ev, ec;
+};
+
+int log2_exact(uint32_t x) {
+  for (int k = 0; k < 32; ++k) if ((1u << k) == x) return k;
+  return -1;
+}
+
+}  // namespace
+
+struct samu_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  std::string err;
+  bool poisoned = false;
+  int n_sm = 148;
+  ModelReg models[SAMU_MAX_NODES];
+
+  // application
+  bool app_loaded = false;
+  samu_engine_cfg eng{};
+  int n_nodes = 0, n_req = 0;
+  std::vector<int32_t> node_model, node_begin, node_end, node_input;
+  std::vector<samu_request> req;
+  std::vector<int32_t> succ;
+  std::vector<uint8_t> cross;
+  std::vector<std::vector<int32_t>> waves;
+  DevBuf d_l_in_base, d_cap, d_pred, d_node, d_succ, d_cross;
+  DevBuf d_ev, d_ec, d_eoff, d_mnode, d_lmax;
+  std::vector<DevBuf> d_waves;
+  std::map<std::pair<int, int>, DevBuf> coef;                      // (model, tp slot) -> dense table
+  std::map<std::pair<int, int>, std::pair<DevBuf, DevBuf>> rep;    // (node, dp) -> (off, req)
+  std::map<std::pair<int, int>, std::vector<uint32_t>> rep_off_host;
+
+  // launch scratch
+  DevBuf d_cands, d_items, d_counter, d_rep_rec, d_scratch_q, d_scratch_key, d_scratch_idx, d_error;
+  DevBuf d_sum, d_gather_send, d_gather_recv;
+  int sim_blocks_per_sm = 0;
+
+  // stats
+  int64_t n_sims = 0;
+  uint64_t req_iters = 0;
+};
+
+#define FAIL(ctx, code, msg)          \
+  do {                                \
+    (ctx)->err = (msg);               \
+    return (code);                    \
+  } while (0)
+
+#define CK(ctx, call)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess) {                                                           \
+      (ctx)->err = std::string("CUDA: ") + cudaGetErrorString(e_) + " at " #call;      \
+      if (e_ != cudaErrorMemoryAllocation) (ctx)->poisoned = true;                     \
+      return e_ == cudaErrorMemoryAllocation ? SAMU_E_NOMEM : SAMU_E_CUDA;             \
+    }                                                                                  \
+  } while (0)
+
+#define CKN(ctx, call)                                                                 \
+  do {                                                                                 \
+    ncclResult_t e_ = (call);                                                          \
+    if (e_ != ncclSuccess) {                                                           \
+      (ctx)->err = std::string("NCCL: ") + ncclGetErrorString(e_);                     \
+      (ctx)->poisoned = true;                                                          \
+      return SAMU_E_NCCL;                                                              \
+    }                                                                                  \
+  } while (0)
+
+#define GUARD(ctx)                                                                     \
+  do {                                                                                 \
+    if (!(ctx)) return SAMU_E_INVALID;                                                 \
+    if ((ctx)->poisoned) return SAMU_E_STATE;                                          \
+    cudaSetDevice((ctx)->device);                                                      \
+  } while (0)
+
+#define RET(x)                 \
+  do {                         \
+    samu_status r_ = (x);      \
+    if (r_ != SAMU_OK) return r_; \
+  } while (0)
+
+template <class T>
+static cudaError_t upload(DevBuf& b, const std::vector<T>& v, cudaStream_t s) {
+  cudaError_t e = b.ensure(sizeof(T) * v.size());
+  if (e != cudaSuccess) return e;
+  if (v.empty()) return cudaSuccess;
+  e = cudaMemcpyAsync(b.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(s);
+}
+
+// ---------------------------------------------------------------------------------------------
+// engine arithmetic (reading c5/c6): blocks per replica, or -1 if the plan is invalid
+// ---------------------------------------------------------------------------------------------
+static int64_t plan_blocks(const samu_ctx* c, int model, int dp, int tp) {
+  const samu_model_spec& M = c->models[model].spec;
+  const samu_engine_cfg& e = c->eng;
+  const int slot = log2_exact((uint32_t)tp);
+  if (slot < 0 || slot >= SAMU_N_TP_SLOTS || !((M.tp_mask >> slot) & 1u)) return -1;
+  if (M.hidden % (uint32_t)tp) return -1;
+  if (dp < 1 || dp > SAMU_MAX_DP || (uint32_t)(dp * tp) > e.n_gpus) return -1;
+  const uint64_t util = e.mem_bytes_per_gpu * e.mem_util_permille / 1000;
+  const uint64_t wshard = (M.weight_bytes + (uint64_t)tp - 1) / (uint64_t)tp;
+  if (util <= wshard) return -1;
+  const uint64_t kv = std::min<uint64_t>(e.kv_cap_bytes_per_gpu, util - wshard);
+  uint64_t blocks = ((uint64_t)tp * kv) / ((uint64_t)e.block_size * M.kv_bytes_per_token);
+  if (blocks < (M.l_max + e.block_size - 1) / e.block_size) return -1;
+  if (blocks > 0x7fffffffull) blocks = 0x7fffffffull;
+  return (int64_t)blocks;
+}
+
+// valid plans of a model: ascending #gpu, then ascending tp
+static std::vector<std::pair<int, int>> plans_of(const samu_ctx* c, int model) {
+  std::vector<std::pair<int, int>> out;
+  for (int gpus = 1; gpus <= (int)c->eng.n_gpus; ++gpus)
+    for (int t = 1; t <= gpus; t *= 2)
+      if (gpus % t == 0 && plan_blocks(c, model, gpus / t, t) >= 0) out.push_back({gpus / t, t});
+  return out;
+}
+
+// ---------------------------------------------------------------------------------------------
+// C ABI: context
+// ---------------------------------------------------------------------------------------------
+extern "C" samu_status samu_nccl_unique_id(uint8_t out[128]) {
+  if (!out) return SAMU_E_INVALID;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return SAMU_E_NCCL;
+  std::memcpy(out, id.internal, 128);
+  return SAMU_OK;
+}
+
+extern "C" samu_status samu_ctx_create(samu_ctx** out, int32_t cuda_device, void* cuda_stream, int32_t rank,
+                                       int32_t world, const uint8_t* nccl_unique_id) {
+  if (!out) return SAMU_E_INVALID;
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world || (world > 1 && !nccl_unique_id)) return SAMU_E_INVALID;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return SAMU_E_CUDA;
+  if (cuda_device < 0 || cuda_device >= ndev) return SAMU_E_INVALID;
+  samu_ctx* c = new samu_ctx();
+  c->device = cuda_device;
+  c->rank = rank;
+  c->world = world;
+  if (cudaSetDevice(cuda_device) != cudaSuccess) { delete c; return SAMU_E_CUDA; }
+  cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, cuda_device);
+  if (cuda_stream) c->stream = (cudaStream_t)cuda_stream;
+  else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) { delete c; return SAMU_E_CUDA; }
+    c->own_stream = true;
+  }
+  if (world > 1) {
+    ncclUniqueId id;
+    std::memcpy(id.internal, nccl_unique_id, 128);
+    if (ncclCommInitRank(&c->comm, world, id, rank) != ncclSuccess) { delete c; return SAMU_E_NCCL; }
+  }
+  *out = c;
+  return SAMU_OK;
+}
+
+extern "C" void samu_ctx_destroy(samu_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+extern "C" const char* samu_last_error(const samu_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+// ---------------------------------------------------------------------------------------------
+// C ABI: registration
+// ---------------------------------------------------------------------------------------------
+extern "C" samu_status samu_model_register(samu_ctx* c, int32_t model_id, const samu_model_spec* spec,
+                                           int32_t n_buckets, const uint32_t* bucket_B, const double* coeff,
+                                           const double* load_s) {
+  GUARD(c);
+  if (model_id < 0 || model_id >= SAMU_MAX_NODES || !spec || n_buckets < 1 || !bucket_B || !coeff || !load_s)
+    FAIL(c, SAMU_E_INVALID, "model_register: bad arguments");
+  const samu_model_spec& s = *spec;
+  if (s.n_layers < 1 || s.hidden < 1 || s.c < 1 || s.l_max < 1 || s.l_max > 65535 || s.tp_mask == 0 ||
+      (s.tp_mask >> SAMU_N_TP_SLOTS) || s.kv_bytes_per_token < 1)
+    FAIL(c, SAMU_E_INVALID, "model_register: invalid spec");
+  for (int k = 0; k < n_buckets; ++k)
+    if (bucket_B[k] < 1 || (k && bucket_B[k] <= bucket_B[k - 1]))
+      FAIL(c, SAMU_E_INVALID, "model_register: buckets not strictly increasing");
+  // worst-case prefill FLOPs of one iteration must fit u64 (B*s <= 256 * l_max tokens)
+  {
+    const long double lm = (long double)std::max<uint32_t>(s.l_max, 65535u);
+    const long double worst = (long double)s.n_layers * ((long double)s.c * 256.0L * lm + 2.0L * 256.0L * s.hidden * lm * lm);
+    if (worst >= 1.8e19L) FAIL(c, SAMU_E_INVALID, "model_register: FLOPs could overflow u64");
+  }
+  ModelReg& M = c->models[model_id];
+  M.spec = s;
+  M.bucket_B.assign(bucket_B, bucket_B + n_buckets);
+  M.coeff.assign(coeff, coeff + (size_t)SAMU_N_TP_SLOTS * 3 * 2 * n_buckets);
+  M.load.assign(load_s, load_s + (size_t)SAMU_N_TP_SLOTS * SAMU_MAX_DP);
+  M.spec_set = true;
+  c->app_loaded = false;   // tables depend on the engine config: re-derive at app load
+  return SAMU_OK;
+}
+
+extern "C" samu_status samu_ecdf_load(samu_ctx* c, int32_t model_id, const uint32_t* values, const uint32_t* cum,
+                                      int32_t n_points) {
+  GUARD(c);
+  if (model_id < 0 || model_id >= SAMU_MAX_NODES || !values || !cum || n_points < 1)
+    FAIL(c, SAMU_E_INVALID, "ecdf_load: bad arguments");
+  for (int k = 0; k < n_points; ++k) {
+    if ((k && values[k] <= values[k - 1]) || cum[k] < 1 || (k && cum[k] <= cum[k - 1]))
+      FAIL(c, SAMU_E_INVALID, "ecdf_load: knots must be strictly increasing (P:466)");
+  }
+  ModelReg& M = c->models[model_id];
+  M.ev.assign(values, values + n_points);
+  M.ec.assign(cum, cum + n_points);
+  M.ecdf_set = true;
+  c->app_loaded = false;
+  return SAMU_OK;
+}
+
+extern "C" samu_status samu_app_load(samu_ctx* c, const samu_engine_cfg* engine, int32_t n_nodes,
+                                     const int32_t* node_model, int32_t n_req, const samu_request* reqs) {
+  GUARD(c);
+  if (!engine || n_nodes < 1 || n_nodes > SAMU_MAX_NODES || !node_model || n_req < 0 || (n_req && !reqs))
+    FAIL(c, SAMU_E_INVALID, "app_load: bad arguments");
+  const samu_engine_cfg& e = *engine;
+  if (e.max_num_seqs < 1 || e.max_num_seqs > SAMU_MAX_SEQS || e.block_size < 1 || e.block_size > 32 ||
+      e.n_gpus < 1 || e.n_gpus > 16 || e.mem_util_permille > 1000)
+    FAIL(c, SAMU_E_INVALID, "app_load: invalid engine config");
+  c->app_loaded = false;
+  c->eng = e;
+  c->n_nodes = n_nodes;
+  c->n_req = n_req;
+  c->node_model.assign(node_model, node_model + n_nodes);
+  for (int v = 0; v < n_nodes; ++v) {
+    const int m = node_model[v];
+    if (m < 0 || m >= SAMU_MAX_NODES || !c->models[m].spec_set || !c->models[m].ecdf_set)
+      FAIL(c, SAMU_E_INVALID, "app_load: node model not registered or no eCDF");
+  }
+  c->req.assign(reqs, reqs + n_req);
+  c->node_begin.assign(n_nodes, 0);
+  c->node_end.assign(n_nodes, 0);
+  c->node_input.assign(n_nodes, -1);
+  c->succ.assign(n_req, -1);
+  c->cross.assign(n_req, 0);
+  std::vector<int> has_same(n_nodes, 0), has_cross(n_nodes, 0);
+  int last = -1;
+  for (int r = 0; r < n_req; ++r) {
+    const samu_request& q = c->req[r];
+    if (q.node < 0 || q.node >= n_nodes || q.node < last) FAIL(c, SAMU_E_INVALID, "app_load: requests not grouped by ascending node");
+    if (q.node != last) { c->node_begin[q.node] = r; last = q.node; }
+    c->node_end[q.node] = r + 1;
+    const samu_model_spec& M = c->models[node_model[q.node]].spec;
+    if (q.l_in_base > 65535 || q.chain < -1) FAIL(c, SAMU_E_INVALID, "app_load: bad request field");
+    if (q.pred < -1 || q.pred >= r) FAIL(c, SAMU_E_INVALID, "app_load: pred must precede its request");
+    if (q.pred < 0) {
+      if (q.l_in_base > M.l_max) FAIL(c, SAMU_E_INVALID, "app_load: l_in > l_max (S:199)");
+    } else {
+      const samu_request& p = c->req[q.pred];
+      if (p.node == q.node) {
+        if (p.chain != q.chain || q.chain < 0) FAIL(c, SAMU_E_INVALID, "app_load: chain successor must share chain id");
+        if (c->succ[q.pred] >= 0) FAIL(c, SAMU_E_INVALID, "app_load: same-node dependencies must form chains");
+        c->succ[q.pred] = r;
+        has_same[q.node] = 1;
+      } else {
+        if (c->node_input[q.node] >= 0 && c->node_input[q.node] != p.node)
+          FAIL(c, SAMU_E_INVALID, "app_load: a node may depend on one input node only");
+        c->node_input[q.node] = p.node;
+        c->cross[r] = 1;
+        has_cross[q.node] = 1;
+      }
+    }
+  }
+  for (int v = 0; v < n_nodes; ++v)
+    if (has_same[v] && has_cross[v]) FAIL(c, SAMU_E_INVALID, "app_load: node mixes chain and cross-node predecessors");
+  // sampling waves: chains rooted at pred < 0 first, then cross-node requests by node depth
+  std::vector<int> depth(n_nodes, 0);
+  for (int v = 0; v < n_nodes; ++v) if (c->node_input[v] >= 0) depth[v] = depth[c->node_input[v]] + 1;
+  int maxd = 0;
+  for (int v = 0; v < n_nodes; ++v) maxd = std::max(maxd, depth[v]);
+  c->waves.assign(maxd + 1, {});
+  for (int r = 0; r < n_req; ++r) {
+    const samu_request& q = c->req[r];
+    if (q.pred < 0) c->waves[0].push_back(r);
+    else if (c->cross[r]) c->waves[depth[q.node]].push_back(r);
+  }
+  cudaStream_t s = c->stream;
+  std::vector<uint32_t> lib(n_req), cap(n_req);
+  std::vector<int32_t> pred(n_req), nd(n_req);
+  for (int r = 0; r < n_req; ++r) { lib[r] = c->req[r].l_in_base; cap[r] = c->req[r].cap_y; pred[r] = c->req[r].pred; nd[r] = c->req[r].node; }
+  CK(c, upload(c->d_l_in_base, lib, s));
+  CK(c, upload(c->d_cap, cap, s));
+  CK(c, upload(c->d_pred, pred, s));
+  CK(c, upload(c->d_node, nd, s));
+  CK(c, upload(c->d_succ, c->succ, s));
+  CK(c, upload(c->d_cross, c->cross, s));
+  c->d_waves.clear();
+  for (auto& w : c->waves) { c->d_waves.emplace_back(); CK(c, upload(c->d_waves.back(), w, s)); }
+  // eCDF tables (all registered models, packed)
+  std::vector<uint32_t> ev, ec, lmax(n_nodes);
+  std::vector<int32_t> eoff(SAMU_MAX_NODES + 1, 0);
+  for (int m = 0; m < SAMU_MAX_NODES; ++m) {
+    eoff[m] = (int32_t)ev.size();
+    if (c->models[m].ecdf_set) {
+      ev.insert(ev.end(), c->models[m].ev.begin(), c->models[m].ev.end());
+      ec.insert(ec.end(), c->models[m].ec.begin(), c->models[m].ec.end());
+    }
+  }
+  eoff[SAMU_MAX_NODES] = (int32_t)ev.size();
+  for (int v = 0; v < n_nodes; ++v) lmax[v] = c->models[node_model[v]].spec.l_max;
+  CK(c, upload(c->d_ev, ev, s));
+  CK(c, upload(c->d_ec, ec, s));
+  CK(c, upload(c->d_eoff, eoff, s));
+  CK(c, upload(c->d_mnode, c->node_model, s));
+  CK(c, upload(c->d_lmax, lmax, s));
+  // dense coefficient tables for every (model of a node, allowed tp) (reading c11)
+  c->coef.clear();
+  for (int v = 0; v < n_nodes; ++v) {
+    const int m = node_model[v];
+    const ModelReg& M = c->models[m];
+    for (int slot = 0; slot < SAMU_N_TP_SLOTS; ++slot) {
+      if (!((M.spec.tp_mask >> slot) & 1u) || c->coef.count({m, slot})) continue;
+      const int nb = (int)M.bucket_B.size();
+      DevBuf bb, cs;
+      CK(c, upload(bb, M.bucket_B, s));
+      std::vector<double> part(M.coeff.begin() + (size_t)slot * 6 * nb, M.coeff.begin() + (size_t)(slot + 1) * 6 * nb);
+      CK(c, upload(cs, part, s));
+      DevBuf& out = c->coef[{m, slot}];
+      CK(c, out.ensure(sizeof(double) * 6 * e.max_num_seqs));
+      CK(c, launch_dense_coeff(bb.as<uint32_t>(), nb, cs.as<double>(), e.max_num_seqs, out.as<double>(), s));
+      CK(c, cudaStreamSynchronize(s));
+    }
+  }
+  c->rep.clear();
+  c->rep_off_host.clear();
+  c->app_loaded = true;
+  return SAMU_OK;
+}
+
+static DevApp dev_app(const samu_ctx* c) {
+  DevApp a;
+  a.n_req = c->n_req;
+  a.n_nodes = c->n_nodes;
+  a.l_in_base = c->d_l_in_base.as<uint32_t>();
+  a.cap_y = c->d_cap.as<uint32_t>();
+  a.pred = c->d_pred.as<int32_t>();
+  a.node = c->d_node.as<int32_t>();
+  a.succ = c->d_succ.as<int32_t>();
+  a.cross = c->d_cross.as<uint8_t>();
+  return a;
+}
+
+// requests of `node` grouped by dp replica (c13): key = chain id if >= 0 else index within node
+static samu_status replicas(samu_ctx* c, int node, int dp, const uint32_t** off, const uint32_t** lst) {
+  auto key = std::make_pair(node, dp);
+  auto it = c->rep.find(key);
+  if (it == c->rep.end()) {
+    std::vector<std::vector<uint32_t>> L(dp);
+    for (int r = c->node_begin[node]; r < c->node_end[node]; ++r) {
+      const int kk = c->req[r].chain >= 0 ? c->req[r].chain : r - c->node_begin[node];
+      L[kk % dp].push_back((uint32_t)r);
+    }
+    std::vector<uint32_t> o(dp + 1, 0), l;
+    for (int j = 0; j < dp; ++j) { o[j + 1] = o[j] + (uint32_t)L[j].size(); l.insert(l.end(), L[j].begin(), L[j].end()); }
+    auto& pr = c->rep[key];
+    CK(c, upload(pr.first, o, c->stream));
+    CK(c, upload(pr.second, l, c->stream));
+    c->rep_off_host[key] = o;
+    it = c->rep.find(key);
+  }
+  *off = it->second.first.as<uint32_t>();
+  *lst = it->second.second.as<uint32_t>();
+  return SAMU_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// sampling
+// ---------------------------------------------------------------------------------------------
+extern "C" samu_status samu_sample_lengths(samu_ctx* c, uint64_t seed, int32_t trial_begin, int32_t n_trials,
+                                           uint16_t* out_l_out, uint16_t* out_l_in_eff) {
+  GUARD(c);
+  if (!c->app_loaded) FAIL(c, SAMU_E_INVALID, "sample_lengths: no app loaded");
+  if (n_trials < 0 || trial_begin < 0 || (n_trials && (!out_l_out || !out_l_in_eff)))
+    FAIL(c, SAMU_E_INVALID, "sample_lengths: bad arguments");
+  if (n_trials > 65535) FAIL(c, SAMU_E_INVALID, "sample_lengths: at most 65535 trials per call");
+  DevApp a = dev_app(c);
+  DevEcdf e;
+  e.values = c->d_ev.as<uint32_t>();
+  e.cum = c->d_ec.as<uint32_t>();
+  e.off = c->d_eoff.as<int32_t>();
+  e.model_of_node = c->d_mnode.as<int32_t>();
+  e.l_max_of_node = c->d_lmax.as<uint32_t>();
+  for (size_t w = 0; w < c->waves.size(); ++w)
+    CK(c, launch_sample(a, e, c->d_waves[w].as<int32_t>(), (int32_t)c->waves[w].size(), seed, trial_begin, n_trials,
+                        out_l_out, out_l_in_eff, c->stream));
+  return SAMU_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// batched simulation (internal form used by samu_simulate_batch and the greedy)
+// ---------------------------------------------------------------------------------------------
+struct SimJob {
+  samu_candidate cand;
+  int phase = 0;                       // dependency depth inside the batch
+  const double* src_fin = nullptr;     // [T][n]
+  const double* tau = nullptr;         // [T]
+  const samu_trial_rec* tau_rec = nullptr;
+  double* fin_t_out = nullptr;         // [T][n]
+  uint32_t* fin_iter_out = nullptr;    // [T][n]
+  samu_trial_rec* out_rec = nullptr;   // [T]
+};
+
+struct StatePtrs {
+  uint32_t* st = nullptr;
+  uint16_t* g = nullptr;
+  double* fin_t = nullptr;
+  double* over = nullptr;
+};
+
+static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16_t* l_out, const uint16_t* l_in,
+                            int32_t T, const StatePtrs& S) {
+  if (jobs.empty() || T == 0) return SAMU_OK;
+  cudaStream_t s = c->stream;
+  int max_phase = 0;
+  for (auto& j : jobs) max_phase = std::max(max_phase, j.phase);
+  if (!c->sim_blocks_per_sm) {
+    int bpsm = 0;
+    CK(c, simulate_prepare(&bpsm));
+    if (bpsm < 1) FAIL(c, SAMU_E_CUDA, "simulate: kernel does not fit on an SM");
+    c->sim_blocks_per_sm = bpsm;
+  }
+  CK(c, c->d_error.ensure(sizeof(int32_t)));
+  CK(c, cudaMemsetAsync(c->d_error.p, 0, sizeof(int32_t), s));
+  for (int ph = 0; ph <= max_phase; ++ph) {
+    std::vector<int> idx;
+    for (int i = 0; i < (int)jobs.size(); ++i) if (jobs[i].phase == ph) idx.push_back(i);
+    if (idx.empty()) continue;
+    std::vector<DevCand> dc(idx.size());
+    std::vector<uint64_t> cost(idx.size());
+    uint32_t max_q = 1, max_p = 1;
+    for (size_t x = 0; x < idx.size(); ++x) {
+      const SimJob& J = jobs[idx[x]];
+      const samu_candidate& cd = J.cand;
+      const int node = cd.node, model = c->node_model[node];
+      const ModelReg& M = c->models[model];
+      const int64_t blocks = plan_blocks(c, model, cd.dp, cd.tp);
+      if (blocks < 0) FAIL(c, SAMU_E_INVALID, "simulate: invalid plan for the node's model");
+      DevCand& D = dc[x];
+      D.node = node; D.dp = cd.dp; D.tp = cd.tp; D.resume = cd.resume ? 1 : 0; D.commit = cd.commit ? 1 : 0; D.src = -1;
+      D.max_seqs = c->eng.max_num_seqs;
+      D.bs = c->eng.block_size;
+      D.budget = std::max(M.spec.l_max, c->eng.min_batched_tokens);
+      D.blocks = (int32_t)blocks;
+      D.L = M.spec.n_layers;
+      D.h_tp = M.spec.hidden / (uint32_t)cd.tp;
+      D.c = M.spec.c;
+      const int slot = log2_exact((uint32_t)cd.tp);
+      D.load_s = M.load[(size_t)slot * SAMU_MAX_DP + (cd.dp - 1)];
+      D.coef = c->coef.at({model, slot}).as<double>();
+      RET(replicas(c, node, cd.dp, &D.rep_off, &D.rep_req));
+      D.src_fin = J.src_fin;
+      D.tau = J.tau;
+      D.tau_rec = J.tau_rec;
+      D.fin_t_out = J.fin_t_out;
+      D.fin_iter_out = J.fin_iter_out;
+      const std::vector<uint32_t>& ho = c->rep_off_host.at({node, cd.dp});
+      uint32_t mx = 0;
+      for (int j = 0; j < cd.dp; ++j) mx = std::max(mx, ho[j + 1] - ho[j]);
+      max_q = std::max(max_q, mx);
+      if (c->node_input[node] >= 0) max_p = std::max(max_p, mx);
+      cost[x] = mx;
+    }
+    // longest-first work items (cand, trial, replica)
+    std::vector<int> order(idx.size());
+    for (size_t x = 0; x < idx.size(); ++x) order[x] = (int)x;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+    std::vector<uint2> items;
+    for (int x : order)
+      for (int k = 0; k < T; ++k)
+        for (int j = 0; j < dc[x].dp; ++j) items.push_back(make_uint2((uint32_t)x, ((uint32_t)k << 4) | (uint32_t)j));
+    CK(c, upload(c->d_cands, dc, s));
+    CK(c, upload(c->d_items, items, s));
+    CK(c, c->d_counter.ensure(sizeof(uint32_t)));
+    CK(c, cudaMemsetAsync(c->d_counter.p, 0, sizeof(uint32_t), s));
+    CK(c, c->d_rep_rec.ensure(sizeof(samu_trial_rec) * 16 * idx.size() * T));
+    const int bpsm = c->sim_blocks_per_sm;
+    const int64_t warps_needed = (int64_t)items.size();
+    int n_blocks = (int)std::min<int64_t>((int64_t)c->n_sm * bpsm, (warps_needed + SAMU_WARPS_PER_BLOCK - 1) / SAMU_WARPS_PER_BLOCK);
+    n_blocks = std::max(n_blocks, 1);
+    const size_t n_warps = (size_t)n_blocks * SAMU_WARPS_PER_BLOCK;
+    CK(c, c->d_scratch_q.ensure(sizeof(uint32_t) * n_warps * max_q));
+    CK(c, c->d_scratch_key.ensure(sizeof(uint64_t) * n_warps * 2 * max_p));
+    CK(c, c->d_scratch_idx.ensure(sizeof(uint32_t) * n_warps * 2 * max_p));
+    SimLaunch L;
+    L.app = dev_app(c);
+    L.cands = c->d_cands.as<DevCand>();
+    L.n_cands = (int32_t)idx.size();
+    L.n_trials = T;
+    L.items = c->d_items.as<uint2>();
+    L.n_items = (int32_t)items.size();
+    L.next_item = c->d_counter.as<uint32_t>();
+    L.l_out = l_out;
+    L.l_in = l_in;
+    L.st = S.st;
+    L.g = S.g;
+    L.fin_t = S.fin_t;
+    L.over = S.over;
+    L.rep_rec = c->d_rep_rec.as<samu_trial_rec>();
+    L.scratch_q = c->d_scratch_q.as<uint32_t>();
+    L.scratch_key = c->d_scratch_key.as<uint64_t>();
+    L.scratch_idx = c->d_scratch_idx.as<uint32_t>();
+    L.max_q = (int32_t)max_q;
+    L.max_p = (int32_t)max_p;
+    L.error = c->d_error.as<int32_t>();
+    CK(c, launch_simulate(L, n_blocks, s));
+    // combine replicas into the per-(candidate, trial) records
+    for (size_t x = 0; x < idx.size(); ++x) {
+      CK(c, launch_combine(L.rep_rec + x * T * 16, L.cands + x, 1, T, jobs[idx[x]].out_rec, S.over, c->n_nodes, s));
+    }
+    c->n_sims += (int64_t)idx.size() * T;
+    int32_t herr = 0;
+    CK(c, cudaMemcpyAsync(&herr, c->d_error.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CK(c, cudaStreamSynchronize(s));
+    if (herr) FAIL(c, herr, herr == SAMU_E_INFEASIBLE ? "simulate: capacity below one sequence"
+                                                   : "simulate: inconsistent WorkloadState / scratch overflow");
+  }
+  return SAMU_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// trial sharding: rank r owns trials [begin, begin + count) of T (contiguous blocks)
+// ---------------------------------------------------------------------------------------------
+static void trial_share(int T, int world, int rank, int* begin, int* count) {
+  const int base = T / world, rem = T % world;
+  *count = base + (rank < rem ? 1 : 0);
+  *begin = rank * base + std::min(rank, rem);
+}
+
+// all-gather per-(job, local trial) records [n][T_local] into rows of `dst` ([*][T]) at `slots`
+static samu_status gather_records(samu_ctx* c, const samu_trial_rec* local, int n, int T, samu_trial_rec* dst,
+                                  const std::vector<int>& slots) {
+  cudaStream_t s = c->stream;
+  if (n == 0) return SAMU_OK;
+  if (c->world == 1) {
+    for (int x = 0; x < n; ++x)
+      if (dst + (size_t)slots[x] * T != local + (size_t)x * T)
+        CK(c, cudaMemcpyAsync(dst + (size_t)slots[x] * T, local + (size_t)x * T, sizeof(samu_trial_rec) * T,
+                              cudaMemcpyDeviceToDevice, s));
+    return SAMU_OK;
+  }
+  int b0, cnt0;
+  trial_share(T, c->world, c->rank, &b0, &cnt0);
+  const int Tmax = (T + c->world - 1) / c->world;
+  const size_t row = sizeof(samu_trial_rec) * Tmax;
+  CK(c, c->d_gather_send.ensure(row * n));
+  CK(c, c->d_gather_recv.ensure(row * n * c->world));
+  CK(c, cudaMemsetAsync(c->d_gather_send.p, 0, row * n, s));
+  CK(c, cudaMemcpy2DAsync(c->d_gather_send.p, row, local, sizeof(samu_trial_rec) * cnt0, sizeof(samu_trial_rec) * cnt0, n,
+                          cudaMemcpyDeviceToDevice, s));
+  CKN(c, ncclAllGather(c->d_gather_send.p, c->d_gather_recv.p, row * n, ncclUint8, c->comm, s));
+  for (int w = 0; w < c->world; ++w) {
+    int bw, cw;
+    trial_share(T, c->world, w, &bw, &cw);
+    if (!cw) continue;
+    const samu_trial_rec* src = c->d_gather_recv.as<samu_trial_rec>() + (size_t)w * n * Tmax;
+    for (int x = 0; x < n; ++x)
+      CK(c, cudaMemcpyAsync(dst + (size_t)slots[x] * T + bw, src + (size_t)x * Tmax, sizeof(samu_trial_rec) * cw,
+                            cudaMemcpyDeviceToDevice, s));
+  }
+  return SAMU_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// C ABI: samu_simulate_batch
+// ---------------------------------------------------------------------------------------------
+extern "C" samu_status samu_simulate_batch(samu_ctx* c, const samu_candidate* cands, int32_t n_cands,
+                                           const uint16_t* l_out, const uint16_t* l_in_eff, int32_t n_trials,
+                                           uint32_t* st, uint16_t* g, double* fin_t, double* overshoot,
+                                           const double* time_limit, samu_trial_rec* out_recs,
+                                           samu_cand_summary* out_summary, uint32_t* out_fin_iter,
+                                           double* out_fin_t) {
+  GUARD(c);
+  if (!c->app_loaded) FAIL(c, SAMU_E_INVALID, "simulate_batch: no app loaded");
+  if (n_cands < 0 || (n_cands && !cands) || n_trials < 0 || (n_trials && (!l_out || !l_in_eff)) || !out_recs)
+    FAIL(c, SAMU_E_INVALID, "simulate_batch: bad arguments");
+  if (n_trials >= (1 << 27)) FAIL(c, SAMU_E_INVALID, "simulate_batch: too many trials");
+  const bool has_state = st != nullptr;
+  if (has_state && (!g || !fin_t || !overshoot)) FAIL(c, SAMU_E_INVALID, "simulate_batch: partial state");
+  const size_t n = (size_t)c->n_req;
+  std::vector<SimJob> jobs(n_cands);
+  std::vector<int> commit_nodes;
+  std::vector<DevBuf> own_fin;
+  std::vector<int> needs_fin(n_cands, 0);
+  for (int i = 0; i < n_cands; ++i) {
+    const samu_candidate& cd = cands[i];
+    if (cd.node < 0 || cd.node >= c->n_nodes) FAIL(c, SAMU_E_INVALID, "simulate_batch: bad node");
+    if (plan_blocks(c, c->node_model[cd.node], cd.dp, cd.tp) < 0) FAIL(c, SAMU_E_INVALID, "simulate_batch: invalid plan");
+    if (cd.dep_src >= 0) {
+      if (cd.dep_src >= i || cands[cd.dep_src].node != c->node_input[cd.node])
+        FAIL(c, SAMU_E_INVALID, "simulate_batch: dep_src must be an earlier candidate of the node's input node");
+      needs_fin[cd.dep_src] = 1;
+    }
+    if (cd.commit) {
+      if (!has_state) FAIL(c, SAMU_E_INVALID, "simulate_batch: commit needs a WorkloadState");
+      if (std::find(commit_nodes.begin(), commit_nodes.end(), cd.node) != commit_nodes.end())
+        FAIL(c, SAMU_E_INVALID, "simulate_batch: two committing candidates for one node");
+      commit_nodes.push_back(cd.node);
+    }
+  }
+  for (int i = 0; i < n_cands; ++i) {
+    SimJob& J = jobs[i];
+    J.cand = cands[i];
+    J.phase = cands[i].dep_src >= 0 ? jobs[cands[i].dep_src].phase + 1 : 0;
+    J.tau = time_limit ? time_limit + (size_t)i * n_trials : nullptr;
+    J.out_rec = out_recs + (size_t)i * n_trials;
+    J.fin_iter_out = out_fin_iter ? out_fin_iter + (size_t)i * n_trials * n : nullptr;
+    if (out_fin_t) J.fin_t_out = out_fin_t + (size_t)i * n_trials * n;
+    else if (needs_fin[i]) {
+      own_fin.emplace_back();
+      CK(c, own_fin.back().ensure(sizeof(double) * n_trials * n));
+      J.fin_t_out = own_fin.back().as<double>();
+    }
+    if (out_fin_iter) CK(c, cudaMemsetAsync(J.fin_iter_out, 0xFF, sizeof(uint32_t) * n_trials * n, c->stream));
+    if (J.fin_t_out) {
+      std::vector<double> inf((size_t)n_trials * n, std::numeric_limits<double>::infinity());
+      CK(c, cudaMemcpyAsync(J.fin_t_out, inf.data(), sizeof(double) * inf.size(), cudaMemcpyHostToDevice, c->stream));
+      CK(c, cudaStreamSynchronize(c->stream));
+    }
+  }
+  for (int i = 0; i < n_cands; ++i)
+    if (cands[i].dep_src >= 0) jobs[i].src_fin = jobs[cands[i].dep_src].fin_t_out;
+  StatePtrs S{st, g, fin_t, overshoot};
+  RET(run_jobs(c, jobs, l_out, l_in_eff, n_trials, S));
+  if (out_summary && n_cands) {
+    int T_total = n_trials;
+    const samu_trial_rec* all = out_recs;
+    if (c->world > 1) {
+      // every rank holds n_trials local trials; the world total is their sum
+      int32_t Tl = n_trials, Tsum = 0;
+      DevBuf tmp;
+      CK(c, tmp.ensure(sizeof(int32_t) * 2));
+      CK(c, cudaMemcpyAsync(tmp.p, &Tl, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+      CKN(c, ncclAllReduce(tmp.p, tmp.as<int32_t>() + 1, 1, ncclInt32, ncclSum, c->comm, c->stream));
+      CK(c, cudaMemcpyAsync(&Tsum, tmp.as<int32_t>() + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+      CK(c, cudaStreamSynchronize(c->stream));
+      int b, cnt;
+      trial_share(Tsum, c->world, c->rank, &b, &cnt);
+      if (cnt != n_trials) FAIL(c, SAMU_E_INVALID, "simulate_batch: local trial count must follow the contiguous split");
+      T_total = Tsum;
+      CK(c, c->d_sum.ensure(sizeof(samu_trial_rec) * (size_t)n_cands * T_total));
+      std::vector<int> slots(n_cands);
+      for (int i = 0; i < n_cands; ++i) slots[i] = i;
+      RET(gather_records(c, out_recs, n_cands, T_total, c->d_sum.as<samu_trial_rec>(), slots));
+      all = c->d_sum.as<samu_trial_rec>();
+    }
+    DevBuf dsum;
+    CK(c, dsum.ensure(sizeof(samu_cand_summary) * n_cands));
+    CK(c, launch_summary(all, n_cands, T_total, dsum.as<samu_cand_summary>(), c->stream));
+    CK(c, cudaMemcpyAsync(out_summary, dsum.p, sizeof(samu_cand_summary) * n_cands, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+  }
+  return SAMU_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// C ABI: samu_plan_greedy — Algorithm 1 with the device estimator
+// ---------------------------------------------------------------------------------------------
+namespace {
+
+struct Ent {
+  int node, dp, tp;
+  bool operator==(const Ent& o) const { return node == o.node && dp == o.dp && tp == o.tp; }
+};
+
+struct Greedy {
+  samu_ctx* c;
+  int T = 0, Tl = 0, tb = 0;
+  size_t n = 0;
+  DevBuf lo, li, st, g, fin_t, over;
+  StatePtrs S;
+  std::vector<Ent> prev;
+  // per-stage caches of simulations: records [slot][T] (all trials), finish-time buffers
+  DevBuf cache, local_rec, d_sc, d_out, d_best, d_any;
+  int cap_slots = 0, n_slots = 0;
+  std::map<std::vector<int>, int> full_slot, cut_slot;
+  std::map<int, DevBuf> fin_buf;           // full slot -> [Tl][n] finish times (dependency sources)
+  std::map<int, int> pending_phase;        // slot -> phase within the pending batch
+  std::vector<SimJob> pending;
+  std::vector<int> pending_slots;
+  std::vector<int> pending_tau;            // f* full slot whose records give tau, or -1
+  int64_t evals = 0;
+  std::vector<bool> is_input;
+
+  bool resumes(const Ent& e) const {
+    for (const Ent& x : prev) if (x == e) return true;
+    return false;
+  }
+  std::vector<int> key_of(const Ent& e, const std::vector<Ent>& E) const {
+    std::vector<int> k{e.node, e.dp, e.tp, resumes(e) ? 1 : 0};
+    const int src = c->node_input[e.node];
+    if (src >= 0)
+      for (const Ent& x : E)
+        if (x.node == src) { auto ks = key_of(x, E); k.insert(k.end(), ks.begin(), ks.end()); }
+    return k;
+  }
+  samu_status grow(int need) {
+    if (need <= cap_slots) return SAMU_OK;
+    int nc = std::max(need, std::max(64, cap_slots * 2));
+    DevBuf nb;
+    CK(c, nb.ensure(sizeof(samu_trial_rec) * (size_t)nc * T));
+    if (n_slots) CK(c, cudaMemcpyAsync(nb.p, cache.p, sizeof(samu_trial_rec) * (size_t)n_slots * T, cudaMemcpyDeviceToDevice, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    cache = std::move(nb);
+    cap_slots = nc;
+    return SAMU_OK;
+  }
+  samu_trial_rec* rec(int slot) { return cache.as<samu_trial_rec>() + (size_t)slot * T; }
+
+  samu_status ensure_full(const Ent& e, const std::vector<Ent>& E, int* out_slot) {
+    auto key = key_of(e, E);
+    auto it = full_slot.find(key);
+    if (it != full_slot.end()) { *out_slot = it->second; return SAMU_OK; }
+    const double* sf = nullptr;
+    int phase = 0;
+    const int src = c->node_input[e.node];
+    if (src >= 0)
+      for (const Ent& x : E)
+        if (x.node == src) {
+          int ss;
+          RET(ensure_full(x, E, &ss));
+          sf = fin_buf.at(ss).as<double>();
+          auto pp = pending_phase.find(ss);
+          if (pp != pending_phase.end()) phase = pp->second + 1;
+        }
+    const int slot = n_slots++;
+    RET(grow(n_slots));
+    full_slot[key] = slot;
+    SimJob J;
+    J.cand = samu_candidate{e.node, e.dp, e.tp, resumes(e) ? 1 : 0, -1, 0};
+    J.phase = phase;
+    J.src_fin = sf;
+    if (is_input[e.node]) {
+      DevBuf& fb = fin_buf[slot];
+      CK(c, fb.ensure(sizeof(double) * (size_t)Tl * n));
+      J.fin_t_out = fb.as<double>();
+    }
+    pending.push_back(J);
+    pending_slots.push_back(slot);
+    pending_tau.push_back(-1);
+    pending_phase[slot] = phase;
+    *out_slot = slot;
+    return SAMU_OK;
+  }
+  samu_status ensure_cut(const Ent& e, const Ent& f, const std::vector<Ent>& E, int fslot, int* out_slot) {
+    auto key = key_of(e, E);
+    auto kf = key_of(f, E);
+    key.push_back(-1);
+    key.insert(key.end(), kf.begin(), kf.end());
+    auto it = cut_slot.find(key);
+    if (it != cut_slot.end()) { *out_slot = it->second; return SAMU_OK; }
+    const double* sf = nullptr;
+    const int src = c->node_input[e.node];
+    if (src >= 0)
+      for (const Ent& x : E)
+        if (x.node == src) { int ss; RET(ensure_full(x, E, &ss)); sf = fin_buf.at(ss).as<double>(); }
+    const int slot = n_slots++;
+    RET(grow(n_slots));
+    cut_slot[key] = slot;
+    SimJob J;
+    J.cand = samu_candidate{e.node, e.dp, e.tp, resumes(e) ? 1 : 0, -1, 0};
+    J.phase = 0;
+    J.src_fin = sf;
+    pending.push_back(J);             // tau_k = T_f*^(k) (this rank's trials), resolved at flush
+    pending_slots.push_back(slot);
+    pending_tau.push_back(fslot);
+    *out_slot = slot;
+    return SAMU_OK;
+  }
+  // run the pending simulations, then all-gather their records into the cache
+  samu_status flush() {
+    if (pending.empty()) return SAMU_OK;
+    // the cache may have been reallocated after tau_rec pointers were taken: re-point them
+    CK(c, local_rec.ensure(sizeof(samu_trial_rec) * pending.size() * std::max(Tl, 1)));
+    for (size_t x = 0; x < pending.size(); ++x) {
+      pending[x].out_rec = (c->world == 1) ? rec(pending_slots[x]) : local_rec.as<samu_trial_rec>() + x * Tl;
+      pending[x].tau_rec = pending_tau[x] >= 0 ? rec(pending_tau[x]) + tb : nullptr;
+      if (pending[x].fin_t_out) {
+        std::vector<double> inf((size_t)Tl * n, std::numeric_limits<double>::infinity());
+        CK(c, cudaMemcpyAsync(pending[x].fin_t_out, inf.data(), sizeof(double) * inf.size(), cudaMemcpyHostToDevice, c->stream));
+        CK(c, cudaStreamSynchronize(c->stream));
+      }
+    }
+    RET(run_jobs(c, pending, lo.as<uint16_t>(), li.as<uint16_t>(), Tl, S));
+    if (c->world > 1) RET(gather_records(c, local_rec.as<samu_trial_rec>(), (int)pending.size(), T, cache.as<samu_trial_rec>(), pending_slots));
+    pending.clear();
+    pending_slots.clear();
+    pending_tau.clear();
+    pending_phase.clear();
+    return SAMU_OK;
+  }
+
+  samu_status run(uint64_t seed, int T_total, samu_plan* plan) {
+    T = T_total;
+    n = (size_t)c->n_req;
+    trial_share(T, c->world, c->rank, &tb, &Tl);
+    cudaStream_t s = c->stream;
+    is_input.assign(c->n_nodes, false);
+    for (int v = 0; v < c->n_nodes; ++v) if (c->node_input[v] >= 0) is_input[c->node_input[v]] = true;
+    const size_t tn = (size_t)std::max(Tl, 1) * n;
+    CK(c, lo.ensure(sizeof(uint16_t) * tn));
+    CK(c, li.ensure(sizeof(uint16_t) * tn));
+    CK(c, st.ensure(sizeof(uint32_t) * tn));
+    CK(c, g.ensure(sizeof(uint16_t) * tn));
+    CK(c, fin_t.ensure(sizeof(double) * tn));
+    CK(c, over.ensure(sizeof(double) * (size_t)std::max(Tl, 1) * c->n_nodes * 16));
+    CK(c, cudaMemsetAsync(st.p, 0, sizeof(uint32_t) * tn, s));
+    CK(c, cudaMemsetAsync(g.p, 0, sizeof(uint16_t) * tn, s));
+    CK(c, cudaMemsetAsync(over.p, 0, sizeof(double) * (size_t)std::max(Tl, 1) * c->n_nodes * 16, s));
+    {
+      std::vector<double> inf(tn, std::numeric_limits<double>::infinity());
+      CK(c, cudaMemcpyAsync(fin_t.p, inf.data(), sizeof(double) * tn, cudaMemcpyHostToDevice, s));
+    }
+    if (Tl) RET(samu_sample_lengths(c, seed, tb, Tl, lo.as<uint16_t>(), li.as<uint16_t>()));
+    S = StatePtrs{st.as<uint32_t>(), g.as<uint16_t>(), fin_t.as<double>(), over.as<double>()};
+    CK(c, d_best.ensure(sizeof(int32_t) + sizeof(double)));
+    CK(c, d_any.ensure(sizeof(int32_t) * (size_t)c->n_nodes * std::max(Tl, 1) + 2 * sizeof(int32_t) * SAMU_MAX_NODES));
+    std::vector<std::vector<std::pair<int, int>>> plans(c->n_nodes);
+    for (int v = 0; v < c->n_nodes; ++v) plans[v] = plans_of(c, c->node_model[v]);
+    std::memset(plan, 0, sizeof(*plan));
+    const int N = (int)c->eng.n_gpus;
+    for (;;) {
+      // unfinished nodes (in any trial of any rank)
+      std::vector<int> undone(c->n_nodes, 0);
+      RET(node_status(undone));
+      std::vector<int> unfinished;
+      for (int v = 0; v < c->n_nodes; ++v) if (undone[v]) unfinished.push_back(v);
+      if (unfinished.empty()) break;
+      if (plan->n_stages >= 64) FAIL(c, SAMU_E_STATE, "plan_greedy: too many stages");
+      full_slot.clear(); cut_slot.clear(); fin_buf.clear(); n_slots = 0;
+      std::vector<Ent> Es;
+      double TE_star = 0.0;
+      StageOut chosen{};
+      for (;;) {
+        std::vector<int> ready;
+        for (int v : unfinished) {
+          const int u = c->node_input[v];
+          bool ok = u < 0 || !undone[u];
+          for (const Ent& e : Es) if (e.node == u) ok = true;
+          if (ok) ready.push_back(v);
+        }
+        struct Cand { std::vector<Ent> E; Ent P; };
+        std::vector<Cand> cands;
+        int g_star = 0;
+        for (const Ent& e : Es) g_star += e.dp * e.tp;
+        for (int v : ready)
+          for (auto& pl : plans[v]) {
+            Ent P{v, pl.first, pl.second};
+            int prime = -1;
+            for (size_t i = 0; i < Es.size(); ++i) if (Es[i].node == v) prime = (int)i;
+            std::vector<Ent> E = Es;
+            int gE = 0;
+            if (prime >= 0) {
+              E[prime] = P;
+              for (const Ent& x : E) gE += x.dp * x.tp;
+              if (!(g_star < gE && gE <= N)) continue;      // Alg. 1 line 11
+            } else {
+              E.push_back(P);
+              for (const Ent& x : E) gE += x.dp * x.tp;
+              if (gE > N) continue;                          // Alg. 1 line 14
+            }
+            std::sort(E.begin(), E.end(), [](const Ent& a, const Ent& b) { return a.node < b.node; });
+            cands.push_back({E, P});
+          }
+        if (cands.empty()) break;
+        const int nc = (int)cands.size();
+        std::vector<StageCand> sc(nc);
+        for (int x = 0; x < nc; ++x) {
+          StageCand& q = sc[x];
+          std::memset(&q, 0, sizeof(q));
+          q.n_entries = (int)cands[x].E.size();
+          q.gpus = 0;
+          for (int i = 0; i < q.n_entries; ++i) {
+            const Ent& e = cands[x].E[i];
+            RET(ensure_full(e, cands[x].E, &q.full_slot[i]));
+            q.node[i] = e.node;
+            q.cut_slot[i] = -1;
+            q.gpus += e.dp * e.tp;
+          }
+          q.changed_node = cands[x].P.node;
+          q.changed_dp = cands[x].P.dp;
+          q.changed_tp = cands[x].P.tp;
+        }
+        RET(flush());
+        CK(c, upload(d_sc, sc, s));
+        CK(c, d_out.ensure(sizeof(StageOut) * nc));
+        CK(c, launch_fstar(cache.as<samu_trial_rec>(), T, d_sc.as<StageCand>(), nc, d_out.as<StageOut>(), s));
+        std::vector<StageOut> so(nc);
+        CK(c, cudaMemcpyAsync(so.data(), d_out.p, sizeof(StageOut) * nc, cudaMemcpyDeviceToHost, s));
+        CK(c, cudaStreamSynchronize(s));
+        for (int x = 0; x < nc; ++x) {
+          const int f = so[x].fstar;
+          for (int i = 0; i < sc[x].n_entries; ++i)
+            if (i != f) RET(ensure_cut(cands[x].E[i], cands[x].E[f], cands[x].E, sc[x].full_slot[f], &sc[x].cut_slot[i]));
+        }
+        RET(flush());
+        CK(c, upload(d_sc, sc, s));
+        CK(c, launch_stage_score(cache.as<samu_trial_rec>(), T, d_sc.as<StageCand>(), nc, d_out.as<StageOut>(), TE_star,
+                                 g_star, d_best.as<int32_t>(), reinterpret_cast<double*>(d_best.as<char>() + 8), s));
+        evals += nc;
+        int32_t best = -1;
+        double maxdT = 0.0;
+        CK(c, cudaMemcpyAsync(&best, d_best.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        CK(c, cudaMemcpyAsync(&maxdT, d_best.as<char>() + 8, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(c, cudaMemcpyAsync(so.data(), d_out.p, sizeof(StageOut) * nc, cudaMemcpyDeviceToHost, s));
+        CK(c, cudaStreamSynchronize(s));
+        if (maxdT < 0.0) break;                               // Alg. 1 line 19
+        Es = cands[best].E;
+        TE_star = so[best].TE;
+        chosen = so[best];
+      }
+      if (Es.empty()) FAIL(c, SAMU_E_INFEASIBLE, "plan_greedy: no ready model fits an empty stage");
+      evals += 1;   // the stage is scored once more at commit (oracle parity of the counter)
+      // commit (Alg. 1 lines 24-25): f* to completion, the others cut at t_E^(k), state carried
+      const int f = chosen.fstar;
+      int fslot = -1;
+      RET(ensure_full(Es[f], Es, &fslot));
+      std::vector<SimJob> jobs;
+      CK(c, local_rec.ensure(sizeof(samu_trial_rec) * Es.size() * std::max(Tl, 1)));
+      for (size_t i = 0; i < Es.size(); ++i) {
+        const Ent& e = Es[i];
+        SimJob J;
+        J.cand = samu_candidate{e.node, e.dp, e.tp, resumes(e) ? 1 : 0, -1, 1};
+        J.phase = 0;
+        const int src = c->node_input[e.node];
+        for (size_t q = 0; q < Es.size(); ++q)
+          if (Es[q].node == src) {
+            int ss;
+            RET(ensure_full(Es[q], Es, &ss));
+            J.src_fin = fin_buf.at(ss).as<double>();
+            J.phase = 1;
+          }
+        J.tau_rec = ((int)i == f) ? nullptr : rec(fslot) + tb;
+        J.out_rec = local_rec.as<samu_trial_rec>() + i * Tl;
+        jobs.push_back(J);
+      }
+      RET(flush());
+      // depth > 1 chains of dependencies commit in topological (node id) order
+      for (size_t i = 0; i < jobs.size(); ++i) {
+        int d = 0, v = Es[i].node;
+        while (c->node_input[v] >= 0) { ++d; v = c->node_input[v]; }
+        jobs[i].phase = d;
+      }
+      RET(run_jobs(c, jobs, lo.as<uint16_t>(), li.as<uint16_t>(), Tl, S));
+      CK(c, launch_rebase(st.as<uint32_t>(), fin_t.as<double>(), (int64_t)Tl * n, rec(fslot) + tb, (int32_t)n, s));
+      samu_plan_stage& PS = plan->stages[plan->n_stages++];
+      PS.n_entries = (int)Es.size();
+      for (size_t i = 0; i < Es.size(); ++i) { PS.node[i] = Es[i].node; PS.dp[i] = Es[i].dp; PS.tp[i] = Es[i].tp; }
+      PS.fstar = Es[f].node;
+      PS.mean_tE = chosen.mean_tE;
+      PS.T_E = chosen.TE;
+      plan->total += chosen.mean_tE;
+      prev = Es;
+    }
+    plan->n_cand_evals = evals;
+    return SAMU_OK;
+  }
+
+  // undone[v] = 1 if node v has an unfinished request in any trial (OR over ranks)
+  samu_status node_status(std::vector<int>& undone) {
+    cudaStream_t s = c->stream;
+    int32_t* any = d_any.as<int32_t>();
+    int32_t* red = any + (size_t)c->n_nodes * std::max(Tl, 1);
+    std::vector<int32_t> h((size_t)c->n_nodes * std::max(Tl, 1), 0), flag(c->n_nodes, 0);
+    if (Tl) {
+      CK(c, launch_node_done(st.as<uint32_t>(), Tl, (int32_t)n, c->d_node.as<int32_t>(), any, c->n_nodes, s));
+      CK(c, cudaMemcpyAsync(h.data(), any, sizeof(int32_t) * h.size(), cudaMemcpyDeviceToHost, s));
+      CK(c, cudaStreamSynchronize(s));
+      for (int v = 0; v < c->n_nodes; ++v)
+        for (int k = 0; k < Tl; ++k) flag[v] |= h[(size_t)v * Tl + k];
+    }
+    if (c->world > 1) {
+      CK(c, cudaMemcpyAsync(red, flag.data(), sizeof(int32_t) * c->n_nodes, cudaMemcpyHostToDevice, s));
+      CKN(c, ncclAllReduce(red, red + SAMU_MAX_NODES, c->n_nodes, ncclInt32, ncclMax, c->comm, s));
+      CK(c, cudaMemcpyAsync(flag.data(), red + SAMU_MAX_NODES, sizeof(int32_t) * c->n_nodes, cudaMemcpyDeviceToHost, s));
+      CK(c, cudaStreamSynchronize(s));
+    }
+    for (int v = 0; v < c->n_nodes; ++v) undone[v] = flag[v];
+    return SAMU_OK;
+  }
+};
+
+}  // namespace
+
+extern "C" samu_status samu_plan_greedy(samu_ctx* c, uint64_t seed, int32_t n_trials, samu_plan** out) {
+  GUARD(c);
+  if (!out || n_trials < 1) FAIL(c, SAMU_E_INVALID, "plan_greedy: bad arguments");
+  if (!c->app_loaded) FAIL(c, SAMU_E_INVALID, "plan_greedy: no app loaded");
+  *out = nullptr;
+  samu_plan* p = new samu_plan();
+  Greedy G;
+  G.c = c;
+  const int64_t sims0 = c->n_sims;
+  samu_status rc = G.run(seed, n_trials, p);
+  if (rc != SAMU_OK) { delete p; return rc; }
+  p->n_sims = c->n_sims - sims0;
+  *out = p;
+  return SAMU_OK;
+}
+
+extern "C" void samu_plan_free(samu_plan* p) { delete p; }

@@ -1,0 +1,110 @@
+// Internal declarations shared by libsamu's translation units (product path only; the oracle
+// under oracle/ shares nothing with this tree).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/samu.h"
+
+#define SAMU_EMPTY 0xFFFFFFFFu
+#define SAMU_WARPS_PER_BLOCK 8
+
+// ------------------------------------------------------------------------------------------
+// Application tables on the device (uploaded by samu_app_load)
+// ------------------------------------------------------------------------------------------
+struct DevApp {
+  int32_t n_req, n_nodes;
+  const uint32_t* l_in_base;   // [n]
+  const uint32_t* cap_y;       // [n]
+  const int32_t* pred;         // [n]
+  const int32_t* node;         // [n]
+  const int32_t* succ;         // [n] same-node chain successor or -1
+  const uint8_t* cross;        // [n] 1 if pred is in another node
+};
+
+// eCDF tables for the sampler: per model offset into packed knot arrays
+struct DevEcdf {
+  const uint32_t* values;      // packed knots, all models
+  const uint32_t* cum;
+  const int32_t* off;          // [n_models + 1]
+  const int32_t* model_of_node;  // [n_nodes]
+  const uint32_t* l_max_of_node; // [n_nodes]
+};
+
+// One candidate (node, plan) as the simulation kernel sees it.
+struct DevCand {
+  int32_t node, dp, tp, resume, commit, src;
+  uint32_t max_seqs, bs, budget;
+  int32_t blocks;              // KV blocks per replica (c5)
+  uint32_t L, h_tp;            // layers, h / tp
+  uint64_t c;                  // per-layer matmul weight elements
+  double load_s;               // loading time of (model, dp, tp)
+  const double* coef;          // dense [3 phases][2 (a,b)][max_seqs]
+  const uint32_t* rep_off;     // [dp + 1]
+  const uint32_t* rep_req;     // requests of the node grouped by replica, index order
+  const double* src_fin;       // [T][n] finish times of the dependency source, or null
+  const double* tau;           // [T] time limits or null
+  const samu_trial_rec* tau_rec;  // [T] take tau_k = tau_rec[k].t_end (f* of a stage), or null
+  double* fin_t_out;           // [T][n] or null
+  uint32_t* fin_iter_out;      // [T][n] or null
+};
+
+struct SimLaunch {
+  DevApp app;
+  const DevCand* cands;
+  int32_t n_cands;
+  int32_t n_trials;
+  const uint2* items;          // (cand, trial*16 + replica), longest first
+  int32_t n_items;
+  uint32_t* next_item;         // work counter
+  const uint16_t* l_out;       // [T][n]
+  const uint16_t* l_in;        // [T][n]
+  uint32_t* st;                // [T][n] or null (fresh)
+  uint16_t* g;
+  double* fin_t;
+  double* over;                // [T][n_nodes][16]
+  samu_trial_rec* rep_rec;     // [n_cands][T][16]
+  uint32_t* scratch_q;         // [n_warps][max_q]
+  uint64_t* scratch_key;       // [n_warps][2][max_p]
+  uint32_t* scratch_idx;       // [n_warps][2][max_p]
+  int32_t max_q, max_p;
+  int32_t* error;              // first error code (0 = ok)
+};
+
+// launchers (return cudaError_t of the launch)
+cudaError_t launch_sample(const DevApp& app, const DevEcdf& e, const int32_t* seq_head, int32_t n_seq,
+                          uint64_t seed, int32_t trial_begin, int32_t n_trials, uint16_t* l_out,
+                          uint16_t* l_in, cudaStream_t s);
+cudaError_t launch_dense_coeff(const uint32_t* bucket_B, int32_t nb, const double* coeff_slot,
+                               uint32_t max_seqs, double* out, cudaStream_t s);
+cudaError_t launch_simulate(const SimLaunch& L, int32_t n_blocks, cudaStream_t s);
+cudaError_t simulate_prepare(int* blocks_per_sm);
+int32_t simulate_smem_bytes();
+cudaError_t launch_combine(const samu_trial_rec* rep_rec, const DevCand* cands, int32_t n_cands, int32_t n_trials,
+                           samu_trial_rec* out, double* over, int32_t n_nodes, cudaStream_t s);
+cudaError_t launch_summary(const samu_trial_rec* recs, int32_t n_cands, int32_t n_trials,
+                           samu_cand_summary* out, cudaStream_t s);
+cudaError_t launch_rebase(uint32_t* st, double* fin_t, int64_t n_total, const samu_trial_rec* fstar_rec,
+                          int32_t n_req, cudaStream_t s);
+cudaError_t launch_node_done(const uint32_t* st, int32_t n_trials, int32_t n_req, const int32_t* node,
+                             int32_t* out_any_undone /*[n_nodes][n_trials]*/, int32_t n_nodes, cudaStream_t s);
+
+// stage scoring (greedy): see k_reduce.cu
+struct StageCand {
+  int32_t n_entries;
+  int32_t full_slot[16];       // record slot (in the full-sim cache) of each entry
+  int32_t cut_slot[16];        // record slot of each entry's cut sim (after f* is known), -1 for f*
+  int32_t node[16];
+  int32_t gpus;                // #gpu of the candidate stage
+  int32_t changed_node, changed_dp, changed_tp;
+};
+struct StageOut {
+  int32_t fstar;               // entry index of f*
+  int32_t pad;
+  double TE, mean_tE;
+};
+cudaError_t launch_fstar(const samu_trial_rec* cache, int32_t T, const StageCand* sc, int32_t n, StageOut* out,
+                         cudaStream_t s);
+cudaError_t launch_stage_score(const samu_trial_rec* cache, int32_t T, const StageCand* sc, int32_t n,
+                               StageOut* out, double TE_star, int32_t gpus_star, int32_t* best,
+                               double* max_dT, cudaStream_t s);

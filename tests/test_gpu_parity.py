@@ -1,0 +1,257 @@
+"""GPU parity: the CUDA path (through libsamu's C ABI) vs the CPU oracle, element by element.
+
+Bar (BASELINE.json north_star): sampled lengths, per-request finish iterations, records and the
+greedy plan bit-exact; fp64 totals within 1e-9 rel — asserted here as exact equality, since
+both sides evaluate the same operations in the same order (readings c17, c22, c24).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import samu_workloads as W
+from tests import fixtures as F
+
+pytestmark = pytest.mark.gpu
+SEED = W.SAMPLING_SEED
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    return torch
+
+
+def gpu(w):
+    from paper_2503_16893_b200 import Samu
+    S = Samu(0)
+    S.load_workload(w)
+    return S
+
+
+def u16(t):
+    return t.cpu().numpy().view(np.uint16)
+
+
+def recs(out):
+    from paper_2503_16893_b200 import recs_to_numpy
+    return recs_to_numpy(out["recs"])
+
+
+def assert_rec_equal(g, o, ctx=""):
+    for f in ("t_end", "flops_lo", "flops_hi", "req_iters", "iters", "flags"):
+        assert np.array_equal(g[f], o[f]), f"{ctx}: field {f} differs\n gpu={g[f][:8]}\n ora={o[f][:8]}"
+
+
+def plans_sample(P, node, k=6):
+    pl = P.plans(P.w.node_model[node])
+    if len(pl) <= k:
+        return pl
+    idx = np.linspace(0, len(pl) - 1, k).round().astype(int)
+    return [pl[i] for i in sorted(set(idx))]
+
+
+# ------------------------------------------------------------------------------------------
+# K1 sampler
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name,kw", [("c1", {}), ("c2", dict(n_prompts=300)), ("c3", dict(n_prompts=2000)),
+                                     ("c4", dict(n_docs=200)), ("c5", dict(n_prompts=500, n_docs=200))])
+def test_sampler_bit_exact(name, kw):
+    w = W.make_workload(name, n_trials=8, **kw)
+    P = O.Problem(w)
+    S = gpu(w)
+    for tb, T in [(0, 8), (5, 3)]:
+        lo, li = P.sample(SEED, tb, T)
+        glo, gli = S.samu_sample_lengths(SEED, tb, T)
+        assert np.array_equal(u16(glo), lo) and np.array_equal(u16(gli), li)
+
+
+def test_sampler_full_size_c5_sampled_trials():
+    # BASELINE configs[4] at full size (50,000 requests): trials 0, 511, 1023 checked exactly
+    w = W.make_workload("c5")
+    P = O.Problem(w)
+    S = gpu(w)
+    for tb in (0, 511, 1023):
+        lo, li = P.sample(SEED, tb, 1)
+        glo, gli = S.samu_sample_lengths(SEED, tb, 1)
+        assert np.array_equal(u16(glo), lo) and np.array_equal(u16(gli), li)
+
+
+# ------------------------------------------------------------------------------------------
+# K2 simulation, fresh state
+# ------------------------------------------------------------------------------------------
+def _sim_parity(w, cands, T, tb=0, tau=None):
+    P = O.Problem(w)
+    S = gpu(w)
+    lo, li = P.sample(SEED, tb, T)
+    glo, gli = S.samu_sample_lengths(SEED, tb, T)
+    out = S.samu_simulate_batch(cands, glo, gli, time_limit=tau, want_fin_iter=True, want_fin_t=True)
+    g = recs(out)
+    fi = out["fin_iter"].cpu().numpy().view(np.uint32)
+    ft = out["fin_t"].cpu().numpy()
+    for ci, cd in enumerate(cands):
+        node, dp, tp = cd[:3]
+        o, ofi, oft = P.simulate(node, dp, tp, lo, li, tau=None if tau is None else tau[ci], want_fin=True)
+        assert_rec_equal(g[ci], o, f"cand {cd}")
+        a, b = w.node_range(node)
+        assert np.array_equal(fi[ci][:, a:b], ofi[:, a:b]), f"finish iterations differ for {cd}"
+        assert np.array_equal(ft[ci][:, a:b], oft[:, a:b]), f"finish times differ for {cd}"
+    return g
+
+
+@pytest.mark.parametrize("name,kw,T", [("c1", {}, 1), ("c2", dict(n_prompts=400), 4), ("c3", dict(n_prompts=1500), 3)])
+def test_simulate_bit_exact_independent(name, kw, T):
+    w = W.make_workload(name, n_trials=T, **kw)
+    P = O.Problem(w)
+    cands = []
+    for v in range(w.n_nodes):
+        for (dp, tp) in plans_sample(P, v, 5):
+            cands.append((v, dp, tp))
+    _sim_parity(w, cands, T, tb=2)
+
+
+def test_simulate_bit_exact_time_limits():
+    w = W.make_workload("c2", n_prompts=300, n_trials=3)
+    P = O.Problem(w)
+    cands = [(0, 1, 1), (2, 2, 1), (5, 1, 4), (3, 4, 2)]
+    lo, li = P.sample(SEED, 0, 3)
+    full = [P.simulate(*c, lo, li)[0]["t_end"] for c in cands]
+    rng = np.random.default_rng(0)
+    tau = np.array([f * rng.uniform(0.1, 0.9, 3) for f in full])
+    g = _sim_parity(w, cands, 3, tau=tau)
+    assert np.all(g["flags"] & 2)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_simulate_fuzz_tight_kv_preemption(seed):
+    # random small workloads with few KV blocks: preemption, token budget and slot limits
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(5, 120))
+    lin = rng.integers(1, 60, n)
+    lout = rng.integers(0, 80, n)
+    eng = F.engine(kv_cap=int(rng.integers(9, 40)) * 16, min_batched_tokens=int(rng.integers(144, 400)),
+                   max_num_seqs=int(rng.integers(1, 40)), block_size=int(rng.choice([4, 8, 16, 7])), n_gpus=4)
+    cf = np.zeros((W.N_TP_SLOTS, 3, 2, F.NB))
+    cf[:, :, :, :] = rng.uniform(1e-4, 1e-2, (W.N_TP_SLOTS, 3, 2, F.NB))
+    cf[:, 0, 0, :] = 1e-12
+    w = F.tiny(lin, lout, sp=F.spec(l_max=140, tp_values=(1, 2), L=2, h=16, c=1000), eng=eng, cf=cf, n_trials=2)
+    _sim_parity(w, [(0, 1, 1), (0, 2, 1), (0, 1, 2), (0, 3, 1)], 2)
+
+
+def test_hand_traces_on_gpu():
+    for kind, expect_t in (("const", 63.0), ("B", 80.0), ("S", 32 + 784 + 1012 + 33 + 979)):
+        w = F.tiny([16, 16], [40, 40], sp=F.spec(l_max=64), cf=kind, eng=F.engine(kv_cap=64, min_batched_tokens=64))
+        g = _sim_parity(w, [(0, 1, 1)], 1)
+        assert g["t_end"][0, 0] == expect_t
+    w = F.tiny([10, 10], [2, 1], eng=F.engine(max_num_seqs=2))
+    g = _sim_parity(w, [(0, 1, 1)], 1)
+    assert g["t_end"][0, 0] == 2.0
+
+
+def test_uniform_lengths_exactly_L_iterations_gpu():
+    for L in (1, 3, 50):
+        w = F.tiny(np.full(300, 20), np.full(300, L))
+        g = _sim_parity(w, [(0, 1, 1)], 1)
+        assert g["iters"][0, 0] == L
+
+
+# ------------------------------------------------------------------------------------------
+# dependencies (chains + evaluator), commit / resume state
+# ------------------------------------------------------------------------------------------
+def test_dependency_parity_c4():
+    w = W.make_workload("c4", n_docs=150, n_trials=3)
+    P = O.Problem(w)
+    S = gpu(w)
+    lo, li = P.sample(SEED, 0, 3)
+    glo, gli = S.samu_sample_lengths(SEED, 0, 3)
+    for (dps, tps), (dpe, tpe) in [((1, 1), (1, 2)), ((2, 2), (4, 1)), ((3, 1), (1, 8))]:
+        out = S.samu_simulate_batch([(0, dps, tps, 0, -1, 0), (1, dpe, tpe, 0, 0, 0)], glo, gli, want_fin_iter=True,
+                                    want_fin_t=True)
+        g = recs(out)
+        os_, ofs, fts = P.simulate(0, dps, tps, lo, li, want_fin=True)
+        oe, ofe, fte = P.simulate(1, dpe, tpe, lo, li, src_fin=fts, want_fin=True)
+        assert_rec_equal(g[0], os_, "summariser")
+        assert_rec_equal(g[1], oe, "evaluator")
+        fi = out["fin_iter"].cpu().numpy().view(np.uint32)
+        a, b = w.node_range(0)
+        assert np.array_equal(fi[0][:, a:b], ofs[:, a:b])
+        a, b = w.node_range(1)
+        assert np.array_equal(fi[1][:, a:b], ofe[:, a:b])
+
+
+def _state_np(s):
+    return dict(st=s["st"].cpu().numpy().view(np.uint32), g=s["g"].cpu().numpy().view(np.uint16),
+                fin_t=s["fin_t"].cpu().numpy(), over=s["over"].cpu().numpy())
+
+
+@pytest.mark.parametrize("name,kw,node,plans", [
+    ("c2", dict(n_prompts=300), 4, [(2, 1), (1, 2)]),
+    ("c4", dict(n_docs=120), 0, [(1, 1), (2, 1)]),
+])
+def test_commit_then_resume_and_reload_parity(name, kw, node, plans):
+    T = 3
+    w = W.make_workload(name, n_trials=T, **kw)
+    P = O.Problem(w)
+    S = gpu(w)
+    lo, li = P.sample(SEED, 0, T)
+    glo, gli = S.samu_sample_lengths(SEED, 0, T)
+    (dp1, tp1), (dp2, tp2) = plans
+    full = P.simulate(node, dp1, tp1, lo, li)[0]["t_end"]
+    tau = full * np.array([0.3, 0.55, 0.8])
+    ost = P.fresh_state(T)
+    gst = S.fresh_state(T)
+    o1, _, _ = P.simulate(node, dp1, tp1, lo, li, state=ost, tau=tau, commit=True)
+    g1 = recs(S.samu_simulate_batch([(node, dp1, tp1, 0, -1, 1)], glo, gli, state=gst, time_limit=tau[None]))
+    assert_rec_equal(g1[0], o1, "cut+commit")
+    gs = _state_np(gst)
+    for f in ("st", "g", "fin_t", "over"):
+        assert np.array_equal(gs[f], ost[f]), f"state field {f} differs after commit"
+    # resume with the same plan, and reload with another plan, from the committed state
+    ost2 = {k: v.copy() for k, v in ost.items()}
+    o2, _, _ = P.simulate(node, dp1, tp1, lo, li, resume=1, state=ost)
+    o3, _, _ = P.simulate(node, dp2, tp2, lo, li, resume=0, state=ost2)
+    g2 = recs(S.samu_simulate_batch([(node, dp1, tp1, 1, -1, 0), (node, dp2, tp2, 0, -1, 0)], glo, gli, state=gst))
+    assert_rec_equal(g2[0], o2, "resume")
+    assert_rec_equal(g2[1], o3, "reload")
+
+
+# ------------------------------------------------------------------------------------------
+# K3 summaries
+# ------------------------------------------------------------------------------------------
+def test_summary_mean_and_percentiles():
+    w = W.make_workload("c2", n_prompts=200, n_trials=37)
+    S = gpu(w)
+    glo, gli = S.samu_sample_lengths(SEED, 0, 37)
+    out = S.samu_simulate_batch([(0, 1, 1), (5, 2, 4)], glo, gli, summary=True)
+    g = recs(out)
+    for ci in range(2):
+        t = g["t_end"][ci]
+        s = 0.0
+        for x in t:
+            s += float(x)
+        sm = out["summary"][ci]
+        assert sm["mean_t"] == s / 37
+        for p in (50, 90, 99):
+            assert sm[f"p{p}_t"] == np.percentile(t, p, method="inverted_cdf")
+
+
+# ------------------------------------------------------------------------------------------
+# greedy planner (Algorithm 1)
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name,kw,T", [
+    ("c1", {}, 1),
+    ("c2", dict(n_prompts=120), 3),
+    ("c3", dict(n_prompts=600), 2),
+    ("c4", dict(n_docs=60), 2),
+])
+def test_greedy_plan_bit_exact(name, kw, T):
+    w = W.make_workload(name, n_trials=T, **kw)
+    po = O.Problem(w).plan_greedy(SEED, T)
+    pg = gpu(w).samu_plan_greedy(SEED, T)
+    assert len(pg["stages"]) == len(po["stages"])
+    for sg, so in zip(pg["stages"], po["stages"]):
+        assert sg["entries"] == so["entries"]
+        assert sg["fstar"] == so["fstar"]
+        assert sg["mean_tE"] == so["mean_tE"]
+        assert sg["T_E"] == so["T_E"]
+    assert pg["total"] == po["total"]
+    assert pg["n_cand_evals"] == po["n_cand_evals"]
