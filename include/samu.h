@@ -132,8 +132,8 @@ typedef struct samu_plan {
 
 /* ---- context ---------------------------------------------------------------------------- */
 
-/* Create a context on CUDA device `cuda_device`, ordered on `cuda_stream` (a cudaStream_t, or
- * NULL for a context-owned stream).  rank / world: this process's position among the processes
+/* Create a context on CUDA device `cuda_device`, ordered on `cuda_stream` (a cudaStream_t; NULL
+ * is the CUDA default stream, e.g. PyTorch's default current stream).  rank / world: this process's position among the processes
  * sharding the Monte-Carlo trials; world > 1 requires `nccl_unique_id` (128 bytes, host, from
  * samu_nccl_unique_id on rank 0 and broadcast by the caller).  *out owned by the caller until
  * samu_ctx_destroy. */

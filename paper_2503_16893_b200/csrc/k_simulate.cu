@@ -78,7 +78,9 @@ __device__ __forceinline__ double iter_cost(const double* __restrict__ coef, uin
   return __dadd_rn(__dadd_rn(tc, tp), ts);
 }
 
-__device__ __forceinline__ void set_error(int32_t* e, int32_t code) { atomicCAS(e, 0, code); }
+__device__ __forceinline__ void set_error(int32_t* e, int32_t code, int32_t site) {
+  if (atomicCAS(e, 0, code) == 0) e[1] = site;
+}
 
 struct Sim {
   // uniform scalar state
@@ -86,8 +88,9 @@ struct Sim {
   uint64_t fl_lo, fl_hi, reqit;
   uint32_t iter, d, needidx, B, S, next_fin, next_rank;
   int32_t F, maxO;
-  uint32_t stack_cnt, q_head, q_tail, n_heads, pend_ptr, n_pend;
+  uint32_t stack_cnt, q_head, q_tail, n_heads, n_front, pend_ptr, n_pend;
   int32_t err;
+  int32_t site;
 };
 
 __device__ __forceinline__ void add_flops(Sim& m, uint64_t f) {
@@ -112,6 +115,53 @@ __device__ __forceinline__ void rescan(WarpSm& W, Sim& m, int lane) {
   m.maxO = __reduce_max_sync(FULL, mx);
 }
 
+
+// Stable LSD radix sort of n (key, idx) pairs by the 64-bit key (8 passes of 8 bits, passes where
+// every key shares the digit are skipped), one warp, 256-bin histogram in shared memory.
+// Returns the buffer holding the sorted keys; *out_idx the matching indices.
+__device__ const uint64_t* warp_radix_sort(uint64_t* ka, uint32_t* ia, uint64_t* kb, uint32_t* ib, uint32_t n,
+                                           uint32_t* hist, int lane, uint32_t** out_idx) {
+  for (int pass = 0; pass < 8; ++pass) {
+    const int sh = pass * 8;
+    for (int b = lane; b < 256; b += 32) hist[b] = 0;
+    __syncwarp();
+    for (uint32_t i = lane; i < n; i += 32) atomicAdd(&hist[(ka[i] >> sh) & 255u], 1u);
+    __syncwarp();
+    uint32_t loc[8], sum = 0;
+    bool one_bin = false;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) { loc[b] = hist[lane * 8 + b]; sum += loc[b]; one_bin |= loc[b] == n; }
+    if (__any_sync(FULL, one_bin)) { __syncwarp(); continue; }
+    const uint32_t incl = warp_incl_scan(sum, lane);
+    uint32_t run = incl - sum;
+    __syncwarp();
+#pragma unroll
+    for (int b = 0; b < 8; ++b) { hist[lane * 8 + b] = run; run += loc[b]; }
+    __syncwarp();
+    for (uint32_t base = 0; base < n; base += 32) {
+      const uint32_t i = base + lane;
+      const bool v = i < n;
+      const uint32_t act = __ballot_sync(FULL, v);
+      if (v) {
+        const uint64_t key = ka[i];
+        const uint32_t dg = (uint32_t)(key >> sh) & 255u;
+        const uint32_t peers = __match_any_sync(act, dg);
+        const uint32_t pos = hist[dg] + __popc(peers & lanemask_lt());
+        kb[pos] = key;
+        ib[pos] = ia[i];
+        __syncwarp(act);
+        if ((peers & lanemask_lt()) == 0) hist[dg] += __popc(peers);
+      }
+      __syncwarp();
+    }
+    uint64_t* tk = ka; ka = kb; kb = tk;
+    uint32_t* ti = ia; ia = ib; ib = ti;
+  }
+  __syncwarp();
+  *out_idx = ia;
+  return ka;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------------------------
@@ -121,8 +171,8 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
   WarpSm& W = reinterpret_cast<WarpSm*>(smem_raw)[warp];
   const int gw = blockIdx.x * SAMU_WARPS_PER_BLOCK + warp;
   uint32_t* q = P.scratch_q + (size_t)gw * P.max_q;
-  uint64_t* pkey = P.scratch_key + (size_t)gw * 2 * P.max_p;
-  uint32_t* pidx = P.scratch_idx + (size_t)gw * 2 * P.max_p;
+  uint64_t* pkey = P.scratch_key + (size_t)gw * 4 * P.max_p;
+  uint32_t* pidx = P.scratch_idx + (size_t)gw * 4 * P.max_p;
   const DevApp& A = P.app;
   const int n = A.n_req;
 
@@ -154,33 +204,49 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
     m.fl_lo = m.fl_hi = m.reqit = 0;
     m.iter = 0; m.d = 0; m.needidx = 0; m.B = 0; m.S = 0; m.next_rank = 0;
     m.F = C.blocks; m.maxO = INT_MIN; m.next_fin = FULL;
-    m.stack_cnt = 0; m.q_head = 0; m.q_tail = 0; m.n_heads = 0; m.pend_ptr = 0; m.n_pend = 0;
+    m.stack_cnt = 0; m.q_head = 0; m.q_tail = 0; m.n_heads = 0; m.n_front = 0; m.pend_ptr = 0; m.n_pend = 0;
     m.err = 0;
+    m.site = 0;
 
     for (int s = lane; s < SLOTS; s += 32) W.s_req[s] = SAMU_EMPTY;
     W.hist[lane] = 0;
     __syncwarp();
 
     // ---- initial state from the carried WorkloadState (c18, c27) ----
-    uint32_t n_run = 0, n_pre = 0, n_q = 0;
+    // W = [preempted stack (smem, new preemptions)] + queue: [front: recomputed running (reload)
+    // and earlier-preempted requests][never-started heads, index order][queued / arrived]
+    uint64_t* skey = pkey + 2 * (size_t)P.max_p;   // carried-entry sort buffers
+    uint32_t* sidx = pidx + 2 * (size_t)P.max_p;
+    uint32_t n_run = 0, n_pre = 0, n_q = 0, n_cls = 0;
     bool all_done = true;
     for (uint32_t base = r0; base < r1; base += 32) {
       const uint32_t idx = base + lane;
       const bool valid = idx < r1;
       const uint32_t r = valid ? __ldg(C.rep_req + idx) : 0u;
       const uint32_t w = (valid && st) ? st[r] : 0u;
-      const uint32_t s = w >> 28;
+      const uint32_t s = w >> 28, rk = w & 0x0FFFFFFFu;
       const int32_t pr = valid ? __ldg(A.pred + r) : -1;
       const bool cross = valid && pr >= 0 && __ldg(A.cross + r);
       const bool fresh = valid && s == SAMU_ST_FRESH;
       const bool head = fresh && pr < 0;
       const bool pend = fresh && cross;
       const bool succ_wait = fresh && pr >= 0 && !cross;
-      if (succ_wait && st && (st[pr] >> 28) == SAMU_ST_DONE) m.err = SAMU_E_STATE;
-      if (valid && s > SAMU_ST_DONE) m.err = SAMU_E_STATE;
+      if (succ_wait && st && (st[pr] >> 28) == SAMU_ST_DONE) { m.err = SAMU_E_STATE; m.site = 1; }
+      if (valid && s > SAMU_ST_DONE) { m.err = SAMU_E_STATE; m.site = 2; }
       const uint32_t bh = __ballot_sync(FULL, head);
-      if (head) q[m.q_tail + __popc(bh & lanemask_lt())] = r;
-      m.q_tail += __popc(bh);
+      if (head && !st) q[m.n_heads + __popc(bh & lanemask_lt())] = r;   // fresh state: no front region
+      m.n_heads += __popc(bh);
+      // carried entries: class 0 running (reload) | 1 preempted | 3 queued | 4 running (resume)
+      uint32_t cls = 7;
+      if (valid && s == SAMU_ST_RUNNING) cls = C.resume ? 4u : 0u;
+      else if (valid && s == SAMU_ST_PREEMPTED) cls = 1u;
+      else if (valid && s == SAMU_ST_QUEUED) cls = 3u;
+      const uint32_t bc = __ballot_sync(FULL, cls != 7);
+      if (cls != 7) {
+        const uint32_t pos = n_cls + __popc(bc & lanemask_lt());
+        if (pos < (uint32_t)P.max_p) { skey[pos] = ((uint64_t)cls << 60) | ((uint64_t)rk << 32) | r; sidx[pos] = r; }
+      }
+      n_cls += __popc(bc);
       const uint32_t bp = __ballot_sync(FULL, pend);
       if (pend) {
         double ready;
@@ -196,114 +262,80 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
       n_q += __popc(__ballot_sync(FULL, valid && s == SAMU_ST_QUEUED));
       if (__ballot_sync(FULL, valid && s != SAMU_ST_DONE)) all_done = false;
     }
+    m.site = (int32_t)__reduce_max_sync(FULL, (uint32_t)m.site);
     m.err = __reduce_max_sync(FULL, (uint32_t)(-m.err)) ? SAMU_E_STATE : 0;
-    m.n_heads = m.q_tail;
-    if (m.n_pend > (uint32_t)P.max_p || m.q_tail + n_q > (uint32_t)P.max_q) m.err = SAMU_E_STATE;
-    const uint32_t n_stack0 = C.resume ? n_pre : n_run + n_pre;
-    if ((C.resume && n_run > ms) || n_stack0 > SLOTS) m.err = SAMU_E_STATE;
-    if (!m.err && (n_run | n_pre | n_q)) {
-      int32_t used = 0;
-      uint32_t S0 = 0;
+    m.n_front = C.resume ? n_pre : n_run + n_pre;
+    if (m.n_pend > (uint32_t)P.max_p || n_cls > (uint32_t)P.max_p ||
+        m.n_front + m.n_heads + n_q > (uint32_t)P.max_q) { m.err = SAMU_E_STATE; m.site = 3; }
+    if (C.resume && n_run > ms) { m.err = SAMU_E_STATE; m.site = 4; }
+    m.q_tail = m.n_front + m.n_heads + n_q;
+    if (!m.err && st) {
+      // heads after the front region, in index order
+      uint32_t nh = 0;
       for (uint32_t base = r0; base < r1; base += 32) {
         const uint32_t idx = base + lane;
         const bool valid = idx < r1;
         const uint32_t r = valid ? __ldg(C.rep_req + idx) : 0u;
-        const uint32_t w = valid ? st[r] : 0u;
-        const uint32_t s = w >> 28, rk = w & 0x0FFFFFFFu;
-        if (valid && s == SAMU_ST_RUNNING) {
-          const uint32_t g = gst[r];
-          if (rk >= n_run) { m.err = SAMU_E_STATE; }
-          else if (C.resume) {
+        const bool head = valid && (st[r] >> 28) == SAMU_ST_FRESH && __ldg(A.pred + r) < 0;
+        const uint32_t bh = __ballot_sync(FULL, head);
+        if (head) q[m.n_front + nh + __popc(bh & lanemask_lt())] = r;
+        nh += __popc(bh);
+      }
+      if (n_cls) {
+        // carried entries in (class, rank / seq, index) order (the oracle's sorted pairs)
+        uint32_t* sorted_idx;
+        const uint64_t* sorted = warp_radix_sort(skey, sidx, skey + P.max_p, sidx + P.max_p, n_cls, W.tmp, lane,
+                                                 &sorted_idx);
+        (void)sorted;
+        int32_t used = 0;
+        uint32_t S0 = 0;
+        const uint32_t q_base = m.n_front + m.n_heads;
+        for (uint32_t i = lane; i < n_cls; i += 32) {
+          const uint32_t r = sorted_idx[i];
+          if (i < m.n_front) q[i] = r;
+          else if (i < m.n_front + n_q) q[q_base + (i - m.n_front)] = r;
+          else {   // resume: running requests keep their slots in admission order
+            const uint32_t jx = i - m.n_front - n_q;
+            const uint32_t g = gst[r];
             const uint32_t lin = li[r];
             const uint32_t Lr = max((uint32_t)lo[r], 1u);
             const int32_t o = (int32_t)(lin + g);
             const uint32_t ph = posmod(o - 1, bs);
-            W.s_req[rk] = r;
-            W.s_fin[rk] = Lr - g;
-            W.s_o[rk] = o;
-            W.s_meta[rk] = (rk << 5) | ph;
+            if (g >= Lr || g == 0) { m.err = SAMU_E_STATE; m.site = 5; }
+            W.s_req[jx] = r;
+            W.s_fin[jx] = Lr - g;
+            W.s_o[jx] = o;
+            W.s_meta[jx] = (jx << 5) | ph;
             atomicAdd(&W.hist[ph], 1u);
             used += (int32_t)cdiv(lin + g - 1, bs);
             S0 += lin + g;
-          } else {
-            const uint32_t pos = n_stack0 - 1 - rk;
-            W.stk_req[pos] = r;
-            W.stk_g[pos] = g;
           }
-        } else if (valid && s == SAMU_ST_PREEMPTED) {
-          const uint32_t p = (C.resume ? 0u : n_run) + rk;
-          if (p >= n_stack0) m.err = SAMU_E_STATE;
-          else { W.stk_req[n_stack0 - 1 - p] = r; W.stk_g[n_stack0 - 1 - p] = gst[r]; }
-        } else if (valid && s == SAMU_ST_QUEUED) {
-          if (rk >= n_q) m.err = SAMU_E_STATE;
-          else q[m.n_heads + rk] = r;
+        }
+        used = (int32_t)__reduce_add_sync(FULL, (uint32_t)used);
+        S0 = __reduce_add_sync(FULL, S0);
+        m.site = (int32_t)__reduce_max_sync(FULL, (uint32_t)m.site);
+        m.err = __reduce_max_sync(FULL, (uint32_t)(-m.err)) ? SAMU_E_STATE : 0;
+        if (C.resume) {
+          m.B = n_run;
+          m.S = S0;
+          m.F -= used;
+          m.next_rank = n_run;
+          if (m.F < 0) { m.err = SAMU_E_STATE; m.site = 8; }
         }
       }
-      used = (int32_t)__reduce_add_sync(FULL, (uint32_t)used);
-      S0 = __reduce_add_sync(FULL, S0);
-      m.err = __reduce_max_sync(FULL, (uint32_t)(-m.err)) ? SAMU_E_STATE : 0;
-      if (C.resume) {
-        m.B = n_run;
-        m.S = S0;
-        m.F -= used;
-        m.next_rank = n_run;
-        if (m.F < 0) m.err = SAMU_E_STATE;
-      }
-      m.stack_cnt = n_stack0;
-      m.q_tail = m.n_heads + n_q;
     }
     __syncwarp();
     if (m.B) rescan(W, m, lane);
 
-    // ---- sort pending cross-node arrivals by (ready, index): stable LSD radix (8 x 8 bits) ----
+    // ---- pending cross-node arrivals in (ready, index) order: stable LSD radix sort ----
+    const uint64_t* pk = pkey;
+    const uint32_t* pi = pidx;
     if (!m.err && m.n_pend > 1) {
-      uint64_t* ka = pkey;
-      uint64_t* kb = pkey + P.max_p;
-      uint32_t* ia = pidx;
-      uint32_t* ib = pidx + P.max_p;
-      for (int pass = 0; pass < 8; ++pass) {
-        const int sh = pass * 8;
-        for (int b = lane; b < 256; b += 32) W.tmp[b] = 0;
-        __syncwarp();
-        for (uint32_t i = lane; i < m.n_pend; i += 32) atomicAdd(&W.tmp[(ka[i] >> sh) & 255u], 1u);
-        __syncwarp();
-        // exclusive scan of the 256 bins: lane handles 8 consecutive bins
-        uint32_t loc[8], sum = 0;
-        bool one_bin = false;
-#pragma unroll
-        for (int b = 0; b < 8; ++b) { loc[b] = W.tmp[lane * 8 + b]; sum += loc[b]; one_bin |= loc[b] == m.n_pend; }
-        if (__any_sync(FULL, one_bin)) { __syncwarp(); continue; }   // one bin holds every key: no-op pass
-        const uint32_t incl = warp_incl_scan(sum, lane);
-        uint32_t run = incl - sum;
-        __syncwarp();
-#pragma unroll
-        for (int b = 0; b < 8; ++b) { W.tmp[lane * 8 + b] = run; run += loc[b]; }
-        __syncwarp();
-        for (uint32_t base = 0; base < m.n_pend; base += 32) {
-          const uint32_t i = base + lane;
-          const bool v = i < m.n_pend;
-          const uint32_t act = __ballot_sync(FULL, v);
-          if (v) {
-            const uint64_t key = ka[i];
-            const uint32_t dg = (uint32_t)(key >> sh) & 255u;
-            const uint32_t peers = __match_any_sync(act, dg);
-            const uint32_t pos = W.tmp[dg] + __popc(peers & lanemask_lt());
-            kb[pos] = key;
-            ib[pos] = ia[i];
-            __syncwarp(act);
-            if ((peers & lanemask_lt()) == 0) W.tmp[dg] += __popc(peers);
-          }
-          __syncwarp();
-        }
-        uint64_t* tk = ka; ka = kb; kb = tk;
-        uint32_t* ti = ia; ia = ib; ib = ti;
-      }
-      if (ka != pkey) {   // odd number of effective passes: copy back
-        for (uint32_t i = lane; i < m.n_pend; i += 32) { pkey[i] = ka[i]; pidx[i] = ia[i]; }
-        __syncwarp();
-      }
+      uint32_t* si;
+      pk = warp_radix_sort(pkey, pidx, pkey + P.max_p, pidx + P.max_p, m.n_pend, W.tmp, lane, &si);
+      pi = si;
     }
-    m.next_ready = m.n_pend ? kdouble(pkey[0]) : CUDART_INF;
+    m.next_ready = m.n_pend ? kdouble(pk[0]) : CUDART_INF;
     const uint64_t K1 = 2ull * C.L * C.h_tp;
     bool cut = false;
 
@@ -313,13 +345,13 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
       // (2) pending cross-node arrivals with ready <= t join the back of W
       while (m.pend_ptr < m.n_pend && m.next_ready <= m.t) {
         const uint32_t i = m.pend_ptr + lane;
-        const bool ok = i < m.n_pend && kdouble(pkey[i]) <= m.t;
+        const bool ok = i < m.n_pend && kdouble(pk[i]) <= m.t;
         const uint32_t b = __ballot_sync(FULL, ok);
         const uint32_t cnt = (b == FULL) ? 32u : (uint32_t)(__ffs(~b) - 1);
-        if (lane < cnt) q[m.q_tail + lane] = pidx[i];
+        if (lane < cnt) q[m.q_tail + lane] = pi[i];
         m.q_tail += cnt;
         m.pend_ptr += cnt;
-        m.next_ready = m.pend_ptr < m.n_pend ? kdouble(pkey[m.pend_ptr]) : CUDART_INF;
+        m.next_ready = m.pend_ptr < m.n_pend ? kdouble(pk[m.pend_ptr]) : CUDART_INF;
       }
       const bool wnon = m.stack_cnt > 0 || m.q_head < m.q_tail;
       if (m.B == 0 && !wnon) {
@@ -331,7 +363,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
       if (wnon && m.B < ms) {
         uint32_t hr, hg;
         if (m.stack_cnt) { hr = W.stk_req[m.stack_cnt - 1]; hg = W.stk_g[m.stack_cnt - 1]; }
-        else { hr = q[m.q_head]; hg = 0; }
+        else { hr = q[m.q_head]; hg = m.q_head < m.n_front ? (uint32_t)gst[hr] : 0u; }
         const uint32_t p = (uint32_t)li[hr] + hg;
         fits = p <= C.budget && (int32_t)cdiv(p, bs) <= m.F;
       }
@@ -346,7 +378,11 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
           const bool valid = (uint32_t)lane < avail;
           uint32_t r = 0, g = 0;
           if ((uint32_t)lane < m.stack_cnt) { r = W.stk_req[m.stack_cnt - 1 - lane]; g = W.stk_g[m.stack_cnt - 1 - lane]; }
-          else if (valid) r = q[m.q_head + lane - m.stack_cnt];
+          else if (valid) {
+            const uint32_t qp = m.q_head + lane - m.stack_cnt;
+            r = q[qp];
+            if (qp < m.n_front) g = gst[r];   // recompute front keeps its generated tokens
+          }
           const uint32_t p = valid ? (uint32_t)li[r] + g : 0u;
           const uint32_t nb = valid ? cdiv(p, bs) : 0u;
           const uint32_t sp = warp_incl_scan(p, lane), sb = warp_incl_scan(nb, lane);
@@ -424,7 +460,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
         m.next_rank += k_adm;
         if (n_stay) rescan(W, m, lane);
       } else {
-        if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; break; }
+        if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; m.site = 9; break; }
         // ================= decode run (c9): uniform iterations until an event ===============
         uint32_t B = m.B;
         uint64_t K0 = (uint64_t)C.L * C.c * B;
@@ -464,7 +500,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
               m.stack_cnt += 1;
               m.B -= 1;
               m.S -= l;
-              if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; break; }
+              if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; m.site = 10; break; }
             }
             if (m.err) break;
             rescan(W, m, lane);
@@ -562,7 +598,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
 
     // ---- write back (commit) and the per-replica record ----
     const bool done = !m.err && m.B == 0 && m.stack_cnt == 0 && m.q_head == m.q_tail && m.pend_ptr == m.n_pend;
-    if (m.err) set_error(P.error, m.err);
+    if (m.err && lane == 0) set_error(P.error, m.err, m.site);
     if (commit && !m.err) {
       for (int s = lane; s < SLOTS; s += 32) {
         const uint32_t rq = W.s_req[s];
@@ -580,11 +616,12 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
         st[rq] = (SAMU_ST_PREEMPTED << 28) | (m.stack_cnt - 1 - i);
         gst[rq] = (uint16_t)W.stk_g[i];
       }
-      const uint32_t qbase = max(m.q_head, m.n_heads);
+      const uint32_t qbase = max(m.q_head, m.n_front + m.n_heads);
       for (uint32_t pos = m.q_head + lane; pos < m.q_tail; pos += 32) {
         const uint32_t rq = q[pos];
-        if (pos >= m.n_heads) st[rq] = (SAMU_ST_QUEUED << 28) | (pos - qbase);
-        gst[rq] = 0;
+        if (pos < m.n_front) st[rq] = (SAMU_ST_PREEMPTED << 28) | (m.stack_cnt + pos - m.q_head);
+        else if (pos < m.n_front + m.n_heads) gst[rq] = 0;
+        else { st[rq] = (SAMU_ST_QUEUED << 28) | (pos - qbase); gst[rq] = 0; }
       }
       if (over && lane == 0) over[j] = (done || !cut) ? 0.0 : __dsub_rn(m.t, m.tau);
     }

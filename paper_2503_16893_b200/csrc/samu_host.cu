@@ -197,11 +197,7 @@ extern "C" samu_status samu_ctx_create(samu_ctx** out, int32_t cuda_device, void
   c->world = world;
   if (cudaSetDevice(cuda_device) != cudaSuccess) { delete c; return SAMU_E_CUDA; }
   cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, cuda_device);
-  if (cuda_stream) c->stream = (cudaStream_t)cuda_stream;
-  else {
-    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) { delete c; return SAMU_E_CUDA; }
-    c->own_stream = true;
-  }
+  c->stream = (cudaStream_t)cuda_stream;   // NULL = the CUDA default (legacy) stream
   if (world > 1) {
     ncclUniqueId id;
     std::memcpy(id.internal, nccl_unique_id, 128);
@@ -482,8 +478,8 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
     if (bpsm < 1) FAIL(c, SAMU_E_CUDA, "simulate: kernel does not fit on an SM");
     c->sim_blocks_per_sm = bpsm;
   }
-  CK(c, c->d_error.ensure(sizeof(int32_t)));
-  CK(c, cudaMemsetAsync(c->d_error.p, 0, sizeof(int32_t), s));
+  CK(c, c->d_error.ensure(2 * sizeof(int32_t)));
+  CK(c, cudaMemsetAsync(c->d_error.p, 0, 2 * sizeof(int32_t), s));
   for (int ph = 0; ph <= max_phase; ++ph) {
     std::vector<int> idx;
     for (int i = 0; i < (int)jobs.size(); ++i) if (jobs[i].phase == ph) idx.push_back(i);
@@ -520,7 +516,7 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
       uint32_t mx = 0;
       for (int j = 0; j < cd.dp; ++j) mx = std::max(mx, ho[j + 1] - ho[j]);
       max_q = std::max(max_q, mx);
-      if (c->node_input[node] >= 0) max_p = std::max(max_p, mx);
+      if (c->node_input[node] >= 0 || S.st) max_p = std::max(max_p, mx);
       cost[x] = mx;
     }
     // longest-first work items (cand, trial, replica)
@@ -542,8 +538,8 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
     n_blocks = std::max(n_blocks, 1);
     const size_t n_warps = (size_t)n_blocks * SAMU_WARPS_PER_BLOCK;
     CK(c, c->d_scratch_q.ensure(sizeof(uint32_t) * n_warps * max_q));
-    CK(c, c->d_scratch_key.ensure(sizeof(uint64_t) * n_warps * 2 * max_p));
-    CK(c, c->d_scratch_idx.ensure(sizeof(uint32_t) * n_warps * 2 * max_p));
+    CK(c, c->d_scratch_key.ensure(sizeof(uint64_t) * n_warps * 4 * max_p));
+    CK(c, c->d_scratch_idx.ensure(sizeof(uint32_t) * n_warps * 4 * max_p));
     SimLaunch L;
     L.app = dev_app(c);
     L.cands = c->d_cands.as<DevCand>();
@@ -571,11 +567,19 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
       CK(c, launch_combine(L.rep_rec + x * T * 16, L.cands + x, 1, T, jobs[idx[x]].out_rec, S.over, c->n_nodes, s));
     }
     c->n_sims += (int64_t)idx.size() * T;
-    int32_t herr = 0;
-    CK(c, cudaMemcpyAsync(&herr, c->d_error.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    int32_t herr[2] = {0, 0};
+    CK(c, cudaMemcpyAsync(herr, c->d_error.p, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     CK(c, cudaStreamSynchronize(s));
-    if (herr) FAIL(c, herr, herr == SAMU_E_INFEASIBLE ? "simulate: capacity below one sequence"
-                                                   : "simulate: inconsistent WorkloadState / scratch overflow");
+    if (herr[0]) {
+      static const char* sites[] = {"?", "waiting chain successor of a done request", "bad status word",
+                                    "scratch overflow", "running/preempted set exceeds the engine slots",
+                                    "running rank out of range", "preempted seq out of range",
+                                    "queued seq out of range", "carried KV blocks exceed capacity",
+                                    "head cannot fit an empty engine", "preemption emptied the engine"};
+      const int si = (herr[1] >= 0 && herr[1] <= 10) ? herr[1] : 0;
+      FAIL(c, herr[0], std::string(herr[0] == SAMU_E_INFEASIBLE ? "simulate: infeasible (capacity below one sequence): "
+                                                              : "simulate: inconsistent WorkloadState: ") + sites[si]);
+    }
   }
   return SAMU_OK;
 }
@@ -761,7 +765,7 @@ struct Greedy {
     int nc = std::max(need, std::max(64, cap_slots * 2));
     DevBuf nb;
     CK(c, nb.ensure(sizeof(samu_trial_rec) * (size_t)nc * T));
-    if (n_slots) CK(c, cudaMemcpyAsync(nb.p, cache.p, sizeof(samu_trial_rec) * (size_t)n_slots * T, cudaMemcpyDeviceToDevice, c->stream));
+    if (cap_slots) CK(c, cudaMemcpyAsync(nb.p, cache.p, sizeof(samu_trial_rec) * (size_t)cap_slots * T, cudaMemcpyDeviceToDevice, c->stream));
     CK(c, cudaStreamSynchronize(c->stream));
     cache = std::move(nb);
     cap_slots = nc;

@@ -65,8 +65,8 @@ struct SimLaunch {
   double* over;                // [T][n_nodes][16]
   samu_trial_rec* rep_rec;     // [n_cands][T][16]
   uint32_t* scratch_q;         // [n_warps][max_q]
-  uint64_t* scratch_key;       // [n_warps][2][max_p]
-  uint32_t* scratch_idx;       // [n_warps][2][max_p]
+  uint64_t* scratch_key;       // [n_warps][4][max_p]: pending sort (2) + carried-state sort (2)
+  uint32_t* scratch_idx;       // [n_warps][4][max_p]
   int32_t max_q, max_p;
   int32_t* error;              // first error code (0 = ok)
 };

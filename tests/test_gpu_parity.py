@@ -149,7 +149,8 @@ def test_hand_traces_on_gpu():
 
 def test_uniform_lengths_exactly_L_iterations_gpu():
     for L in (1, 3, 50):
-        w = F.tiny(np.full(300, 20), np.full(300, L))
+        # reading c4 preconditions: max_num_seqs >= n and token budget >= sum(l_in)
+        w = F.tiny(np.full(250, 20), np.full(250, L), eng=F.engine(min_batched_tokens=100000))
         g = _sim_parity(w, [(0, 1, 1)], 1)
         assert g["iters"][0, 0] == L
 
