@@ -141,6 +141,8 @@ samu_status samu_ctx_create(samu_ctx** out, int32_t cuda_device, void* cuda_stre
                             int32_t world, const uint8_t* nccl_unique_id);
 void samu_ctx_destroy(samu_ctx* ctx);
 const char* samu_last_error(const samu_ctx* ctx);
+/* Number of CUDA kernels this context has launched so far (instrumentation). */
+uint64_t samu_launch_count(const samu_ctx* ctx);
 samu_status samu_nccl_unique_id(uint8_t out[128]);
 
 /* Register model `model_id` (0..63): spec, per-B coefficient buckets and the loading table.
@@ -163,6 +165,11 @@ samu_status samu_ecdf_load(samu_ctx* ctx, int32_t model_id, const uint32_t* valu
  * request array (host [n_req], layout rules above).  Validates (SAMU_E_INVALID) and uploads. */
 samu_status samu_app_load(samu_ctx* ctx, const samu_engine_cfg* engine, int32_t n_nodes,
                           const int32_t* node_model, int32_t n_req, const samu_request* reqs);
+
+/* Valid execution plans of `node`'s model on the planned machine: writes up
+ * to `cap` (dp, tp) pairs in order of ascending dp*tp then tp into host dp[] / tp[] and returns
+ * their total count (>= 0), or a negative samu_status. */
+int32_t samu_enumerate_plans(samu_ctx* ctx, int32_t node, int32_t* dp, int32_t* tp, int32_t cap);
 
 /* ---- the hot path ---------------------------------------------------------------------- */
 

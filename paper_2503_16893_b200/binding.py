@@ -65,9 +65,10 @@ REC_DTYPE = np.dtype([("t_end", "<f8"), ("flops_lo", "<u8"), ("flops_hi", "<u8")
                       ("iters", "<u4"), ("flags", "<u4")])
 assert REC_DTYPE.itemsize == C.sizeof(samu_trial_rec) == 40
 
-EXPORTED = ["samu_ctx_create", "samu_ctx_destroy", "samu_last_error", "samu_nccl_unique_id", "samu_model_register",
-            "samu_ecdf_load", "samu_app_load", "samu_sample_lengths", "samu_simulate_batch", "samu_plan_greedy",
-            "samu_plan_free"]
+EXPORTED = ["samu_ctx_create", "samu_ctx_destroy", "samu_last_error", "samu_launch_count", "samu_nccl_unique_id",
+            "samu_model_register",
+            "samu_ecdf_load", "samu_app_load", "samu_enumerate_plans", "samu_sample_lengths", "samu_simulate_batch",
+            "samu_plan_greedy", "samu_plan_free"]
 
 _lib = None
 
@@ -86,9 +87,13 @@ def lib():
         L.samu_last_error.argtypes = [P]
         L.samu_last_error.restype = C.c_char_p
         L.samu_nccl_unique_id.argtypes = [P]
+        L.samu_launch_count.argtypes = [P]
+        L.samu_launch_count.restype = C.c_uint64
         L.samu_model_register.argtypes = [P, C.c_int32, C.POINTER(samu_model_spec), C.c_int32, P, P, P]
         L.samu_ecdf_load.argtypes = [P, C.c_int32, P, P, C.c_int32]
         L.samu_app_load.argtypes = [P, C.POINTER(samu_engine_cfg), C.c_int32, P, C.c_int32, P]
+        L.samu_enumerate_plans.argtypes = [P, C.c_int32, P, P, C.c_int32]
+        L.samu_enumerate_plans.restype = C.c_int32
         L.samu_sample_lengths.argtypes = [P, C.c_uint64, C.c_int32, C.c_int32, P, P]
         L.samu_simulate_batch.argtypes = [P, P, C.c_int32, P, P, C.c_int32, P, P, P, P, P, P, P, P, P]
         L.samu_plan_greedy.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(C.POINTER(samu_plan))]
@@ -157,6 +162,9 @@ class Samu:
         if rc:
             raise SamuError(rc, lib().samu_last_error(self.h).decode())
 
+    def samu_launch_count(self) -> int:
+        return int(lib().samu_launch_count(self.h))
+
     # ---- registration -------------------------------------------------------------------
     def samu_model_register(self, model_id: int, spec: Dict, bucket_B, coeff, load):
         sp = samu_model_spec(spec["L"], spec["h"], spec["c"], spec["l_max"], spec["tp_mask"], spec["weight_bytes"],
@@ -190,6 +198,15 @@ class Samu:
             self.samu_model_register(m, spec, w.coeff_B, w.coeff[m], w.load[m])
             self.samu_ecdf_load(m, w.ecdf_values[m], w.ecdf_cum[m])
         self.samu_app_load(w.engine, w.node_model, w.l_in_base, w.cap_y, w.pred, w.node, w.chain)
+
+    def samu_enumerate_plans(self, node: int):
+        n = lib().samu_enumerate_plans(self.h, node, None, None, 0)
+        if n < 0:
+            self._check(n)
+        dp = np.zeros(max(n, 1), np.int32)
+        tp = np.zeros(max(n, 1), np.int32)
+        lib().samu_enumerate_plans(self.h, node, _np_ptr(dp), _np_ptr(tp), n)
+        return list(zip(dp[:n].tolist(), tp[:n].tolist()))
 
     # ---- hot path -----------------------------------------------------------------------
     def samu_sample_lengths(self, seed: int, trial_begin: int, n_trials: int, out=None):

@@ -22,7 +22,7 @@ __device__ __forceinline__ void add128(uint64_t& hi, uint64_t& lo, uint64_t bhi,
 // model result per trial: max over replicas of the end clock, sums of the rest;
 // a model whose requests were all done before the call has T = 0 and no load (c28)
 __global__ void k_combine(const samu_trial_rec* __restrict__ rep, const DevCand* __restrict__ cands, int32_t n_cands,
-                          int32_t T, samu_trial_rec* __restrict__ out, double* over, int32_t n_nodes) {
+                          int32_t T, double* over, int32_t n_nodes) {
   const int32_t x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= n_cands * T) return;
   const int32_t c = x / T, k = x % T;
@@ -50,7 +50,7 @@ __global__ void k_combine(const samu_trial_rec* __restrict__ rep, const DevCand*
     o.t_end = t; o.flops_lo = lo; o.flops_hi = hi; o.req_iters = ri; o.iters = it; o.flags = done | (cut << 1);
     if (ov) for (int j = C.dp; j < 16; ++j) ov[j] = 0.0;
   }
-  out[x] = o;
+  C.out_rec[k] = o;
 }
 
 // per-candidate summary over T trials: sequential mean, nearest-rank percentiles via an
@@ -182,10 +182,10 @@ __global__ void k_stage_score(const samu_trial_rec* __restrict__ cache, int32_t 
 }  // namespace
 
 cudaError_t launch_combine(const samu_trial_rec* rep_rec, const DevCand* cands, int32_t n_cands, int32_t n_trials,
-                           samu_trial_rec* out, double* over, int32_t n_nodes, cudaStream_t s) {
+                           double* over, int32_t n_nodes, cudaStream_t s) {
   const int32_t tot = n_cands * n_trials;
   if (!tot) return cudaSuccess;
-  k_combine<<<(tot + 127) / 128, 128, 0, s>>>(rep_rec, cands, n_cands, n_trials, out, over, n_nodes);
+  k_combine<<<(tot + 127) / 128, 128, 0, s>>>(rep_rec, cands, n_cands, n_trials, over, n_nodes);
   return cudaGetLastError();
 }
 

@@ -91,6 +91,7 @@ struct samu_ctx {
 
   // stats
   int64_t n_sims = 0;
+  uint64_t launches = 0;          // kernels launched by this context
   uint64_t req_iters = 0;
 };
 
@@ -132,6 +133,11 @@ struct samu_ctx {
     samu_status r_ = (x);      \
     if (r_ != SAMU_OK) return r_; \
   } while (0)
+
+static inline cudaError_t samu_count(samu_ctx* c, cudaError_t e) {
+  c->launches += 1;
+  return e;
+}
 
 template <class T>
 static cudaError_t upload(DevBuf& b, const std::vector<T>& v, cudaStream_t s) {
@@ -217,6 +223,8 @@ extern "C" void samu_ctx_destroy(samu_ctx* c) {
 }
 
 extern "C" const char* samu_last_error(const samu_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+extern "C" uint64_t samu_launch_count(const samu_ctx* c) { return c ? c->launches : 0; }
 
 // ---------------------------------------------------------------------------------------------
 // C ABI: registration
@@ -376,7 +384,7 @@ extern "C" samu_status samu_app_load(samu_ctx* c, const samu_engine_cfg* engine,
       CK(c, upload(cs, part, s));
       DevBuf& out = c->coef[{m, slot}];
       CK(c, out.ensure(sizeof(double) * 6 * e.max_num_seqs));
-      CK(c, launch_dense_coeff(bb.as<uint32_t>(), nb, cs.as<double>(), e.max_num_seqs, out.as<double>(), s));
+      CK(c, samu_count(c, launch_dense_coeff(bb.as<uint32_t>(), nb, cs.as<double>(), e.max_num_seqs, out.as<double>(), s)));
       CK(c, cudaStreamSynchronize(s));
     }
   }
@@ -384,6 +392,15 @@ extern "C" samu_status samu_app_load(samu_ctx* c, const samu_engine_cfg* engine,
   c->rep_off_host.clear();
   c->app_loaded = true;
   return SAMU_OK;
+}
+
+extern "C" int32_t samu_enumerate_plans(samu_ctx* c, int32_t node, int32_t* dp, int32_t* tp, int32_t cap) {
+  GUARD(c);
+  if (!c->app_loaded || node < 0 || node >= c->n_nodes || cap < 0 || (cap && (!dp || !tp)))
+    FAIL(c, SAMU_E_INVALID, "enumerate_plans: bad arguments");
+  auto pl = plans_of(c, c->node_model[node]);
+  for (int i = 0; i < (int)pl.size() && i < cap; ++i) { dp[i] = pl[i].first; tp[i] = pl[i].second; }
+  return (int32_t)pl.size();
 }
 
 static DevApp dev_app(const samu_ctx* c) {
@@ -440,8 +457,8 @@ extern "C" samu_status samu_sample_lengths(samu_ctx* c, uint64_t seed, int32_t t
   e.model_of_node = c->d_mnode.as<int32_t>();
   e.l_max_of_node = c->d_lmax.as<uint32_t>();
   for (size_t w = 0; w < c->waves.size(); ++w)
-    CK(c, launch_sample(a, e, c->d_waves[w].as<int32_t>(), (int32_t)c->waves[w].size(), seed, trial_begin, n_trials,
-                        out_l_out, out_l_in_eff, c->stream));
+    CK(c, samu_count(c, launch_sample(a, e, c->d_waves[w].as<int32_t>(), (int32_t)c->waves[w].size(), seed, trial_begin, n_trials,
+                        out_l_out, out_l_in_eff, c->stream)));
   return SAMU_OK;
 }
 
@@ -512,6 +529,7 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
       D.tau_rec = J.tau_rec;
       D.fin_t_out = J.fin_t_out;
       D.fin_iter_out = J.fin_iter_out;
+      D.out_rec = J.out_rec;
       const std::vector<uint32_t>& ho = c->rep_off_host.at({node, cd.dp});
       uint32_t mx = 0;
       for (int j = 0; j < cd.dp; ++j) mx = std::max(mx, ho[j + 1] - ho[j]);
@@ -563,9 +581,8 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
     L.error = c->d_error.as<int32_t>();
     CK(c, launch_simulate(L, n_blocks, s));
     // combine replicas into the per-(candidate, trial) records
-    for (size_t x = 0; x < idx.size(); ++x) {
-      CK(c, launch_combine(L.rep_rec + x * T * 16, L.cands + x, 1, T, jobs[idx[x]].out_rec, S.over, c->n_nodes, s));
-    }
+    CK(c, launch_combine(L.rep_rec, L.cands, (int32_t)idx.size(), T, S.over, c->n_nodes, s));
+    c->launches += 2;
     c->n_sims += (int64_t)idx.size() * T;
     int32_t herr[2] = {0, 0};
     CK(c, cudaMemcpyAsync(herr, c->d_error.p, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
@@ -712,7 +729,7 @@ extern "C" samu_status samu_simulate_batch(samu_ctx* c, const samu_candidate* ca
     }
     DevBuf dsum;
     CK(c, dsum.ensure(sizeof(samu_cand_summary) * n_cands));
-    CK(c, launch_summary(all, n_cands, T_total, dsum.as<samu_cand_summary>(), c->stream));
+    CK(c, samu_count(c, launch_summary(all, n_cands, T_total, dsum.as<samu_cand_summary>(), c->stream)));
     CK(c, cudaMemcpyAsync(out_summary, dsum.p, sizeof(samu_cand_summary) * n_cands, cudaMemcpyDeviceToHost, c->stream));
     CK(c, cudaStreamSynchronize(c->stream));
   }
@@ -950,7 +967,7 @@ struct Greedy {
         RET(flush());
         CK(c, upload(d_sc, sc, s));
         CK(c, d_out.ensure(sizeof(StageOut) * nc));
-        CK(c, launch_fstar(cache.as<samu_trial_rec>(), T, d_sc.as<StageCand>(), nc, d_out.as<StageOut>(), s));
+        CK(c, samu_count(c, launch_fstar(cache.as<samu_trial_rec>(), T, d_sc.as<StageCand>(), nc, d_out.as<StageOut>(), s)));
         std::vector<StageOut> so(nc);
         CK(c, cudaMemcpyAsync(so.data(), d_out.p, sizeof(StageOut) * nc, cudaMemcpyDeviceToHost, s));
         CK(c, cudaStreamSynchronize(s));
@@ -961,8 +978,8 @@ struct Greedy {
         }
         RET(flush());
         CK(c, upload(d_sc, sc, s));
-        CK(c, launch_stage_score(cache.as<samu_trial_rec>(), T, d_sc.as<StageCand>(), nc, d_out.as<StageOut>(), TE_star,
-                                 g_star, d_best.as<int32_t>(), reinterpret_cast<double*>(d_best.as<char>() + 8), s));
+        CK(c, samu_count(c, launch_stage_score(cache.as<samu_trial_rec>(), T, d_sc.as<StageCand>(), nc, d_out.as<StageOut>(), TE_star,
+                                 g_star, d_best.as<int32_t>(), reinterpret_cast<double*>(d_best.as<char>() + 8), s)));
         evals += nc;
         int32_t best = -1;
         double maxdT = 0.0;
@@ -1008,7 +1025,7 @@ struct Greedy {
         jobs[i].phase = d;
       }
       RET(run_jobs(c, jobs, lo.as<uint16_t>(), li.as<uint16_t>(), Tl, S));
-      CK(c, launch_rebase(st.as<uint32_t>(), fin_t.as<double>(), (int64_t)Tl * n, rec(fslot) + tb, (int32_t)n, s));
+      CK(c, samu_count(c, launch_rebase(st.as<uint32_t>(), fin_t.as<double>(), (int64_t)Tl * n, rec(fslot) + tb, (int32_t)n, s)));
       samu_plan_stage& PS = plan->stages[plan->n_stages++];
       PS.n_entries = (int)Es.size();
       for (size_t i = 0; i < Es.size(); ++i) { PS.node[i] = Es[i].node; PS.dp[i] = Es[i].dp; PS.tp[i] = Es[i].tp; }
@@ -1029,7 +1046,7 @@ struct Greedy {
     int32_t* red = any + (size_t)c->n_nodes * std::max(Tl, 1);
     std::vector<int32_t> h((size_t)c->n_nodes * std::max(Tl, 1), 0), flag(c->n_nodes, 0);
     if (Tl) {
-      CK(c, launch_node_done(st.as<uint32_t>(), Tl, (int32_t)n, c->d_node.as<int32_t>(), any, c->n_nodes, s));
+      CK(c, samu_count(c, launch_node_done(st.as<uint32_t>(), Tl, (int32_t)n, c->d_node.as<int32_t>(), any, c->n_nodes, s)));
       CK(c, cudaMemcpyAsync(h.data(), any, sizeof(int32_t) * h.size(), cudaMemcpyDeviceToHost, s));
       CK(c, cudaStreamSynchronize(s));
       for (int v = 0; v < c->n_nodes; ++v)

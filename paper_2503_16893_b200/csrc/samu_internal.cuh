@@ -47,6 +47,7 @@ struct DevCand {
   const samu_trial_rec* tau_rec;  // [T] take tau_k = tau_rec[k].t_end (f* of a stage), or null
   double* fin_t_out;           // [T][n] or null
   uint32_t* fin_iter_out;      // [T][n] or null
+  samu_trial_rec* out_rec;     // [T] per-(candidate, trial) records (after the replica combine)
 };
 
 struct SimLaunch {
@@ -81,7 +82,7 @@ cudaError_t launch_simulate(const SimLaunch& L, int32_t n_blocks, cudaStream_t s
 cudaError_t simulate_prepare(int* blocks_per_sm);
 int32_t simulate_smem_bytes();
 cudaError_t launch_combine(const samu_trial_rec* rep_rec, const DevCand* cands, int32_t n_cands, int32_t n_trials,
-                           samu_trial_rec* out, double* over, int32_t n_nodes, cudaStream_t s);
+                           double* over, int32_t n_nodes, cudaStream_t s);
 cudaError_t launch_summary(const samu_trial_rec* recs, int32_t n_cands, int32_t n_trials,
                            samu_cand_summary* out, cudaStream_t s);
 cudaError_t launch_rebase(uint32_t* st, double* fin_t, int64_t n_total, const samu_trial_rec* fstar_rec,
