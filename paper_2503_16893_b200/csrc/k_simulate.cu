@@ -1,19 +1,20 @@
 // K2: iteration-level continuous-batching simulation (readings c3-c9,
-// c13, c15, c18, c19, c24, c25), one warp per (candidate, trial, dp replica).
+// c13, c15, c18, c19, c23-c25), one warp per (candidate, trial, dp replica).
 //
 // Design (B200-first, not a translation of the per-request oracle loop):
 //  * persistent grid, one work item per warp, pulled from an atomic counter over a host-sorted
 //    longest-first item list (replica-sims differ ~100x in length);
-//  * the running set lives in shared memory: 256 slots, lane L owns slots L + 32 j, so slot
-//    scans are bank-conflict free;
-//  * the per-iteration state is O(1): B, S = sum(l), s = d + max(l - d), the exact KV-block need
-//    of decode step d comes from a histogram over (l - 1 - d) mod bs (every running request
-//    advances one token per decode, so its phase is fixed at admission); finishes are events at
-//    the minimum finish decode-index — a uniform decode iteration touches no request;
-//  * admission is a warp prefix-scan over the next 32 queue heads (tokens and KV blocks), retire
-//    is a slot scan + REDUX reductions only at finish events;
-//  * Eq. prefill / decode FLOPs are exact u64 (u128 sums); the latency is evaluated in fp64 with
-//    explicit round-to-nearest intrinsics (no contraction) in the contract's order (c24).
+//  * the running set lives in shared memory: 256 slots, lane L owns slots L + 32 j (bank-conflict
+//    free), with the lane's occupancy bits in a register;
+//  * between events every running request advances one token per decode, so a "decode run" has
+//    fixed B while S and B*s grow by B per iteration and the KV-block need of decode d follows
+//    from a histogram over the request phases (l - 1 - d) mod bs fixed at admission.  The run
+//    evaluates the contract's per-iteration latency sum in fp64 — every iteration is visited
+//    (c23) — while FLOPs (u128), request-iterations and block counts of the run are folded in
+//    exact integer closed form;
+//  * events (admission = prefill iteration, finish, preemption) are warp-cooperative: admission
+//    is a warp prefix-scan over the next 32 queue heads (tokens, KV blocks), retirement a slot
+//    scan + ballot / REDUX reductions.
 #include "samu_internal.cuh"
 
 #include <math_constants.h>
@@ -24,17 +25,16 @@ constexpr uint32_t FULL = 0xFFFFFFFFu;
 constexpr int SLOTS = 256;
 
 struct WarpSm {
-  uint32_t s_req[SLOTS];     // request id, SAMU_EMPTY if free
-  uint32_t s_fin[SLOTS];     // decode index at which it finishes
-  int32_t s_o[SLOTS];        // l - d (constant while running)
+  uint32_t s_req[SLOTS];     // request id of an occupied slot
+  int2 s_fo[SLOTS];          // (decode index at which it finishes, l - d)
   uint32_t s_meta[SLOTS];    // admission rank << 5 | phase  (phase = (o - 1) mod bs)
   uint32_t stk_req[SLOTS];   // preempted stack, top = front of W
   uint32_t stk_g[SLOTS];
   uint32_t tmp[SLOTS];       // finished requests of the current iteration / radix histogram
-  uint32_t tmp2[SLOTS];      // released successors
+  uint32_t tmp2[SLOTS];      // staging / released successors
   uint32_t hist[32];         // running requests per phase
-  uint32_t adm_req[32], adm_fin[32], adm_meta[32];
-  int32_t adm_o[32];
+  uint32_t adm_req[32], adm_meta[32];
+  int2 adm_fo[32];
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -61,19 +61,26 @@ __device__ __forceinline__ double kdouble(uint64_t k) {
   return __longlong_as_double((long long)b);
 }
 
-__device__ __forceinline__ uint32_t cdiv(uint32_t a, uint32_t b) { return (a + b - 1) / b; }
-
-__device__ __forceinline__ uint32_t posmod(int32_t a, uint32_t m) {
-  const int32_t r = a % (int32_t)m;
-  return (uint32_t)(r < 0 ? r + (int32_t)m : r);
-}
+// block-size arithmetic with a power-of-two fast path (bs = 16 by default, reading c5)
+struct Bs {
+  uint32_t v, mask, shift;
+  bool pow2;
+  __device__ __forceinline__ uint32_t mod(uint32_t x) const { return pow2 ? (x & mask) : x % v; }
+  __device__ __forceinline__ uint32_t div(uint32_t x) const { return pow2 ? (x >> shift) : x / v; }
+  __device__ __forceinline__ uint32_t cdiv(uint32_t x) const { return div(x + v - 1); }
+  __device__ __forceinline__ uint32_t posmod(int32_t a) const {
+    if (pow2) return (uint32_t)a & mask;
+    const int32_t r = a % (int32_t)v;
+    return (uint32_t)(r < 0 ? r + (int32_t)v : r);
+  }
+};
 
 // Eq. per-iter cost, reading c24: ((fma_c + fma_p) + fma_s), exact integer -> RN
 __device__ __forceinline__ double iter_cost(const double* __restrict__ coef, uint32_t ms, uint32_t B, uint64_t F,
-                                            uint32_t Bs, uint32_t S) {
+                                            uint32_t Bs_, uint32_t S) {
   const double* cb = coef + (B - 1);
   const double tc = __fma_rn(__ldg(cb), __ull2double_rn(F), __ldg(cb + ms));
-  const double tp = __fma_rn(__ldg(cb + 2 * ms), __uint2double_rn(Bs), __ldg(cb + 3 * ms));
+  const double tp = __fma_rn(__ldg(cb + 2 * ms), __uint2double_rn(Bs_), __ldg(cb + 3 * ms));
   const double ts = __fma_rn(__ldg(cb + 4 * ms), __uint2double_rn(S), __ldg(cb + 5 * ms));
   return __dadd_rn(__dadd_rn(tc, tp), ts);
 }
@@ -83,14 +90,13 @@ __device__ __forceinline__ void set_error(int32_t* e, int32_t code, int32_t site
 }
 
 struct Sim {
-  // uniform scalar state
+  // warp-uniform scalar state
   double t, tau, next_ready;
   uint64_t fl_lo, fl_hi, reqit;
   uint32_t iter, d, needidx, B, S, next_fin, next_rank;
   int32_t F, maxO;
   uint32_t stack_cnt, q_head, q_tail, n_heads, n_front, pend_ptr, n_pend;
-  int32_t err;
-  int32_t site;
+  int32_t err, site;
 };
 
 __device__ __forceinline__ void add_flops(Sim& m, uint64_t f) {
@@ -100,21 +106,20 @@ __device__ __forceinline__ void add_flops(Sim& m, uint64_t f) {
 }
 
 // rescan the running set: next finish index and max(l - d)
-__device__ __forceinline__ void rescan(WarpSm& W, Sim& m, int lane) {
+__device__ __forceinline__ void rescan(const WarpSm& W, Sim& m, int lane, uint32_t occ) {
   uint32_t mn = FULL;
   int32_t mx = INT_MIN;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    const int s = lane + 32 * j;
-    if (W.s_req[s] != SAMU_EMPTY) {
-      mn = min(mn, W.s_fin[s]);
-      mx = max(mx, W.s_o[s]);
+    if ((occ >> j) & 1u) {
+      const int2 fo = W.s_fo[lane + 32 * j];
+      mn = min(mn, (uint32_t)fo.x);
+      mx = max(mx, fo.y);
     }
   }
   m.next_fin = __reduce_min_sync(FULL, mn);
   m.maxO = __reduce_max_sync(FULL, mx);
 }
-
 
 // Stable LSD radix sort of n (key, idx) pairs by the 64-bit key (8 passes of 8 bits, passes where
 // every key shares the digit are skipped), one warp, 256-bin histogram in shared memory.
@@ -195,7 +200,12 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
     uint32_t* fio = C.fin_iter_out ? C.fin_iter_out + tb : nullptr;
     double* over = P.over ? P.over + ((size_t)k * A.n_nodes + C.node) * 16 : nullptr;
     const uint32_t r0 = C.rep_off[j], r1 = C.rep_off[j + 1];
-    const uint32_t bs = C.bs, ms = C.max_seqs;
+    const uint32_t ms = C.max_seqs;
+    Bs bs;
+    bs.v = C.bs;
+    bs.pow2 = (C.bs & (C.bs - 1)) == 0;
+    bs.mask = C.bs - 1;
+    bs.shift = __ffs(C.bs) - 1;
     const bool commit = C.commit && st;
 
     Sim m;
@@ -205,10 +215,9 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
     m.iter = 0; m.d = 0; m.needidx = 0; m.B = 0; m.S = 0; m.next_rank = 0;
     m.F = C.blocks; m.maxO = INT_MIN; m.next_fin = FULL;
     m.stack_cnt = 0; m.q_head = 0; m.q_tail = 0; m.n_heads = 0; m.n_front = 0; m.pend_ptr = 0; m.n_pend = 0;
-    m.err = 0;
-    m.site = 0;
+    m.err = 0; m.site = 0;
+    uint32_t occ = 0;   // this lane's occupied slots (bit j = slot lane + 32 j)
 
-    for (int s = lane; s < SLOTS; s += 32) W.s_req[s] = SAMU_EMPTY;
     W.hist[lane] = 0;
     __syncwarp();
 
@@ -257,9 +266,11 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
         if (pos < (uint32_t)P.max_p) { pkey[pos] = dkey(ready); pidx[pos] = r; }
       }
       m.n_pend += __popc(bp);
-      n_run += __popc(__ballot_sync(FULL, valid && s == SAMU_ST_RUNNING));
-      n_pre += __popc(__ballot_sync(FULL, valid && s == SAMU_ST_PREEMPTED));
-      n_q += __popc(__ballot_sync(FULL, valid && s == SAMU_ST_QUEUED));
+      if (bc) {
+        n_run += __popc(__ballot_sync(FULL, valid && s == SAMU_ST_RUNNING));
+        n_pre += __popc(__ballot_sync(FULL, valid && s == SAMU_ST_PREEMPTED));
+        n_q += __popc(__ballot_sync(FULL, valid && s == SAMU_ST_QUEUED));
+      }
       if (__ballot_sync(FULL, valid && s != SAMU_ST_DONE)) all_done = false;
     }
     m.site = (int32_t)__reduce_max_sync(FULL, (uint32_t)m.site);
@@ -284,9 +295,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
       if (n_cls) {
         // carried entries in (class, rank / seq, index) order (the oracle's sorted pairs)
         uint32_t* sorted_idx;
-        const uint64_t* sorted = warp_radix_sort(skey, sidx, skey + P.max_p, sidx + P.max_p, n_cls, W.tmp, lane,
-                                                 &sorted_idx);
-        (void)sorted;
+        warp_radix_sort(skey, sidx, skey + P.max_p, sidx + P.max_p, n_cls, W.tmp, lane, &sorted_idx);
         int32_t used = 0;
         uint32_t S0 = 0;
         const uint32_t q_base = m.n_front + m.n_heads;
@@ -294,20 +303,19 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
           const uint32_t r = sorted_idx[i];
           if (i < m.n_front) q[i] = r;
           else if (i < m.n_front + n_q) q[q_base + (i - m.n_front)] = r;
-          else {   // resume: running requests keep their slots in admission order
+          else {   // resume: running requests keep their admission order in slots 0..B-1
             const uint32_t jx = i - m.n_front - n_q;
             const uint32_t g = gst[r];
             const uint32_t lin = li[r];
             const uint32_t Lr = max((uint32_t)lo[r], 1u);
             const int32_t o = (int32_t)(lin + g);
-            const uint32_t ph = posmod(o - 1, bs);
+            const uint32_t ph = bs.posmod(o - 1);
             if (g >= Lr || g == 0) { m.err = SAMU_E_STATE; m.site = 5; }
             W.s_req[jx] = r;
-            W.s_fin[jx] = Lr - g;
-            W.s_o[jx] = o;
+            W.s_fo[jx] = make_int2((int32_t)(Lr - g), o);
             W.s_meta[jx] = (jx << 5) | ph;
             atomicAdd(&W.hist[ph], 1u);
-            used += (int32_t)cdiv(lin + g - 1, bs);
+            used += (int32_t)bs.cdiv(lin + g - 1);
             S0 += lin + g;
           }
         }
@@ -321,11 +329,14 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
           m.F -= used;
           m.next_rank = n_run;
           if (m.F < 0) { m.err = SAMU_E_STATE; m.site = 8; }
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj)
+            if ((uint32_t)(lane + 32 * jj) < n_run) occ |= 1u << jj;
         }
       }
     }
     __syncwarp();
-    if (m.B) rescan(W, m, lane);
+    if (m.B) rescan(W, m, lane, occ);
 
     // ---- pending cross-node arrivals in (ready, index) order: stable LSD radix sort ----
     const uint64_t* pk = pkey;
@@ -337,18 +348,19 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
     }
     m.next_ready = m.n_pend ? kdouble(pk[0]) : CUDART_INF;
     const uint64_t K1 = 2ull * C.L * C.h_tp;
+    const uint64_t LC = (uint64_t)C.L * C.c;
     bool cut = false;
 
     // ---- main loop (c25) ----
     while (!m.err) {
       if (m.t >= m.tau) { cut = true; break; }
-      // (2) pending cross-node arrivals with ready <= t join the back of W
+      // pending cross-node arrivals with ready <= t join the back of W
       while (m.pend_ptr < m.n_pend && m.next_ready <= m.t) {
         const uint32_t i = m.pend_ptr + lane;
         const bool ok = i < m.n_pend && kdouble(pk[i]) <= m.t;
         const uint32_t b = __ballot_sync(FULL, ok);
         const uint32_t cnt = (b == FULL) ? 32u : (uint32_t)(__ffs(~b) - 1);
-        if (lane < cnt) q[m.q_tail + lane] = pi[i];
+        if ((uint32_t)lane < cnt) q[m.q_tail + lane] = pi[i];
         m.q_tail += cnt;
         m.pend_ptr += cnt;
         m.next_ready = m.pend_ptr < m.n_pend ? kdouble(pk[m.pend_ptr]) : CUDART_INF;
@@ -358,20 +370,20 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
         if (m.pend_ptr < m.n_pend && m.next_ready != CUDART_INF) { m.t = m.next_ready; continue; }
         break;
       }
-      // head of W fits? (slots, token budget, blocks)
+      // does the head of W fit? (slots, token budget, blocks)
       bool fits = false;
       if (wnon && m.B < ms) {
         uint32_t hr, hg;
         if (m.stack_cnt) { hr = W.stk_req[m.stack_cnt - 1]; hg = W.stk_g[m.stack_cnt - 1]; }
         else { hr = q[m.q_head]; hg = m.q_head < m.n_front ? (uint32_t)gst[hr] : 0u; }
         const uint32_t p = (uint32_t)li[hr] + hg;
-        fits = p <= C.budget && (int32_t)cdiv(p, bs) <= m.F;
+        fits = p <= C.budget && (int32_t)bs.cdiv(p) <= m.F;
       }
       uint32_t n_fin = 0;
       if (fits) {
         // ================= prefill iteration (c8): admit a strict FCFS prefix of W =========
-        uint32_t k_adm = 0, tok = 0, smaxp = 0, S_add = 0, n_stay = 0;
-        int32_t blk = 0, freed = 0;
+        uint32_t k_adm = 0, tok = 0, smaxp = 0, S_add = 0, n_stay = 0, mn_new = FULL;
+        int32_t blk = 0, freed = 0, mx_new = INT_MIN;
         for (;;) {
           const uint32_t avail = m.stack_cnt + (m.q_tail - m.q_head);
           if (avail == 0) break;
@@ -384,7 +396,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
             if (qp < m.n_front) g = gst[r];   // recompute front keeps its generated tokens
           }
           const uint32_t p = valid ? (uint32_t)li[r] + g : 0u;
-          const uint32_t nb = valid ? cdiv(p, bs) : 0u;
+          const uint32_t nb = valid ? bs.cdiv(p) : 0u;
           const uint32_t sp = warp_incl_scan(p, lane), sb = warp_incl_scan(nb, lane);
           const bool ok = valid && (m.B + k_adm + lane + 1 <= ms) && (tok + sp <= C.budget) &&
                           ((int32_t)(blk + sb) <= m.F);
@@ -395,43 +407,44 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
           const uint32_t Lr = adm ? max((uint32_t)lo[r], 1u) : 0u;
           const bool finish_now = adm && g + 1 >= Lr;
           const bool stay = adm && !finish_now;
-          // stage stays (admission order) and immediate finishers
           const uint32_t bst = __ballot_sync(FULL, stay);
           const uint32_t bfn = __ballot_sync(FULL, finish_now);
+          int32_t fin_i = 0, o = 0;
           if (stay) {
             const uint32_t a = __popc(bst & lanemask_lt());
-            const int32_t o = (int32_t)(p + 1) - (int32_t)m.d;
-            const uint32_t ph = posmod((int32_t)p - (int32_t)m.d, bs);
+            o = (int32_t)(p + 1) - (int32_t)m.d;
+            fin_i = (int32_t)(m.d + (Lr - (g + 1)));
+            const uint32_t ph = bs.posmod((int32_t)p - (int32_t)m.d);
             W.adm_req[a] = r;
-            W.adm_fin[a] = m.d + (Lr - (g + 1));
-            W.adm_o[a] = o;
+            W.adm_fo[a] = make_int2(fin_i, o);
             W.adm_meta[a] = ((m.next_rank + k_adm + lane) << 5) | ph;
             atomicAdd(&W.hist[ph], 1u);
           }
           if (finish_now) W.tmp[n_fin + __popc(bfn & lanemask_lt())] = r;
           n_fin += __popc(bfn);
           const uint32_t ns = __popc(bst);
-          freed += (int32_t)__reduce_add_sync(FULL, finish_now ? nb : 0u);
-          S_add += __reduce_add_sync(FULL, stay ? p + 1 : 0u);
+          if (bfn) freed += (int32_t)__reduce_add_sync(FULL, finish_now ? nb : 0u);
+          if (bst) {
+            S_add += __reduce_add_sync(FULL, stay ? p + 1 : 0u);
+            mn_new = min(mn_new, __reduce_min_sync(FULL, stay ? (uint32_t)fin_i : FULL));
+            mx_new = max(mx_new, __reduce_max_sync(FULL, stay ? o : INT_MIN));
+          }
           smaxp = max(smaxp, __reduce_max_sync(FULL, adm ? p : 0u));
           __syncwarp();
-          // insert stays into free slots: lane L fills admitted ordinals [ex, ex + nfree)
+          // insert the stays into free slots: lane L fills admitted ordinals [ex, ex + nfree)
           if (ns) {
-            uint32_t freemask = 0;
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj)
-              if (W.s_req[lane + 32 * jj] == SAMU_EMPTY) freemask |= 1u << jj;
-            const uint32_t nf = __popc(freemask);
+            uint32_t fm = ~occ & 0xFFu;
+            const uint32_t nf = __popc(fm);
             const uint32_t ex = warp_incl_scan(nf, lane) - nf;
             uint32_t a = ex;
-            while (freemask && a < ns) {
-              const int jj = __ffs(freemask) - 1;
-              freemask &= freemask - 1;
+            while (fm && a < ns) {
+              const int jj = __ffs(fm) - 1;
+              fm &= fm - 1;
               const int s = lane + 32 * jj;
               W.s_req[s] = W.adm_req[a];
-              W.s_fin[s] = W.adm_fin[a];
-              W.s_o[s] = W.adm_o[a];
+              W.s_fo[s] = W.adm_fo[a];
               W.s_meta[s] = W.adm_meta[a];
+              occ |= 1u << jj;
               ++a;
             }
             __syncwarp();
@@ -448,7 +461,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
         m.F -= blk;
         // Eq. prefill FLOPs: L (c B s + 2 B h s^2 / tp)
         const uint64_t Bp = k_adm, sp64 = smaxp;
-        const uint64_t fl = (uint64_t)C.L * (C.c * Bp * sp64 + 2ull * Bp * C.h_tp * sp64 * sp64);
+        const uint64_t fl = LC * Bp * sp64 + (uint64_t)C.L * 2ull * Bp * C.h_tp * sp64 * sp64;
         const double lat = iter_cost(C.coef, ms, k_adm, fl, k_adm * smaxp, tok);
         m.t = __dadd_rn(m.t, lat);
         add_flops(m, fl);
@@ -458,109 +471,171 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
         m.B += n_stay;
         m.S += S_add;
         m.next_rank += k_adm;
-        if (n_stay) rescan(W, m, lane);
+        m.next_fin = min(m.next_fin, mn_new);
+        m.maxO = max(m.maxO, mx_new);
       } else {
         if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; m.site = 9; break; }
         // ================= decode run (c9): uniform iterations until an event ===============
-        uint32_t B = m.B;
-        uint64_t K0 = (uint64_t)C.L * C.c * B;
-        uint32_t smax = (uint32_t)((int32_t)m.d + m.maxO);
+        const uint32_t B = m.B;
         const double stop_t = fmin(m.tau, m.next_ready);
-        bool event = false;
-        for (;;) {
-          uint32_t need = W.hist[m.needidx];
-          if ((int32_t)need > m.F) {
-            // recompute preemption of the last admitted request (c7)
-            while ((int32_t)need > m.F) {
-              uint32_t best = 0;
-              int bslot = -1;
-#pragma unroll
-              for (int jj = 0; jj < 8; ++jj) {
-                const int s = lane + 32 * jj;
-                if (W.s_req[s] != SAMU_EMPTY && (bslot < 0 || W.s_meta[s] > best)) { best = W.s_meta[s]; bslot = s; }
-              }
-              const uint32_t vmeta = __reduce_max_sync(FULL, bslot >= 0 ? best : 0u);
-              const uint32_t own = __ballot_sync(FULL, bslot >= 0 && best == vmeta);
-              const int ol = __ffs(own) - 1;
-              const int vs = __shfl_sync(FULL, bslot, ol);
-              const uint32_t vr = W.s_req[vs];
-              const int32_t vo = W.s_o[vs];
-              const uint32_t vph = vmeta & 31u;
-              const uint32_t l = (uint32_t)(vo + (int32_t)m.d);
-              m.F += (int32_t)cdiv(l - 1, bs);
-              if (vph == m.needidx) --need;
-              __syncwarp();
-              if (lane == 0) {
-                W.hist[vph] -= 1;
-                W.s_req[vs] = SAMU_EMPTY;
-                W.stk_req[m.stack_cnt] = vr;
-                W.stk_g[m.stack_cnt] = l - (uint32_t)li[vr];
-              }
-              __syncwarp();
-              m.stack_cnt += 1;
-              m.B -= 1;
-              m.S -= l;
-              if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; m.site = 10; break; }
-            }
-            if (m.err) break;
-            rescan(W, m, lane);
-            B = m.B;
-            K0 = (uint64_t)C.L * C.c * B;
-            smax = (uint32_t)((int32_t)m.d + m.maxO);
-            event = true;   // W changed: re-check admission after this iteration
+        // KV need of the run's decodes: histogram rotated to start at needidx, prefix sums
+        const uint32_t hv = (uint32_t)lane < bs.v ? W.hist[bs.mod(m.needidx + bs.v - (uint32_t)lane)] : 0u;
+        const uint32_t pre = warp_incl_scan(hv, lane);
+        const uint32_t m_fin = m.next_fin - m.d;
+        uint32_t i_pre = 0x7fffffffu;   // first run iteration that must preempt
+        {
+          const uint32_t F0 = (uint32_t)m.F;
+          // each bs decodes need exactly B blocks: skip the search when the run cannot run out
+          if ((uint64_t)F0 < (uint64_t)B * ((uint64_t)bs.div(m_fin) + 1)) {
+            const uint32_t q0 = F0 / B, rem = F0 - q0 * B;
+            const uint32_t bad = __ballot_sync(FULL, (uint32_t)lane < bs.v && pre > rem);
+            const uint64_t ip = (uint64_t)q0 * bs.v + (uint32_t)(__ffs(bad) - 1);
+            i_pre = ip > 0x7fffffffull ? 0x7fffffffu : (uint32_t)ip;
           }
-          m.F -= (int32_t)need;
-          // Eq. decode FLOPs: L (c B + 2 h S / tp)
-          const uint64_t fl = K0 + K1 * (uint64_t)m.S;
-          const double lat = iter_cost(C.coef, ms, B, fl, B * smax, m.S);
-          m.t = __dadd_rn(m.t, lat);
-          add_flops(m, fl);
-          m.reqit += B;
-          m.iter += 1;
-          m.S += B;
-          smax += 1;
-          m.d += 1;
-          m.needidx = m.needidx == 0 ? bs - 1 : m.needidx - 1;
-          if (m.d == m.next_fin) {
-            // retire the finishers (ballot / REDUX over the slot scan)
-            uint32_t mn = FULL, cnt = 0, sfin_l = 0;
-            int32_t mx = INT_MIN, fr = 0;
+        }
+        const uint32_t m_run = min(m_fin, i_pre);
+        uint32_t done_it = 0;
+        if (m_run > 0) {
+          const uint64_t K0 = LC * B;
+          const uint32_t smax0 = (uint32_t)((int32_t)m.d + m.maxO);
+          const double* cb = C.coef + (B - 1);
+          const double ac = __ldg(cb), bc = __ldg(cb + ms), ap = __ldg(cb + 2 * ms), bp = __ldg(cb + 3 * ms);
+          const double as_ = __ldg(cb + 4 * ms), bs_ = __ldg(cb + 5 * ms);
+          const uint64_t f_last = K0 + K1 * ((uint64_t)m.S + (uint64_t)B * (m_run - 1));
+          double t = m.t;
+          if (f_last < (1ull << 53)) {
+            // every x of the run is an integer below 2^53: exact fp64 increments == RN conversions
+            double xc = (double)(K0 + K1 * (uint64_t)m.S);
+            const double dxc = (double)(K1 * B), dB = (double)B;
+            double xp = (double)((uint64_t)B * smax0), xs = (double)m.S;
+            uint32_t jj = 0;
+            do {
+              const double tc = __fma_rn(ac, xc, bc);
+              const double tp = __fma_rn(ap, xp, bp);
+              const double ts = __fma_rn(as_, xs, bs_);
+              t = __dadd_rn(t, __dadd_rn(__dadd_rn(tc, tp), ts));
+              xc = __dadd_rn(xc, dxc);
+              xp = __dadd_rn(xp, dB);
+              xs = __dadd_rn(xs, dB);
+              ++jj;
+            } while (jj < m_run && t < stop_t);
+            done_it = jj;
+          } else {
+            uint32_t jj = 0;
+            do {
+              const uint64_t S_j = (uint64_t)m.S + (uint64_t)B * jj;
+              const double tc = __fma_rn(ac, __ull2double_rn(K0 + K1 * S_j), bc);
+              const double tp = __fma_rn(ap, __ull2double_rn((uint64_t)B * (smax0 + jj)), bp);
+              const double ts = __fma_rn(as_, __ull2double_rn(S_j), bs_);
+              t = __dadd_rn(t, __dadd_rn(__dadd_rn(tc, tp), ts));
+              ++jj;
+            } while (jj < m_run && t < stop_t);
+            done_it = jj;
+          }
+          m.t = t;
+          // closed-form exact updates for the done_it iterations of the run
+          const uint64_t mm = done_it;
+          // sum_j (K0 + K1 (S + B j)) = mm K0 + K1 (mm S + B mm (mm - 1) / 2)
+          const uint64_t inner = mm * (uint64_t)m.S + (uint64_t)B * (mm * (mm - 1) / 2);
+          uint64_t lo64 = mm * K0, hi64 = __umul64hi(mm, K0);
+          const uint64_t plo = K1 * inner, phi = __umul64hi(K1, inner);
+          lo64 += plo;
+          hi64 += phi + (lo64 < plo ? 1ull : 0ull);
+          const uint64_t nlo = m.fl_lo + lo64;
+          m.fl_hi += hi64 + (nlo < lo64 ? 1ull : 0ull);
+          m.fl_lo = nlo;
+          m.reqit += (uint64_t)B * mm;
+          m.iter += done_it;
+          const uint32_t rr = bs.mod(done_it);
+          const uint32_t need_sum = bs.div(done_it) * B + (rr ? __shfl_sync(FULL, pre, rr - 1) : 0u);
+          m.F -= (int32_t)need_sum;
+          m.S += B * done_it;
+          m.d += done_it;
+          m.needidx = bs.mod(m.needidx + bs.v - rr);
+        }
+        if (m.d != m.next_fin && done_it == i_pre && !(done_it > 0 && m.t >= stop_t)) {
+          // ---- this decode must preempt (c7): recompute the last admitted requests ----
+          uint32_t need = W.hist[m.needidx];
+          while ((int32_t)need > m.F) {
+            uint32_t best = 0;
+            int bslot = -1;
 #pragma unroll
             for (int jj = 0; jj < 8; ++jj) {
               const int s = lane + 32 * jj;
-              const uint32_t rq = W.s_req[s];
-              if (rq != SAMU_EMPTY) {
-                const uint32_t f = W.s_fin[s];
-                const int32_t o = W.s_o[s];
-                if (f == m.d) {
-                  const uint32_t l_now = (uint32_t)(o + (int32_t)m.d);
-                  fr += (int32_t)cdiv(l_now - 1, bs);
-                  sfin_l += l_now;
-                  atomicSub(&W.hist[W.s_meta[s] & 31u], 1u);
-                  W.s_req[s] = SAMU_EMPTY;
-                  W.tmp2[cnt * 32 + lane] = rq;   // staged per lane (<= 8 each)
-                  ++cnt;
-                } else {
-                  mn = min(mn, f);
-                  mx = max(mx, o);
-                }
+              if (((occ >> jj) & 1u) && (bslot < 0 || W.s_meta[s] > best)) { best = W.s_meta[s]; bslot = s; }
+            }
+            const uint32_t vmeta = __reduce_max_sync(FULL, bslot >= 0 ? best : 0u);
+            const uint32_t own = __ballot_sync(FULL, bslot >= 0 && best == vmeta);
+            const int ol = __ffs(own) - 1;
+            const int vs = __shfl_sync(FULL, bslot, ol);
+            const uint32_t vr = W.s_req[vs];
+            const int32_t vo = W.s_fo[vs].y;
+            const uint32_t vph = vmeta & 31u;
+            const uint32_t l = (uint32_t)(vo + (int32_t)m.d);
+            m.F += (int32_t)bs.cdiv(l - 1);
+            if (vph == m.needidx) --need;
+            __syncwarp();
+            if (lane == ol) {
+              occ &= ~(1u << (vs >> 5));
+              W.hist[vph] -= 1;
+              W.stk_req[m.stack_cnt] = vr;
+              W.stk_g[m.stack_cnt] = l - (uint32_t)li[vr];
+            }
+            __syncwarp();
+            m.stack_cnt += 1;
+            m.B -= 1;
+            m.S -= l;
+            if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; m.site = 10; break; }
+          }
+          if (m.err) break;
+          rescan(W, m, lane, occ);
+          // the preempting decode iteration itself
+          const uint32_t B2 = m.B;
+          const uint32_t smax = (uint32_t)((int32_t)m.d + m.maxO);
+          m.F -= (int32_t)need;
+          const uint64_t fl = LC * B2 + K1 * (uint64_t)m.S;
+          const double lat = iter_cost(C.coef, ms, B2, fl, B2 * smax, m.S);
+          m.t = __dadd_rn(m.t, lat);
+          add_flops(m, fl);
+          m.reqit += B2;
+          m.iter += 1;
+          m.S += B2;
+          m.d += 1;
+          m.needidx = m.needidx == 0 ? bs.v - 1 : m.needidx - 1;
+        }
+        if (m.d == m.next_fin) {
+          // retire the finishers: slot scan over this lane's occupied slots + REDUX reductions
+          uint32_t mn = FULL, cnt = 0, sfin_l = 0;
+          int32_t mx = INT_MIN, fr = 0;
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            if ((occ >> jj) & 1u) {
+              const int s = lane + 32 * jj;
+              const int2 fo = W.s_fo[s];
+              if ((uint32_t)fo.x == m.d) {
+                const uint32_t l_now = (uint32_t)(fo.y + (int32_t)m.d);
+                fr += (int32_t)bs.cdiv(l_now - 1);
+                sfin_l += l_now;
+                atomicSub(&W.hist[W.s_meta[s] & 31u], 1u);
+                occ &= ~(1u << jj);
+                W.tmp2[cnt * 32 + lane] = W.s_req[s];   // staged per lane (<= 8 each)
+                ++cnt;
+              } else {
+                mn = min(mn, (uint32_t)fo.x);
+                mx = max(mx, fo.y);
               }
             }
-            // compact finished ids into tmp in lane-major order
-            const uint32_t ex = warp_incl_scan(cnt, lane) - cnt;
-            for (uint32_t c2 = 0; c2 < cnt; ++c2) W.tmp[ex + c2] = W.tmp2[c2 * 32 + lane];
-            n_fin = __reduce_add_sync(FULL, cnt);
-            m.F += (int32_t)__reduce_add_sync(FULL, (uint32_t)fr);
-            m.S -= __reduce_add_sync(FULL, sfin_l);
-            m.B -= n_fin;
-            m.next_fin = __reduce_min_sync(FULL, mn);
-            m.maxO = __reduce_max_sync(FULL, mx);
-            __syncwarp();
-            event = true;
           }
-          if (event || m.t >= stop_t) break;
+          const uint32_t ex = warp_incl_scan(cnt, lane) - cnt;
+          for (uint32_t c2 = 0; c2 < cnt; ++c2) W.tmp[ex + c2] = W.tmp2[c2 * 32 + lane];
+          n_fin = __reduce_add_sync(FULL, cnt);
+          m.F += (int32_t)__reduce_add_sync(FULL, (uint32_t)fr);
+          m.S -= __reduce_add_sync(FULL, sfin_l);
+          m.B -= n_fin;
+          m.next_fin = __reduce_min_sync(FULL, mn);
+          m.maxO = __reduce_max_sync(FULL, mx);
+          __syncwarp();
         }
-        if (m.err) break;
       }
       // ---- finish records + chain successor release (c19), for this iteration's finishers ----
       if (n_fin) {
@@ -600,15 +675,23 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
     const bool done = !m.err && m.B == 0 && m.stack_cnt == 0 && m.q_head == m.q_tail && m.pend_ptr == m.n_pend;
     if (m.err && lane == 0) set_error(P.error, m.err, m.site);
     if (commit && !m.err) {
-      for (int s = lane; s < SLOTS; s += 32) {
-        const uint32_t rq = W.s_req[s];
-        if (rq != SAMU_EMPTY) {
-          const uint32_t me = W.s_meta[s];
+      // running ranks renumbered 0..B-1 in admission order
+      for (int s = lane; s < SLOTS; s += 32) W.tmp[s] = 0xFFFFFFFFu;
+      __syncwarp();
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+        if ((occ >> jj) & 1u) W.tmp[lane + 32 * jj] = W.s_meta[lane + 32 * jj];
+      __syncwarp();
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        if ((occ >> jj) & 1u) {
+          const int s = lane + 32 * jj;
+          const uint32_t rq = W.s_req[s];
+          const uint32_t me = W.tmp[s];
           uint32_t rank = 0;
-          for (int s2 = 0; s2 < SLOTS; ++s2)
-            if (W.s_req[s2] != SAMU_EMPTY && W.s_meta[s2] < me) ++rank;
+          for (int s2 = 0; s2 < SLOTS; ++s2) rank += W.tmp[s2] < me ? 1u : 0u;
           st[rq] = (SAMU_ST_RUNNING << 28) | rank;
-          gst[rq] = (uint16_t)((uint32_t)(W.s_o[s] + (int32_t)m.d) - (uint32_t)li[rq]);
+          gst[rq] = (uint16_t)((uint32_t)(W.s_fo[s].y + (int32_t)m.d) - (uint32_t)li[rq]);
         }
       }
       for (uint32_t i = lane; i < m.stack_cnt; i += 32) {
