@@ -61,15 +61,16 @@ __device__ __forceinline__ double kdouble(uint64_t k) {
   return __longlong_as_double((long long)b);
 }
 
-// block-size arithmetic with a power-of-two fast path (bs = 16 by default, reading c5)
+// block-size arithmetic; the kernel is instantiated for power-of-two block sizes (bs = 16 by
+// default, reading c5) and for the general case
+template <bool POW2>
 struct Bs {
   uint32_t v, mask, shift;
-  bool pow2;
-  __device__ __forceinline__ uint32_t mod(uint32_t x) const { return pow2 ? (x & mask) : x % v; }
-  __device__ __forceinline__ uint32_t div(uint32_t x) const { return pow2 ? (x >> shift) : x / v; }
+  __device__ __forceinline__ uint32_t mod(uint32_t x) const { return POW2 ? (x & mask) : x % v; }
+  __device__ __forceinline__ uint32_t div(uint32_t x) const { return POW2 ? (x >> shift) : x / v; }
   __device__ __forceinline__ uint32_t cdiv(uint32_t x) const { return div(x + v - 1); }
   __device__ __forceinline__ uint32_t posmod(int32_t a) const {
-    if (pow2) return (uint32_t)a & mask;
+    if (POW2) return (uint32_t)a & mask;
     const int32_t r = a % (int32_t)v;
     return (uint32_t)(r < 0 ? r + (int32_t)v : r);
   }
@@ -103,22 +104,6 @@ __device__ __forceinline__ void add_flops(Sim& m, uint64_t f) {
   const uint64_t lo = m.fl_lo + f;
   m.fl_hi += (lo < m.fl_lo) ? 1ull : 0ull;
   m.fl_lo = lo;
-}
-
-// rescan the running set: next finish index and max(l - d)
-__device__ __forceinline__ void rescan(const WarpSm& W, Sim& m, int lane, uint32_t occ) {
-  uint32_t mn = FULL;
-  int32_t mx = INT_MIN;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    if ((occ >> j) & 1u) {
-      const int2 fo = W.s_fo[lane + 32 * j];
-      mn = min(mn, (uint32_t)fo.x);
-      mx = max(mx, fo.y);
-    }
-  }
-  m.next_fin = __reduce_min_sync(FULL, mn);
-  m.maxO = __reduce_max_sync(FULL, mx);
 }
 
 // Stable LSD radix sort of n (key, idx) pairs by the 64-bit key (8 passes of 8 bits, passes where
@@ -170,6 +155,7 @@ __device__ const uint64_t* warp_radix_sort(uint64_t* ka, uint32_t* ia, uint64_t*
 }  // namespace
 
 // ---------------------------------------------------------------------------------------------
+template <bool POW2>
 __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunch P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -201,9 +187,8 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
     double* over = P.over ? P.over + ((size_t)k * A.n_nodes + C.node) * 16 : nullptr;
     const uint32_t r0 = C.rep_off[j], r1 = C.rep_off[j + 1];
     const uint32_t ms = C.max_seqs;
-    Bs bs;
+    Bs<POW2> bs;
     bs.v = C.bs;
-    bs.pow2 = (C.bs & (C.bs - 1)) == 0;
     bs.mask = C.bs - 1;
     bs.shift = __ffs(C.bs) - 1;
     const bool commit = C.commit && st;
@@ -336,7 +321,6 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
       }
     }
     __syncwarp();
-    if (m.B) rescan(W, m, lane, occ);
 
     // ---- pending cross-node arrivals in (ready, index) order: stable LSD radix sort ----
     const uint64_t* pk = pkey;
@@ -349,7 +333,23 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
     m.next_ready = m.n_pend ? kdouble(pk[0]) : CUDART_INF;
     const uint64_t K1 = 2ull * C.L * C.h_tp;
     const uint64_t LC = (uint64_t)C.L * C.c;
+    const bool need_rel = fio || fto || commit || C.has_succ;
     bool cut = false;
+    // per-lane summaries of this lane's slots: min finish index, max (l - d)
+    uint32_t lminf = FULL;
+    int32_t lmaxo = INT_MIN;
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj)
+      if ((occ >> jj) & 1u) {
+        const int2 fo = W.s_fo[lane + 32 * jj];
+        lminf = min(lminf, (uint32_t)fo.x);
+        lmaxo = max(lmaxo, fo.y);
+      }
+    m.next_fin = __reduce_min_sync(FULL, lminf);
+    m.maxO = __reduce_max_sync(FULL, lmaxo);
+    // window: register cache of the first wn (<= 32) entries of W (lane i = position i):
+    // request, prompt tokens p = l_in + g, tokens still to generate incl. the prefill's (L - g)
+    uint32_t w_r = 0, w_p = 0, w_rem = 0, wn = 0;
 
     // ---- main loop (c25) ----
     while (!m.err) {
@@ -365,37 +365,41 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
         m.pend_ptr += cnt;
         m.next_ready = m.pend_ptr < m.n_pend ? kdouble(pk[m.pend_ptr]) : CUDART_INF;
       }
-      const bool wnon = m.stack_cnt > 0 || m.q_head < m.q_tail;
-      if (m.B == 0 && !wnon) {
+      const uint32_t wlen = m.stack_cnt + (m.q_tail - m.q_head);
+      if (m.B == 0 && wlen == 0) {
         if (m.pend_ptr < m.n_pend && m.next_ready != CUDART_INF) { m.t = m.next_ready; continue; }
         break;
       }
-      // does the head of W fit? (slots, token budget, blocks)
-      bool fits = false;
-      if (wnon && m.B < ms) {
-        uint32_t hr, hg;
-        if (m.stack_cnt) { hr = W.stk_req[m.stack_cnt - 1]; hg = W.stk_g[m.stack_cnt - 1]; }
-        else { hr = q[m.q_head]; hg = m.q_head < m.n_front ? (uint32_t)gst[hr] : 0u; }
-        const uint32_t p = (uint32_t)li[hr] + hg;
-        fits = p <= C.budget && (int32_t)bs.cdiv(p) <= m.F;
+      // refill the window so it holds min(32, |W|) entries
+      {
+        const uint32_t want = min(32u, wlen);
+        if (wn < want) {
+          if ((uint32_t)lane >= wn && (uint32_t)lane < want) {
+            uint32_t r, g;
+            if ((uint32_t)lane < m.stack_cnt) { r = W.stk_req[m.stack_cnt - 1 - lane]; g = W.stk_g[m.stack_cnt - 1 - lane]; }
+            else {
+              const uint32_t qp = m.q_head + lane - m.stack_cnt;
+              r = q[qp];
+              g = qp < m.n_front ? (uint32_t)gst[r] : 0u;   // recompute front keeps its tokens
+            }
+            w_r = r;
+            w_p = (uint32_t)li[r] + g;
+            w_rem = max((uint32_t)lo[r], 1u) - g;
+          }
+          wn = want;
+        }
       }
+      // does the head of W fit? (slots, token budget, blocks)
+      const uint32_t hp = __shfl_sync(FULL, w_p, 0);
+      const bool fits = wlen > 0 && m.B < ms && hp <= C.budget && (int32_t)bs.cdiv(hp) <= m.F;
       uint32_t n_fin = 0;
       if (fits) {
         // ================= prefill iteration (c8): admit a strict FCFS prefix of W =========
-        uint32_t k_adm = 0, tok = 0, smaxp = 0, S_add = 0, n_stay = 0, mn_new = FULL;
-        int32_t blk = 0, freed = 0, mx_new = INT_MIN;
+        uint32_t k_adm = 0, tok = 0, smaxp = 0, S_add = 0, n_stay = 0;
+        int32_t blk = 0, freed = 0;
         for (;;) {
-          const uint32_t avail = m.stack_cnt + (m.q_tail - m.q_head);
-          if (avail == 0) break;
-          const bool valid = (uint32_t)lane < avail;
-          uint32_t r = 0, g = 0;
-          if ((uint32_t)lane < m.stack_cnt) { r = W.stk_req[m.stack_cnt - 1 - lane]; g = W.stk_g[m.stack_cnt - 1 - lane]; }
-          else if (valid) {
-            const uint32_t qp = m.q_head + lane - m.stack_cnt;
-            r = q[qp];
-            if (qp < m.n_front) g = gst[r];   // recompute front keeps its generated tokens
-          }
-          const uint32_t p = valid ? (uint32_t)li[r] + g : 0u;
+          const bool valid = (uint32_t)lane < wn;
+          const uint32_t p = valid ? w_p : 0u;
           const uint32_t nb = valid ? bs.cdiv(p) : 0u;
           const uint32_t sp = warp_incl_scan(p, lane), sb = warp_incl_scan(nb, lane);
           const bool ok = valid && (m.B + k_adm + lane + 1 <= ms) && (tok + sp <= C.budget) &&
@@ -404,48 +408,73 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
           const uint32_t mm = (bal == FULL) ? 32u : (uint32_t)(__ffs(~bal) - 1);
           if (mm == 0) break;
           const bool adm = (uint32_t)lane < mm;
-          const uint32_t Lr = adm ? max((uint32_t)lo[r], 1u) : 0u;
-          const bool finish_now = adm && g + 1 >= Lr;
+          const bool finish_now = adm && w_rem <= 1u;
           const bool stay = adm && !finish_now;
           const uint32_t bst = __ballot_sync(FULL, stay);
           const uint32_t bfn = __ballot_sync(FULL, finish_now);
-          int32_t fin_i = 0, o = 0;
-          if (stay) {
-            const uint32_t a = __popc(bst & lanemask_lt());
-            o = (int32_t)(p + 1) - (int32_t)m.d;
-            fin_i = (int32_t)(m.d + (Lr - (g + 1)));
-            const uint32_t ph = bs.posmod((int32_t)p - (int32_t)m.d);
-            W.adm_req[a] = r;
-            W.adm_fo[a] = make_int2(fin_i, o);
-            W.adm_meta[a] = ((m.next_rank + k_adm + lane) << 5) | ph;
-            atomicAdd(&W.hist[ph], 1u);
-          }
-          if (finish_now) W.tmp[n_fin + __popc(bfn & lanemask_lt())] = r;
-          n_fin += __popc(bfn);
           const uint32_t ns = __popc(bst);
-          if (bfn) freed += (int32_t)__reduce_add_sync(FULL, finish_now ? nb : 0u);
-          if (bst) {
-            S_add += __reduce_add_sync(FULL, stay ? p + 1 : 0u);
-            mn_new = min(mn_new, __reduce_min_sync(FULL, stay ? (uint32_t)fin_i : FULL));
-            mx_new = max(mx_new, __reduce_max_sync(FULL, stay ? o : INT_MIN));
+          int32_t s_fin = 0, s_o = 0;
+          uint32_t s_meta = 0;
+          if (stay) {
+            s_o = (int32_t)(p + 1) - (int32_t)m.d;
+            s_fin = (int32_t)(m.d + w_rem - 1);
+            s_meta = ((m.next_rank + k_adm + lane) << 5) | bs.posmod((int32_t)p - (int32_t)m.d);
+            atomicAdd(&W.hist[s_meta & 31u], 1u);
           }
+          if (finish_now && need_rel) W.tmp[n_fin + __popc(bfn & lanemask_lt())] = w_r;
+          n_fin += __popc(bfn);
+          if (bfn) freed += (int32_t)__reduce_add_sync(FULL, finish_now ? nb : 0u);
+          if (bst) S_add += __reduce_add_sync(FULL, stay ? p + 1 : 0u);
           smaxp = max(smaxp, __reduce_max_sync(FULL, adm ? p : 0u));
-          __syncwarp();
-          // insert the stays into free slots: lane L fills admitted ordinals [ex, ex + nfree)
+          // insert the stays into free slots: the a-th lane with a free slot takes the a-th stay
           if (ns) {
-            uint32_t fm = ~occ & 0xFFu;
-            const uint32_t nf = __popc(fm);
-            const uint32_t ex = warp_incl_scan(nf, lane) - nf;
-            uint32_t a = ex;
-            while (fm && a < ns) {
-              const int jj = __ffs(fm) - 1;
-              fm &= fm - 1;
-              const int s = lane + 32 * jj;
-              W.s_req[s] = W.adm_req[a];
-              W.s_fo[s] = W.adm_fo[a];
-              W.s_meta[s] = W.adm_meta[a];
-              occ |= 1u << jj;
-              ++a;
+            const bool has_free = occ != 0xFFu;
+            const uint32_t fl = __ballot_sync(FULL, has_free);
+            if ((uint32_t)__popc(fl) >= ns) {
+              // a-th stay lane -> a-th lane with a free slot, through a lane table in smem
+              if (stay) W.adm_meta[__popc(bst & lanemask_lt())] = (uint32_t)lane;
+              __syncwarp();
+              const uint32_t a = __popc(fl & lanemask_lt());
+              const bool take = has_free && a < ns;
+              const uint32_t src = take ? W.adm_meta[a] : 0u;
+              const uint32_t r_v = __shfl_sync(FULL, w_r, src);
+              const int32_t f_v = __shfl_sync(FULL, s_fin, src);
+              const int32_t o_v = __shfl_sync(FULL, s_o, src);
+              const uint32_t m_v = __shfl_sync(FULL, s_meta, src);
+              if (take) {
+                const int jb = __ffs(~occ & 0xFFu) - 1;
+                const int s = lane + 32 * jb;
+                W.s_req[s] = r_v;
+                W.s_fo[s] = make_int2(f_v, o_v);
+                W.s_meta[s] = m_v;
+                occ |= 1u << jb;
+                lminf = min(lminf, (uint32_t)f_v);
+                lmaxo = max(lmaxo, o_v);
+              }
+            } else {
+              if (stay) {
+                const uint32_t a = __popc(bst & lanemask_lt());
+                W.adm_req[a] = w_r;
+                W.adm_fo[a] = make_int2(s_fin, s_o);
+                W.adm_meta[a] = s_meta;
+              }
+              __syncwarp();
+              uint32_t fm = ~occ & 0xFFu;
+              const uint32_t nf = __popc(fm);
+              uint32_t a = warp_incl_scan(nf, lane) - nf;
+              while (fm && a < ns) {
+                const int jb = __ffs(fm) - 1;
+                fm &= fm - 1;
+                const int s = lane + 32 * jb;
+                const int2 fo = W.adm_fo[a];
+                W.s_req[s] = W.adm_req[a];
+                W.s_fo[s] = fo;
+                W.s_meta[s] = W.adm_meta[a];
+                occ |= 1u << jb;
+                lminf = min(lminf, (uint32_t)fo.x);
+                lmaxo = max(lmaxo, fo.y);
+                ++a;
+              }
             }
             __syncwarp();
           }
@@ -456,6 +485,28 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
           const uint32_t take = min(mm, m.stack_cnt);
           m.stack_cnt -= take;
           m.q_head += mm - take;
+          // shift the window by mm and refill it
+          w_r = __shfl_down_sync(FULL, w_r, mm == 32 ? 0 : mm);
+          w_p = __shfl_down_sync(FULL, w_p, mm == 32 ? 0 : mm);
+          w_rem = __shfl_down_sync(FULL, w_rem, mm == 32 ? 0 : mm);
+          wn -= mm;
+          const uint32_t wl2 = m.stack_cnt + (m.q_tail - m.q_head);
+          const uint32_t want = min(32u, wl2);
+          if (wn < want) {
+            if ((uint32_t)lane >= wn && (uint32_t)lane < want) {
+              uint32_t r, g;
+              if ((uint32_t)lane < m.stack_cnt) { r = W.stk_req[m.stack_cnt - 1 - lane]; g = W.stk_g[m.stack_cnt - 1 - lane]; }
+              else {
+                const uint32_t qp = m.q_head + lane - m.stack_cnt;
+                r = q[qp];
+                g = qp < m.n_front ? (uint32_t)gst[r] : 0u;
+              }
+              w_r = r;
+              w_p = (uint32_t)li[r] + g;
+              w_rem = max((uint32_t)lo[r], 1u) - g;
+            }
+            wn = want;
+          }
           if (mm < 32) break;
         }
         m.F -= blk;
@@ -471,8 +522,10 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
         m.B += n_stay;
         m.S += S_add;
         m.next_rank += k_adm;
-        m.next_fin = min(m.next_fin, mn_new);
-        m.maxO = max(m.maxO, mx_new);
+        if (n_stay) {
+          m.next_fin = __reduce_min_sync(FULL, lminf);
+          m.maxO = __reduce_max_sync(FULL, lmaxo);
+        }
       } else {
         if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; m.site = 9; break; }
         // ================= decode run (c9): uniform iterations until an event ===============
@@ -537,13 +590,17 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
           const uint64_t mm = done_it;
           // sum_j (K0 + K1 (S + B j)) = mm K0 + K1 (mm S + B mm (mm - 1) / 2)
           const uint64_t inner = mm * (uint64_t)m.S + (uint64_t)B * (mm * (mm - 1) / 2);
-          uint64_t lo64 = mm * K0, hi64 = __umul64hi(mm, K0);
-          const uint64_t plo = K1 * inner, phi = __umul64hi(K1, inner);
-          lo64 += plo;
-          hi64 += phi + (lo64 < plo ? 1ull : 0ull);
-          const uint64_t nlo = m.fl_lo + lo64;
-          m.fl_hi += hi64 + (nlo < lo64 ? 1ull : 0ull);
-          m.fl_lo = nlo;
+          if (f_last < (1ull << 53) && mm < 2048ull) {
+            add_flops(m, mm * K0 + K1 * inner);   // < 2^11 * 2^53: exact in u64
+          } else {
+            uint64_t lo64 = mm * K0, hi64 = __umul64hi(mm, K0);
+            const uint64_t plo = K1 * inner, phi = __umul64hi(K1, inner);
+            lo64 += plo;
+            hi64 += phi + (lo64 < plo ? 1ull : 0ull);
+            const uint64_t nlo = m.fl_lo + lo64;
+            m.fl_hi += hi64 + (nlo < lo64 ? 1ull : 0ull);
+            m.fl_lo = nlo;
+          }
           m.reqit += (uint64_t)B * mm;
           m.iter += done_it;
           const uint32_t rr = bs.mod(done_it);
@@ -572,6 +629,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
             const int32_t vo = W.s_fo[vs].y;
             const uint32_t vph = vmeta & 31u;
             const uint32_t l = (uint32_t)(vo + (int32_t)m.d);
+            const uint32_t vg = l - (uint32_t)li[vr];
             m.F += (int32_t)bs.cdiv(l - 1);
             if (vph == m.needidx) --need;
             __syncwarp();
@@ -579,16 +637,35 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
               occ &= ~(1u << (vs >> 5));
               W.hist[vph] -= 1;
               W.stk_req[m.stack_cnt] = vr;
-              W.stk_g[m.stack_cnt] = l - (uint32_t)li[vr];
+              W.stk_g[m.stack_cnt] = vg;
+              lminf = FULL;
+              lmaxo = INT_MIN;
+#pragma unroll
+              for (int jj = 0; jj < 8; ++jj)
+                if ((occ >> jj) & 1u) {
+                  const int2 fo = W.s_fo[lane + 32 * jj];
+                  lminf = min(lminf, (uint32_t)fo.x);
+                  lmaxo = max(lmaxo, fo.y);
+                }
             }
             __syncwarp();
+            // the victim is the new front of W: shift the window up by one
+            {
+              const uint32_t Lv = max((uint32_t)lo[vr], 1u);
+              const uint32_t pr = __shfl_up_sync(FULL, w_r, 1), pp = __shfl_up_sync(FULL, w_p, 1),
+                             pm = __shfl_up_sync(FULL, w_rem, 1);
+              if (lane == 0) { w_r = vr; w_p = l; w_rem = Lv - vg; }
+              else { w_r = pr; w_p = pp; w_rem = pm; }
+              wn = min(wn + 1, 32u);
+            }
             m.stack_cnt += 1;
             m.B -= 1;
             m.S -= l;
             if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; m.site = 10; break; }
           }
           if (m.err) break;
-          rescan(W, m, lane, occ);
+          m.next_fin = __reduce_min_sync(FULL, lminf);
+          m.maxO = __reduce_max_sync(FULL, lmaxo);
           // the preempting decode iteration itself
           const uint32_t B2 = m.B;
           const uint32_t smax = (uint32_t)((int32_t)m.d + m.maxO);
@@ -604,41 +681,89 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
           m.needidx = m.needidx == 0 ? bs.v - 1 : m.needidx - 1;
         }
         if (m.d == m.next_fin) {
-          // retire the finishers: slot scan over this lane's occupied slots + REDUX reductions
-          uint32_t mn = FULL, cnt = 0, sfin_l = 0;
-          int32_t mx = INT_MIN, fr = 0;
+          // ---- retire the finishers (ballot / REDUX) ----
+          const uint32_t inv = __ballot_sync(FULL, lminf == m.d);
+          const uint32_t ninv = __popc(inv);
+          uint32_t cnt_l = 0, sfin_l = 0;
+          int32_t fr_l = 0;
+          if (ninv <= 4) {
+            // transposed scan: 8-lane group g reads the 8 slots of the g-th involved lane
+            const int g = lane >> 3, jj = lane & 7;
+            if ((inv >> lane) & 1u) W.adm_req[__popc(inv & lanemask_lt())] = (uint32_t)lane;
+            __syncwarp();
+            const uint32_t Lg = (uint32_t)g < ninv ? W.adm_req[g] : 0u;
+            const uint32_t occ_g = __shfl_sync(FULL, occ, Lg);
+            const bool has = (uint32_t)g < ninv && ((occ_g >> jj) & 1u);
+            const int s = (int)Lg + 32 * jj;
+            const int2 fo = has ? W.s_fo[s] : make_int2(0, 0);
+            const bool fin = has && (uint32_t)fo.x == m.d;
+            if (fin) {
+              const uint32_t l_now = (uint32_t)(fo.y + (int32_t)m.d);
+              fr_l = (int32_t)bs.cdiv(l_now - 1);
+              sfin_l = l_now;
+              cnt_l = 1;
+              atomicSub(&W.hist[W.s_meta[s] & 31u], 1u);
+            }
+            const uint32_t fb = __ballot_sync(FULL, fin);
+            if (need_rel && fin) W.tmp[__popc(fb & lanemask_lt())] = W.s_req[s];
+            uint32_t mn = (has && !fin) ? (uint32_t)fo.x : FULL;
+            int32_t mx = (has && !fin) ? fo.y : INT_MIN;
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj) {
-            if ((occ >> jj) & 1u) {
-              const int s = lane + 32 * jj;
-              const int2 fo = W.s_fo[s];
-              if ((uint32_t)fo.x == m.d) {
-                const uint32_t l_now = (uint32_t)(fo.y + (int32_t)m.d);
-                fr += (int32_t)bs.cdiv(l_now - 1);
-                sfin_l += l_now;
-                atomicSub(&W.hist[W.s_meta[s] & 31u], 1u);
-                occ &= ~(1u << jj);
-                W.tmp2[cnt * 32 + lane] = W.s_req[s];   // staged per lane (<= 8 each)
-                ++cnt;
-              } else {
-                mn = min(mn, (uint32_t)fo.x);
-                mx = max(mx, fo.y);
+            for (int o = 1; o < 8; o <<= 1) {
+              mn = min(mn, __shfl_xor_sync(FULL, mn, o));
+              mx = max(mx, __shfl_xor_sync(FULL, mx, o));
+            }
+            // each involved lane takes its group's result
+            const bool me = (inv >> lane) & 1u;
+            const uint32_t gl = 8u * __popc(inv & lanemask_lt());
+            const uint32_t mn_g = __shfl_sync(FULL, mn, me ? gl : 0u);
+            const int32_t mx_g = __shfl_sync(FULL, mx, me ? gl : 0u);
+            if (me) {
+              lminf = mn_g;
+              lmaxo = mx_g;
+              occ &= ~((fb >> gl) & 0xFFu);
+            }
+          } else {
+            uint32_t mn = FULL, cnt = 0;
+            int32_t mx = INT_MIN;
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+              if ((occ >> jj) & 1u) {
+                const int s = lane + 32 * jj;
+                const int2 fo = W.s_fo[s];
+                if ((uint32_t)fo.x == m.d) {
+                  const uint32_t l_now = (uint32_t)(fo.y + (int32_t)m.d);
+                  fr_l += (int32_t)bs.cdiv(l_now - 1);
+                  sfin_l += l_now;
+                  atomicSub(&W.hist[W.s_meta[s] & 31u], 1u);
+                  occ &= ~(1u << jj);
+                  W.tmp2[cnt * 32 + lane] = W.s_req[s];   // staged per lane (<= 8 each)
+                  ++cnt;
+                } else {
+                  mn = min(mn, (uint32_t)fo.x);
+                  mx = max(mx, fo.y);
+                }
               }
             }
+            cnt_l = cnt;
+            lminf = mn;
+            lmaxo = mx;
+            if (need_rel) {
+              const uint32_t ex = warp_incl_scan(cnt, lane) - cnt;
+              for (uint32_t c2 = 0; c2 < cnt; ++c2) W.tmp[ex + c2] = W.tmp2[c2 * 32 + lane];
+            }
           }
-          const uint32_t ex = warp_incl_scan(cnt, lane) - cnt;
-          for (uint32_t c2 = 0; c2 < cnt; ++c2) W.tmp[ex + c2] = W.tmp2[c2 * 32 + lane];
-          n_fin = __reduce_add_sync(FULL, cnt);
-          m.F += (int32_t)__reduce_add_sync(FULL, (uint32_t)fr);
+          n_fin = __reduce_add_sync(FULL, cnt_l);
+          m.F += (int32_t)__reduce_add_sync(FULL, (uint32_t)fr_l);
           m.S -= __reduce_add_sync(FULL, sfin_l);
           m.B -= n_fin;
-          m.next_fin = __reduce_min_sync(FULL, mn);
-          m.maxO = __reduce_max_sync(FULL, mx);
+          m.next_fin = __reduce_min_sync(FULL, lminf);
+          m.maxO = __reduce_max_sync(FULL, lmaxo);
           __syncwarp();
         }
       }
       // ---- finish records + chain successor release (c19), for this iteration's finishers ----
-      if (n_fin) {
+      if (n_fin && need_rel) {
         const uint32_t itx = m.iter - 1;
         uint32_t nrel = 0;
         for (uint32_t base = 0; base < n_fin; base += 32) {
@@ -650,7 +775,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
             if (fio) fio[r] = itx;
             if (fto) fto[r] = m.t;
             if (commit) { st[r] = SAMU_ST_DONE << 28; ft[r] = m.t; }
-            sr = __ldg(A.succ + r);
+            if (C.has_succ) sr = __ldg(A.succ + r);
           }
           const uint32_t br = __ballot_sync(FULL, sr >= 0);
           if (sr >= 0) W.tmp2[nrel + __popc(br & lanemask_lt())] = (uint32_t)sr;
@@ -726,12 +851,20 @@ int32_t simulate_smem_bytes() { return (int32_t)(sizeof(WarpSm) * SAMU_WARPS_PER
 
 cudaError_t simulate_prepare(int* blocks_per_sm) {
   const int smem = simulate_smem_bytes();
-  cudaError_t e = cudaFuncSetAttribute(k_simulate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = cudaFuncSetAttribute(k_simulate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_simulate, 32 * SAMU_WARPS_PER_BLOCK, smem);
+  e = cudaFuncSetAttribute(k_simulate<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  int a = 0, b = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_simulate<true>, 32 * SAMU_WARPS_PER_BLOCK, smem);
+  if (e != cudaSuccess) return e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_simulate<false>, 32 * SAMU_WARPS_PER_BLOCK, smem);
+  *blocks_per_sm = a < b ? a : b;
+  return e;
 }
 
-cudaError_t launch_simulate(const SimLaunch& L, int32_t n_blocks, cudaStream_t s) {
-  k_simulate<<<n_blocks, 32 * SAMU_WARPS_PER_BLOCK, simulate_smem_bytes(), s>>>(L);
+cudaError_t launch_simulate(const SimLaunch& L, int32_t n_blocks, bool pow2_block, cudaStream_t s) {
+  if (pow2_block) k_simulate<true><<<n_blocks, 32 * SAMU_WARPS_PER_BLOCK, simulate_smem_bytes(), s>>>(L);
+  else k_simulate<false><<<n_blocks, 32 * SAMU_WARPS_PER_BLOCK, simulate_smem_bytes(), s>>>(L);
   return cudaGetLastError();
 }

@@ -72,7 +72,7 @@ struct samu_ctx {
   bool app_loaded = false;
   samu_engine_cfg eng{};
   int n_nodes = 0, n_req = 0;
-  std::vector<int32_t> node_model, node_begin, node_end, node_input;
+  std::vector<int32_t> node_model, node_begin, node_end, node_input, node_has_succ;
   std::vector<samu_request> req;
   std::vector<int32_t> succ;
   std::vector<uint8_t> cross;
@@ -330,6 +330,7 @@ extern "C" samu_status samu_app_load(samu_ctx* c, const samu_engine_cfg* engine,
   }
   for (int v = 0; v < n_nodes; ++v)
     if (has_same[v] && has_cross[v]) FAIL(c, SAMU_E_INVALID, "app_load: node mixes chain and cross-node predecessors");
+  c->node_has_succ = has_same;
   // sampling waves: chains rooted at pred < 0 first, then cross-node requests by node depth
   std::vector<int> depth(n_nodes, 0);
   for (int v = 0; v < n_nodes; ++v) if (c->node_input[v] >= 0) depth[v] = depth[c->node_input[v]] + 1;
@@ -512,7 +513,8 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
       const int64_t blocks = plan_blocks(c, model, cd.dp, cd.tp);
       if (blocks < 0) FAIL(c, SAMU_E_INVALID, "simulate: invalid plan for the node's model");
       DevCand& D = dc[x];
-      D.node = node; D.dp = cd.dp; D.tp = cd.tp; D.resume = cd.resume ? 1 : 0; D.commit = cd.commit ? 1 : 0; D.src = -1;
+      D.node = node; D.dp = cd.dp; D.tp = cd.tp; D.resume = cd.resume ? 1 : 0; D.commit = cd.commit ? 1 : 0;
+      D.has_succ = c->node_has_succ[node];
       D.max_seqs = c->eng.max_num_seqs;
       D.bs = c->eng.block_size;
       D.budget = std::max(M.spec.l_max, c->eng.min_batched_tokens);
@@ -579,7 +581,7 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
     L.max_q = (int32_t)max_q;
     L.max_p = (int32_t)max_p;
     L.error = c->d_error.as<int32_t>();
-    CK(c, launch_simulate(L, n_blocks, s));
+    CK(c, launch_simulate(L, n_blocks, (c->eng.block_size & (c->eng.block_size - 1)) == 0, s));
     // combine replicas into the per-(candidate, trial) records
     CK(c, launch_combine(L.rep_rec, L.cands, (int32_t)idx.size(), T, S.over, c->n_nodes, s));
     c->launches += 2;

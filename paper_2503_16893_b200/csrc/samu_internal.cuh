@@ -33,7 +33,7 @@ struct DevEcdf {
 
 // One candidate (node, plan) as the simulation kernel sees it.
 struct DevCand {
-  int32_t node, dp, tp, resume, commit, src;
+  int32_t node, dp, tp, resume, commit, has_succ;
   uint32_t max_seqs, bs, budget;
   int32_t blocks;              // KV blocks per replica (c5)
   uint32_t L, h_tp;            // layers, h / tp
@@ -78,7 +78,7 @@ cudaError_t launch_sample(const DevApp& app, const DevEcdf& e, const int32_t* se
                           uint16_t* l_in, cudaStream_t s);
 cudaError_t launch_dense_coeff(const uint32_t* bucket_B, int32_t nb, const double* coeff_slot,
                                uint32_t max_seqs, double* out, cudaStream_t s);
-cudaError_t launch_simulate(const SimLaunch& L, int32_t n_blocks, cudaStream_t s);
+cudaError_t launch_simulate(const SimLaunch& L, int32_t n_blocks, bool pow2_block, cudaStream_t s);
 cudaError_t simulate_prepare(int* blocks_per_sm);
 int32_t simulate_smem_bytes();
 cudaError_t launch_combine(const samu_trial_rec* rep_rec, const DevCand* cands, int32_t n_cands, int32_t n_trials,
