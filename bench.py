@@ -28,12 +28,13 @@ sys.path.insert(0, ROOT)
 import samu_workloads as W  # noqa: E402
 
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
-# K2 compute roofline: every simulated iteration evaluates the contract's
-# latency model, 6 fp64 ops (3 FMA + 2 ADD + the clock ADD) issued by one warp = 192 fp64
-# lane-ops; B200 has 64 fp64 lanes per SM per clock (37 TFLOP/s nominal FP64) -> 3 SM-clocks
-# per simulated iteration.
+# K2 roofline: the method's arithmetic per simulated iteration is the per-iteration
+# latency model of the contract (c24): 3 fused multiply-adds + 2 adds + the clock add = 9 fp64
+# flops.  Peak: 148 SMs x 64 fp64 FMA lanes x 2 flops x clock (37.2 TFLOP/s at 1965 MHz, the
+# nominal B200 FP64 rate).  Design-independent: a kernel that spends its time elsewhere (event
+# control, redundant lanes) shows a low fraction.
+FP64_FLOPS_PER_ITER = 9
 FP64_LANES_PER_SM = 64
-FP64_LANE_OPS_PER_ITER = 6 * 32
 N_SM = 148
 
 
@@ -281,9 +282,9 @@ def main():
         pk = peaks()
         clock = clk.summary()
         sm_hz = (clock.get("sm_max_mhz") or pk.get("sm_max_mhz") or 1965.0) * 1e6
-        peak_iters = N_SM * FP64_LANES_PER_SM * sm_hz / FP64_LANE_OPS_PER_ITER
+        peak = N_SM * FP64_LANES_PER_SM * 2 * sm_hz
         iters_per_launch = iters / world          # per rank launch (strong scaling: each rank its share)
-        achieved = iters_per_launch / (k2_ms / 1e3)
+        achieved = FP64_FLOPS_PER_ITER * iters_per_launch / (k2_ms / 1e3)
         value = nc * T / (ms / 1e3)
         line = {
             "metric": "simulated candidate-trials/s", "value": value, "unit": "candidate-trials/s",
@@ -294,11 +295,12 @@ def main():
                        "parallelism": f"trials sharded dp{world}",
                        "l2": f"inputs larger than L2: lengths {2 * 2 * T * w.n_req / 1e6:.0f} MB re-sampled every step"},
             "req_iters_per_s": reqit / (ms / 1e3), "sim_iters_per_s": iters / (ms / 1e3),
-            "roofline": {"bound": "alu", "kernel": "k_simulate", "achieved": achieved, "peak": peak_iters,
-                         "unit": "simulated iterations/s", "frac": achieved / peak_iters,
+            "roofline": {"bound": "alu", "kernel": "k_simulate", "achieved": achieved / 1e12, "peak": peak / 1e12,
+                         "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": ncu_traffic(w.name),
-                         "peak_source": "fp64 pipe: 148 SM x 64 lanes x clock / (6 fp64 ops x 32 lanes per iteration)",
-                         "k2_ms_per_launch": k2_ms},
+                         "peak_source": "fp64: 148 SM x 64 FMA lanes x 2 x sm clock (derived, DESIGN.md section 6)",
+                         "work_per_unit": "9 fp64 flops per simulated iteration (latency model, reading c24)",
+                         "sim_iters_per_launch": iters_per_launch, "k2_ms_per_launch": k2_ms},
             "e2e": {"value": nc * T / e2e_s, "unit": "candidate-trials/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches), "clocks": clock,

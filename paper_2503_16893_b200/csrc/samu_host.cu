@@ -657,7 +657,7 @@ extern "C" samu_status samu_simulate_batch(samu_ctx* c, const samu_candidate* ca
                                            double* out_fin_t) {
   GUARD(c);
   if (!c->app_loaded) FAIL(c, SAMU_E_INVALID, "simulate_batch: no app loaded");
-  if (n_cands < 0 || (n_cands && !cands) || n_trials < 0 || (n_trials && (!l_out || !l_in_eff)) || !out_recs)
+  if (n_cands < 0 || (n_cands && !cands) || n_trials < 0 || (n_trials && n_cands && (!l_out || !l_in_eff || !out_recs)))
     FAIL(c, SAMU_E_INVALID, "simulate_batch: bad arguments");
   if (n_trials >= (1 << 27)) FAIL(c, SAMU_E_INVALID, "simulate_batch: too many trials");
   const bool has_state = st != nullptr;

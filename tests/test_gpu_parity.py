@@ -256,3 +256,73 @@ def test_greedy_plan_bit_exact(name, kw, T):
         assert sg["T_E"] == so["T_E"]
     assert pg["total"] == po["total"]
     assert pg["n_cand_evals"] == po["n_cand_evals"]
+
+
+# ------------------------------------------------------------------------------------------
+# full size, bench launch configuration: sampled (candidate, trial) pairs vs the oracle
+# ------------------------------------------------------------------------------------------
+def test_full_size_c5_bench_config_sampled_parity():
+    w = W.make_workload("c5")                      # 50,000 requests, 1024 trials, 12 nodes
+    S = gpu(w)
+    ready = [v for v in range(w.n_nodes) if not np.any((w.pred[w.node == v] >= 0) &
+                                                      (w.node[np.maximum(w.pred[w.node == v], 0)] != v))]
+    cands = [(v, dp, tp) for v in ready for (dp, tp) in S.samu_enumerate_plans(v)]
+    glo, gli = S.samu_sample_lengths(SEED, 0, w.n_trials)
+    g = recs(S.samu_simulate_batch(cands, glo, gli))          # [165, 1024]
+    P = O.Problem(w)
+    rng = np.random.default_rng(2503)
+    picks = [(cands.index(c), int(k)) for c, k in
+             [(cands[0], 0), (cands[-1], 1023)] + [(cands[int(i)], int(k)) for i, k in
+                                                   zip(rng.integers(0, len(cands), 10), rng.integers(0, 1024, 10))]]
+    # the longest replica-sims: the chain summariser with dp = 1
+    summ = [i for i, c in enumerate(cands) if c[0] == 10 and c[1] == 1]
+    picks += [(summ[0], 777)]
+    for ci, k in picks:
+        lo, li = P.sample(SEED, k, 1)
+        node, dp, tp = cands[ci]
+        o = P.simulate(node, dp, tp, lo, li)[0]
+        assert_rec_equal(g[ci][k:k + 1], o, f"cand {cands[ci]} trial {k}")
+
+
+# ------------------------------------------------------------------------------------------
+# edge cases
+# ------------------------------------------------------------------------------------------
+def test_edge_empty_batches_and_empty_node():
+    w = F.multi([dict(l_in=[5, 6, 7], l_out=[3, 1, 2]), dict(l_in=[], l_out=[])], eng=F.engine(n_gpus=8))
+    S = gpu(w)
+    glo, gli = S.samu_sample_lengths(SEED, 0, 2)
+    out = S.samu_simulate_batch([], glo, gli)
+    assert out["recs"].numel() == 0
+    g = recs(S.samu_simulate_batch([(1, 1, 1), (1, 8, 1)], glo, gli))
+    assert np.all(g["t_end"] == 0.0) and np.all(g["flags"] == 1)      # a node with no work is done (c28)
+    import torch
+    z = torch.empty((0, w.n_req), dtype=torch.int16, device="cuda")
+    assert recs(S.samu_simulate_batch([(0, 1, 1)], z, z))["t_end"].size == 0
+
+
+def test_edge_more_replicas_than_requests_and_lin_equals_lmax():
+    # dp = 8 over 5 requests leaves empty replicas (clock = load time); l_in = l_max gives l_out = 0,
+    # which still runs one prefill (reading c3)
+    load = F.zero_load()
+    load[:, :] = 2.5
+    w = F.tiny([64, 10, 64, 3, 60], [5, 4, 9, 1, 2], sp=F.spec(l_max=64), eng=F.engine(n_gpus=8), load=load)
+    g = _sim_parity(w, [(0, 8, 1), (0, 5, 1), (0, 1, 1)], 1)
+    assert np.all(g["t_end"] >= 2.5)
+
+
+def test_edge_max_num_seqs_one_and_256():
+    for ms in (1, 256):
+        w = F.tiny(np.full(300, 9), np.arange(300) % 7 + 1, eng=F.engine(max_num_seqs=ms, min_batched_tokens=3000))
+        _sim_parity(w, [(0, 1, 1)], 1)
+
+
+def test_greedy_plan_bit_exact_mixed_c5_shape():
+    # all three applications at once: ensembling + routing + chain summary (fused summariser +
+    # evaluator co-scheduling), 12 nodes
+    w = W.make_workload("c5", n_prompts=40, n_docs=30, n_trials=2)
+    po = O.Problem(w).plan_greedy(SEED, 2)
+    pg = gpu(w).samu_plan_greedy(SEED, 2)
+    assert [s["entries"] for s in pg["stages"]] == [s["entries"] for s in po["stages"]]
+    for sg, so in zip(pg["stages"], po["stages"]):
+        assert sg["fstar"] == so["fstar"] and sg["mean_tE"] == so["mean_tE"] and sg["T_E"] == so["T_E"]
+    assert pg["total"] == po["total"] and pg["n_cand_evals"] == po["n_cand_evals"]
