@@ -83,13 +83,11 @@ struct samu_ctx {
   std::map<std::pair<int, int>, DevBuf> coef;                      // (model, tp slot) -> dense table
   std::map<std::pair<int, int>, std::pair<DevBuf, DevBuf>> rep;    // (node, dp) -> (off, req)
   std::map<std::pair<int, int>, std::vector<uint32_t>> rep_off_host;
-  std::map<std::pair<int, int>, std::pair<DevBuf, DevBuf>> heads;  // (node, dp) -> chain heads CSR
 
   // launch scratch
   DevBuf d_cands, d_items, d_counter, d_rep_rec, d_scratch_q, d_scratch_key, d_scratch_idx, d_error;
-  DevBuf d_sum, d_gather_send, d_gather_recv, d_lane_mem, d_tail_off;
-  int sim_blocks_per_sm = 0, lane_blocks_per_sm = 0;
-  int k2_mode = 0;   // 0 auto (lane kernel for fresh-state batches), 1 force warp kernel
+  DevBuf d_sum, d_gather_send, d_gather_recv;
+  int sim_blocks_per_sm = 0;
 
   // stats
   int64_t n_sims = 0;
@@ -393,11 +391,6 @@ extern "C" samu_status samu_app_load(samu_ctx* c, const samu_engine_cfg* engine,
   }
   c->rep.clear();
   c->rep_off_host.clear();
-  c->heads.clear();
-  {
-    const char* m = getenv("SAMU_K2");
-    c->k2_mode = (m && std::string(m) == "warp") ? 1 : 0;
-  }
   c->app_loaded = true;
   return SAMU_OK;
 }
@@ -441,28 +434,6 @@ static samu_status replicas(samu_ctx* c, int node, int dp, const uint32_t** off,
     CK(c, upload(pr.second, l, c->stream));
     c->rep_off_host[key] = o;
     it = c->rep.find(key);
-  }
-  *off = it->second.first.as<uint32_t>();
-  *lst = it->second.second.as<uint32_t>();
-  return SAMU_OK;
-}
-
-static samu_status replica_heads(samu_ctx* c, int node, int dp, const uint32_t** off, const uint32_t** lst) {
-  auto key = std::make_pair(node, dp);
-  auto it = c->heads.find(key);
-  if (it == c->heads.end()) {
-    std::vector<std::vector<uint32_t>> L(dp);
-    for (int r = c->node_begin[node]; r < c->node_end[node]; ++r) {
-      if (c->req[r].pred >= 0) continue;
-      const int kk = c->req[r].chain >= 0 ? c->req[r].chain : r - c->node_begin[node];
-      L[kk % dp].push_back((uint32_t)r);
-    }
-    std::vector<uint32_t> o(dp + 1, 0), l;
-    for (int j = 0; j < dp; ++j) { o[j + 1] = o[j] + (uint32_t)L[j].size(); l.insert(l.end(), L[j].begin(), L[j].end()); }
-    auto& pr = c->heads[key];
-    CK(c, upload(pr.first, o, c->stream));
-    CK(c, upload(pr.second, l, c->stream));
-    it = c->heads.find(key);
   }
   *off = it->second.first.as<uint32_t>();
   *lst = it->second.second.as<uint32_t>();
@@ -555,7 +526,6 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
       D.load_s = M.load[(size_t)slot * SAMU_MAX_DP + (cd.dp - 1)];
       D.coef = c->coef.at({model, slot}).as<double>();
       RET(replicas(c, node, cd.dp, &D.rep_off, &D.rep_req));
-      RET(replica_heads(c, node, cd.dp, &D.head_off, &D.head_req));
       D.src_fin = J.src_fin;
       D.tau = J.tau;
       D.tau_rec = J.tau_rec;
@@ -577,70 +547,20 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
     for (int x : order)
       for (int k = 0; k < T; ++k)
         for (int j = 0; j < dc[x].dp; ++j) items.push_back(make_uint2((uint32_t)x, ((uint32_t)k << 4) | (uint32_t)j));
-    // K2 variant: lane-per-simulation for fresh-state batches without cross-node arrivals,
-    // warp-per-simulation otherwise (carried state import/export, evaluator arrivals)
-    bool lane_ok = c->k2_mode == 0 && !S.st;
-    for (size_t x = 0; x < idx.size() && lane_ok; ++x)
-      if (c->node_input[dc[x].node] >= 0 || dc[x].commit) lane_ok = false;
     SimLaunch L;
     L.app = dev_app(c);
-    L.cands = nullptr;
     L.n_cands = (int32_t)idx.size();
     L.n_trials = T;
     L.n_items = (int32_t)items.size();
-    L.next_item = c->d_counter.as<uint32_t>();
     L.l_out = l_out;
     L.l_in = l_in;
     L.st = S.st;
     L.g = S.g;
     L.fin_t = S.fin_t;
     L.over = S.over;
-    L.rep_rec = c->d_rep_rec.as<samu_trial_rec>();
     L.error = c->d_error.as<int32_t>();
-    L.tail_off = nullptr;
     const bool pow2 = (c->eng.block_size & (c->eng.block_size - 1)) == 0;
-    if (lane_ok) {
-      if (!c->lane_blocks_per_sm) {
-        int b = 0;
-        CK(c, lane_prepare(&b));
-        if (b < 1) FAIL(c, SAMU_E_CUDA, "simulate: lane kernel does not fit on an SM");
-        c->lane_blocks_per_sm = b;
-      }
-      // per-item tail regions for chain successors
-      std::vector<uint64_t> toff(items.size() + 1, 0);
-      for (size_t x = 0; x < items.size(); ++x) {
-        const DevCand& D = dc[items[x].x];
-        uint64_t sz = 0;
-        if (D.has_succ) {
-          const std::vector<uint32_t>& ho = c->rep_off_host.at({D.node, D.dp});
-          const uint32_t jj = items[x].y & 15u;
-          sz = ho[jj + 1] - ho[jj];
-        }
-        toff[x + 1] = toff[x] + sz;
-      }
-      CK(c, upload(c->d_tail_off, toff, s));
-      CK(c, c->d_scratch_q.ensure(sizeof(uint32_t) * std::max<uint64_t>(toff.back(), 1)));
-      const int64_t lanes_needed = (int64_t)items.size();
-      int n_blocks = (int)std::min<int64_t>((int64_t)c->n_sm * c->lane_blocks_per_sm, (lanes_needed + 127) / 128);
-      n_blocks = std::max(n_blocks, 1);
-      CK(c, c->d_lane_mem.ensure(lane_mem_bytes() * (size_t)n_blocks * 128));
-      CK(c, upload(c->d_cands, dc, s));
-      CK(c, upload(c->d_items, items, s));
-      CK(c, c->d_counter.ensure(sizeof(uint32_t)));
-      CK(c, cudaMemsetAsync(c->d_counter.p, 0, sizeof(uint32_t), s));
-      CK(c, c->d_rep_rec.ensure(sizeof(samu_trial_rec) * 16 * idx.size() * T));
-      L.cands = c->d_cands.as<DevCand>();
-      L.items = c->d_items.as<uint2>();
-      L.next_item = c->d_counter.as<uint32_t>();
-      L.rep_rec = c->d_rep_rec.as<samu_trial_rec>();
-      L.scratch_q = c->d_scratch_q.as<uint32_t>();
-      L.scratch_key = nullptr;
-      L.scratch_idx = nullptr;
-      L.max_q = 0;
-      L.max_p = 0;
-      L.tail_off = c->d_tail_off.as<uint64_t>();
-      CK(c, launch_simulate_lane(L, c->d_lane_mem.p, n_blocks, pow2, s));
-    } else {
+    {
       const int bpsm = c->sim_blocks_per_sm;
       const int64_t warps_needed = (int64_t)items.size();
       int n_blocks = (int)std::min<int64_t>((int64_t)c->n_sm * bpsm, (warps_needed + SAMU_WARPS_PER_BLOCK - 1) / SAMU_WARPS_PER_BLOCK);

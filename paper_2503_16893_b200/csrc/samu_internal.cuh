@@ -42,8 +42,7 @@ struct DevCand {
   const double* coef;          // dense [3 phases][2 (a,b)][max_seqs]
   const uint32_t* rep_off;     // [dp + 1]
   const uint32_t* rep_req;     // requests of the node grouped by replica, index order
-  const uint32_t* head_off;    // [dp + 1] chain heads (pred < 0) per replica, index order
-  const uint32_t* head_req;
+
   const double* src_fin;       // [T][n] finish times of the dependency source, or null
   const double* tau;           // [T] time limits or null
   const samu_trial_rec* tau_rec;  // [T] take tau_k = tau_rec[k].t_end (f* of a stage), or null
@@ -72,7 +71,6 @@ struct SimLaunch {
   uint32_t* scratch_idx;       // [n_warps][4][max_p]
   int32_t max_q, max_p;
   int32_t* error;              // first error code (0 = ok), error site
-  const uint64_t* tail_off;    // K2L: per-item offset into scratch_q of its tail region
 };
 
 // launchers (return cudaError_t of the launch)
@@ -83,9 +81,7 @@ cudaError_t launch_dense_coeff(const uint32_t* bucket_B, int32_t nb, const doubl
                                uint32_t max_seqs, double* out, cudaStream_t s);
 cudaError_t launch_simulate(const SimLaunch& L, int32_t n_blocks, bool pow2_block, cudaStream_t s);
 cudaError_t simulate_prepare(int* blocks_per_sm);
-size_t lane_mem_bytes();
-cudaError_t lane_prepare(int* blocks_per_sm);
-cudaError_t launch_simulate_lane(const SimLaunch& L, void* mem, int32_t n_blocks, bool pow2_block, cudaStream_t s);
+
 int32_t simulate_smem_bytes();
 cudaError_t launch_combine(const samu_trial_rec* rep_rec, const DevCand* cands, int32_t n_cands, int32_t n_trials,
                            double* over, int32_t n_nodes, cudaStream_t s);
