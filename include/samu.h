@@ -140,6 +140,16 @@ typedef struct samu_plan {
 samu_status samu_ctx_create(samu_ctx** out, int32_t cuda_device, void* cuda_stream, int32_t rank,
                             int32_t world, const uint8_t* nccl_unique_id);
 void samu_ctx_destroy(samu_ctx* ctx);
+
+/* In-process rank group: `world` contexts created with samu_ctx_create_local in one process
+ * (one thread per rank, any devices incl. the same one) run the multi-rank trial sharding with
+ * device-to-device copies instead of NCCL (used to test the sharded path on one GPU).  The group
+ * must outlive its contexts. */
+typedef struct samu_local_group samu_local_group;
+samu_status samu_local_group_create(samu_local_group** out, int32_t world);
+void samu_local_group_destroy(samu_local_group* group);
+samu_status samu_ctx_create_local(samu_ctx** out, int32_t cuda_device, void* cuda_stream, int32_t rank,
+                                  samu_local_group* group);
 const char* samu_last_error(const samu_ctx* ctx);
 /* Number of CUDA kernels this context has launched so far (instrumentation). */
 uint64_t samu_launch_count(const samu_ctx* ctx);

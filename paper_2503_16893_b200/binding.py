@@ -65,7 +65,8 @@ REC_DTYPE = np.dtype([("t_end", "<f8"), ("flops_lo", "<u8"), ("flops_hi", "<u8")
                       ("iters", "<u4"), ("flags", "<u4")])
 assert REC_DTYPE.itemsize == C.sizeof(samu_trial_rec) == 40
 
-EXPORTED = ["samu_ctx_create", "samu_ctx_destroy", "samu_last_error", "samu_launch_count", "samu_nccl_unique_id",
+EXPORTED = ["samu_ctx_create", "samu_ctx_destroy", "samu_local_group_create", "samu_local_group_destroy",
+            "samu_ctx_create_local", "samu_last_error", "samu_launch_count", "samu_nccl_unique_id",
             "samu_model_register",
             "samu_ecdf_load", "samu_app_load", "samu_enumerate_plans", "samu_sample_lengths", "samu_simulate_batch",
             "samu_plan_greedy", "samu_plan_free"]
@@ -82,6 +83,10 @@ def lib():
         L = C.CDLL(LIB_PATH)
         P = C.c_void_p
         L.samu_ctx_create.argtypes = [C.POINTER(P), C.c_int32, P, C.c_int32, C.c_int32, P]
+        L.samu_local_group_create.argtypes = [C.POINTER(P), C.c_int32]
+        L.samu_local_group_destroy.argtypes = [P]
+        L.samu_local_group_destroy.restype = None
+        L.samu_ctx_create_local.argtypes = [C.POINTER(P), C.c_int32, P, C.c_int32, P]
         L.samu_ctx_destroy.argtypes = [P]
         L.samu_ctx_destroy.restype = None
         L.samu_last_error.argtypes = [P]
@@ -125,11 +130,27 @@ def samu_nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+class LocalGroup:
+    """In-process rank group (samu_local_group): one Samu context per thread and rank."""
+
+    def __init__(self, world: int):
+        h = C.c_void_p()
+        rc = lib().samu_local_group_create(C.byref(h), world)
+        if rc:
+            raise SamuError(rc, "samu_local_group_create failed")
+        self.h, self.world = h, world
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.samu_local_group_destroy(self.h)
+            self.h = None
+
+
 class Samu:
     """One libsamu context (one per process / GPU).  Device buffers are torch CUDA tensors."""
 
     def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
-                 stream=None):
+                 stream=None, local_group: Optional[LocalGroup] = None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("libsamu needs a CUDA device (no CPU fallback)")
@@ -137,9 +158,14 @@ class Samu:
         self.device = torch.device("cuda", device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         h = C.c_void_p()
-        idbuf = None if nccl_id is None else (C.c_uint8 * 128).from_buffer_copy(nccl_id)
-        rc = lib().samu_ctx_create(C.byref(h), device, C.c_void_p(self.stream.cuda_stream), rank, world,
-                                   None if idbuf is None else C.cast(idbuf, C.c_void_p))
+        if local_group is not None:
+            world = local_group.world
+            rc = lib().samu_ctx_create_local(C.byref(h), device, C.c_void_p(self.stream.cuda_stream), rank,
+                                             local_group.h)
+        else:
+            idbuf = None if nccl_id is None else (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+            rc = lib().samu_ctx_create(C.byref(h), device, C.c_void_p(self.stream.cuda_stream), rank, world,
+                                       None if idbuf is None else C.cast(idbuf, C.c_void_p))
         if rc:
             raise SamuError(rc, "samu_ctx_create failed")
         self.h = h

@@ -4,6 +4,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -57,12 +59,39 @@ int log2_exact(uint32_t x) {
 
 }  // namespace
 
+// In-process rank group: W contexts in one process (threads), typically on one GPU, exchange
+// device buffers through a host barrier.  Same collective semantics as the NCCL path.
+struct samu_local_group {
+  int world = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int count = 0;
+  uint64_t gen = 0;
+  std::vector<const void*> ptrs;
+  // all ranks publish a pointer, wait until everyone has, then read the others'
+  void exchange(int rank, const void* p) {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t my = gen;
+    ptrs[rank] = p;
+    if (++count == world) { count = 0; ++gen; cv.notify_all(); }
+    else cv.wait(lk, [&] { return gen != my; });
+  }
+  void barrier(int rank) {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t my = gen;
+    (void)rank;
+    if (++count == world) { count = 0; ++gen; cv.notify_all(); }
+    else cv.wait(lk, [&] { return gen != my; });
+  }
+};
+
 struct samu_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
+  samu_local_group* group = nullptr;   // in-process ranks instead of NCCL
   std::string err;
   bool poisoned = false;
   int n_sm = 148;
@@ -133,6 +162,41 @@ struct samu_ctx {
     samu_status r_ = (x);      \
     if (r_ != SAMU_OK) return r_; \
   } while (0)
+
+// ---- collectives over the context's ranks (NCCL, or the in-process group) ----
+static samu_status comm_allgather(samu_ctx* c, const void* send, void* recv, size_t bytes) {
+  cudaStream_t s = c->stream;
+  if (c->group) {
+    CK(c, cudaStreamSynchronize(s));
+    c->group->exchange(c->rank, send);
+    for (int w = 0; w < c->world; ++w)
+      CK(c, cudaMemcpyAsync((char*)recv + (size_t)w * bytes, c->group->ptrs[w], bytes, cudaMemcpyDeviceToDevice, s));
+    CK(c, cudaStreamSynchronize(s));
+    c->group->barrier(c->rank);   // nobody reuses its send buffer before every copy finished
+    return SAMU_OK;
+  }
+  CKN(c, ncclAllGather(send, recv, bytes, ncclUint8, c->comm, s));
+  return SAMU_OK;
+}
+
+// element-wise max (op = 0) or sum (op = 1) of n int32 over ranks, device buffers
+static samu_status comm_allreduce_i32(samu_ctx* c, const int32_t* send, int32_t* recv, int n, int op) {
+  cudaStream_t s = c->stream;
+  if (c->group) {
+    CK(c, cudaStreamSynchronize(s));
+    c->group->exchange(c->rank, send);
+    std::vector<int32_t> acc(n, 0), tmp(n);
+    for (int w = 0; w < c->world; ++w) {
+      CK(c, cudaMemcpy(tmp.data(), c->group->ptrs[w], sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < n; ++i) acc[i] = (w == 0) ? tmp[i] : (op == 0 ? std::max(acc[i], tmp[i]) : acc[i] + tmp[i]);
+    }
+    c->group->barrier(c->rank);
+    CK(c, cudaMemcpy(recv, acc.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+    return SAMU_OK;
+  }
+  CKN(c, ncclAllReduce(send, recv, n, ncclInt32, op == 0 ? ncclMax : ncclSum, c->comm, s));
+  return SAMU_OK;
+}
 
 static inline cudaError_t samu_count(samu_ctx* c, cudaError_t e) {
   c->launches += 1;
@@ -210,6 +274,28 @@ extern "C" samu_status samu_ctx_create(samu_ctx** out, int32_t cuda_device, void
     if (ncclCommInitRank(&c->comm, world, id, rank) != ncclSuccess) { delete c; return SAMU_E_NCCL; }
   }
   *out = c;
+  return SAMU_OK;
+}
+
+extern "C" samu_status samu_local_group_create(samu_local_group** out, int32_t world) {
+  if (!out || world < 1) return SAMU_E_INVALID;
+  samu_local_group* g = new samu_local_group();
+  g->world = world;
+  g->ptrs.assign(world, nullptr);
+  *out = g;
+  return SAMU_OK;
+}
+
+extern "C" void samu_local_group_destroy(samu_local_group* g) { delete g; }
+
+extern "C" samu_status samu_ctx_create_local(samu_ctx** out, int32_t cuda_device, void* cuda_stream, int32_t rank,
+                                             samu_local_group* group) {
+  if (!out || !group || rank < 0 || rank >= group->world) return SAMU_E_INVALID;
+  samu_status rc = samu_ctx_create(out, cuda_device, cuda_stream, 0, 1, nullptr);
+  if (rc != SAMU_OK) return rc;
+  (*out)->rank = rank;
+  (*out)->world = group->world;
+  (*out)->group = group;
   return SAMU_OK;
 }
 
@@ -633,9 +719,10 @@ static samu_status gather_records(samu_ctx* c, const samu_trial_rec* local, int 
   CK(c, c->d_gather_send.ensure(row * n));
   CK(c, c->d_gather_recv.ensure(row * n * c->world));
   CK(c, cudaMemsetAsync(c->d_gather_send.p, 0, row * n, s));
-  CK(c, cudaMemcpy2DAsync(c->d_gather_send.p, row, local, sizeof(samu_trial_rec) * cnt0, sizeof(samu_trial_rec) * cnt0, n,
-                          cudaMemcpyDeviceToDevice, s));
-  CKN(c, ncclAllGather(c->d_gather_send.p, c->d_gather_recv.p, row * n, ncclUint8, c->comm, s));
+  if (cnt0)
+    CK(c, cudaMemcpy2DAsync(c->d_gather_send.p, row, local, sizeof(samu_trial_rec) * cnt0, sizeof(samu_trial_rec) * cnt0,
+                            n, cudaMemcpyDeviceToDevice, s));
+  RET(comm_allgather(c, c->d_gather_send.p, c->d_gather_recv.p, row * n));
   for (int w = 0; w < c->world; ++w) {
     int bw, cw;
     trial_share(T, c->world, w, &bw, &cw);
@@ -718,7 +805,7 @@ extern "C" samu_status samu_simulate_batch(samu_ctx* c, const samu_candidate* ca
       DevBuf tmp;
       CK(c, tmp.ensure(sizeof(int32_t) * 2));
       CK(c, cudaMemcpyAsync(tmp.p, &Tl, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
-      CKN(c, ncclAllReduce(tmp.p, tmp.as<int32_t>() + 1, 1, ncclInt32, ncclSum, c->comm, c->stream));
+      RET(comm_allreduce_i32(c, tmp.as<int32_t>(), tmp.as<int32_t>() + 1, 1, 1));
       CK(c, cudaMemcpyAsync(&Tsum, tmp.as<int32_t>() + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
       CK(c, cudaStreamSynchronize(c->stream));
       int b, cnt;
@@ -1058,7 +1145,7 @@ struct Greedy {
     }
     if (c->world > 1) {
       CK(c, cudaMemcpyAsync(red, flag.data(), sizeof(int32_t) * c->n_nodes, cudaMemcpyHostToDevice, s));
-      CKN(c, ncclAllReduce(red, red + SAMU_MAX_NODES, c->n_nodes, ncclInt32, ncclMax, c->comm, s));
+      RET(comm_allreduce_i32(c, red, red + SAMU_MAX_NODES, c->n_nodes, 0));
       CK(c, cudaMemcpyAsync(flag.data(), red + SAMU_MAX_NODES, sizeof(int32_t) * c->n_nodes, cudaMemcpyDeviceToHost, s));
       CK(c, cudaStreamSynchronize(s));
     }

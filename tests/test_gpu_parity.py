@@ -326,3 +326,69 @@ def test_greedy_plan_bit_exact_mixed_c5_shape():
     for sg, so in zip(pg["stages"], po["stages"]):
         assert sg["fstar"] == so["fstar"] and sg["mean_tE"] == so["mean_tE"] and sg["T_E"] == so["T_E"]
     assert pg["total"] == po["total"] and pg["n_cand_evals"] == po["n_cand_evals"]
+
+
+# ------------------------------------------------------------------------------------------
+# multi-rank trial sharding on one GPU: in-process rank group (same collectives as NCCL)
+# ------------------------------------------------------------------------------------------
+def _run_ranks(world, fn):
+    import threading
+
+    import torch
+    from paper_2503_16893_b200 import LocalGroup, Samu
+    grp = LocalGroup(world)
+    outs, errs = [None] * world, []
+
+    def work(r):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                S = Samu(0, rank=r, local_group=grp, stream=st)
+                outs[r] = fn(S, r, st)
+                st.synchronize()
+                S.close()
+        except Exception as e:   # pragma: no cover - reported below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errs, errs
+    return outs
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_local_ranks_greedy_plan_identical(world):
+    w = W.make_workload("c2", n_prompts=120, n_trials=5)
+    ref = O.Problem(w).plan_greedy(SEED, 5)
+
+    def fn(S, r, st):
+        S.load_workload(w)
+        return S.samu_plan_greedy(SEED, 5)
+
+    for pg in _run_ranks(world, fn):
+        assert [s["entries"] for s in pg["stages"]] == [s["entries"] for s in ref["stages"]]
+        assert [s["mean_tE"] for s in pg["stages"]] == [s["mean_tE"] for s in ref["stages"]]
+        assert [s["T_E"] for s in pg["stages"]] == [s["T_E"] for s in ref["stages"]]
+        assert pg["total"] == ref["total"]
+
+
+def test_local_ranks_sharded_summary_identical():
+    w = W.make_workload("c3", n_prompts=600, n_trials=7)
+    cands = [(0, 1, 1), (1, 2, 2), (3, 4, 1)]
+    S1 = gpu(w)
+    lo, li = S1.samu_sample_lengths(SEED, 0, 7)
+    ref = S1.samu_simulate_batch(cands, lo, li, summary=True)["summary"]
+
+    def fn(S, r, st):
+        S.load_workload(w)
+        base, rem = divmod(7, 2)
+        cnt = base + (1 if r < rem else 0)
+        tb = r * base + min(r, rem)
+        l1, l2 = S.samu_sample_lengths(SEED, tb, cnt)
+        return S.samu_simulate_batch(cands, l1, l2, summary=True)["summary"]
+
+    for summ in _run_ranks(2, fn):
+        assert summ == ref
