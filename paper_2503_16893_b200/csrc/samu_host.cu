@@ -107,7 +107,8 @@ struct samu_ctx {
   std::vector<uint8_t> cross;
   std::vector<std::vector<int32_t>> waves;
   DevBuf d_l_in_base, d_cap, d_pred, d_node, d_succ, d_cross;
-  DevBuf d_ev, d_ec, d_eoff, d_mnode, d_lmax;
+  DevBuf d_tab, d_tab_off, d_nobs, d_mnode, d_lmax;
+  int32_t smem_tab_bytes = 0;
   std::vector<DevBuf> d_waves;
   std::map<std::pair<int, int>, DevBuf> coef;                      // (model, tp slot) -> dense table
   std::map<std::pair<int, int>, std::pair<DevBuf, DevBuf>> rep;    // (node, dp) -> (off, req)
@@ -440,23 +441,36 @@ extern "C" samu_status samu_app_load(samu_ctx* c, const samu_engine_cfg* engine,
   CK(c, upload(c->d_cross, c->cross, s));
   c->d_waves.clear();
   for (auto& w : c->waves) { c->d_waves.emplace_back(); CK(c, upload(c->d_waves.back(), w, s)); }
-  // eCDF tables (all registered models, packed)
-  std::vector<uint32_t> ev, ec, lmax(n_nodes);
-  std::vector<int32_t> eoff(SAMU_MAX_NODES + 1, 0);
-  for (int m = 0; m < SAMU_MAX_NODES; ++m) {
-    eoff[m] = (int32_t)ev.size();
-    if (c->models[m].ecdf_set) {
-      ev.insert(ev.end(), c->models[m].ev.begin(), c->models[m].ev.end());
-      ec.insert(ec.end(), c->models[m].ec.begin(), c->models[m].ec.end());
+  // eCDF tables: each registered model's sorted multiset expanded on the device (reading c2)
+  {
+    std::vector<int32_t> toff(SAMU_MAX_NODES + 1, 0);
+    std::vector<uint32_t> nobs(SAMU_MAX_NODES, 0), lmax(n_nodes);
+    for (int m = 0; m < SAMU_MAX_NODES; ++m) {
+      toff[m + 1] = toff[m];
+      if (c->models[m].ecdf_set) {
+        nobs[m] = c->models[m].ec.back();
+        toff[m + 1] += (int32_t)((nobs[m] + 7u) & ~7u);
+      }
     }
+    CK(c, c->d_tab.ensure(sizeof(uint16_t) * std::max(toff[SAMU_MAX_NODES], 8)));
+    int32_t max_bytes = 0;
+    for (int m = 0; m < SAMU_MAX_NODES; ++m) {
+      if (!c->models[m].ecdf_set) continue;
+      DevBuf v, cu;
+      CK(c, upload(v, c->models[m].ev, s));
+      CK(c, upload(cu, c->models[m].ec, s));
+      CK(c, samu_count(c, launch_ecdf_table(v.as<uint32_t>(), cu.as<uint32_t>(), (int32_t)c->models[m].ev.size(), nobs[m],
+                                            c->d_tab.as<uint16_t>() + toff[m], s)));
+      CK(c, cudaStreamSynchronize(s));
+      max_bytes = std::max(max_bytes, (toff[m + 1] - toff[m]) * 2);
+    }
+    c->smem_tab_bytes = std::min(max_bytes, 200 * 1024);
+    for (int v = 0; v < n_nodes; ++v) lmax[v] = c->models[node_model[v]].spec.l_max;
+    CK(c, upload(c->d_tab_off, toff, s));
+    CK(c, upload(c->d_nobs, nobs, s));
+    CK(c, upload(c->d_mnode, c->node_model, s));
+    CK(c, upload(c->d_lmax, lmax, s));
   }
-  eoff[SAMU_MAX_NODES] = (int32_t)ev.size();
-  for (int v = 0; v < n_nodes; ++v) lmax[v] = c->models[node_model[v]].spec.l_max;
-  CK(c, upload(c->d_ev, ev, s));
-  CK(c, upload(c->d_ec, ec, s));
-  CK(c, upload(c->d_eoff, eoff, s));
-  CK(c, upload(c->d_mnode, c->node_model, s));
-  CK(c, upload(c->d_lmax, lmax, s));
   // dense coefficient tables for every (model of a node, allowed tp) (reading c11)
   c->coef.clear();
   for (int v = 0; v < n_nodes; ++v) {
@@ -538,11 +552,12 @@ extern "C" samu_status samu_sample_lengths(samu_ctx* c, uint64_t seed, int32_t t
   if (n_trials > 65535) FAIL(c, SAMU_E_INVALID, "sample_lengths: at most 65535 trials per call");
   DevApp a = dev_app(c);
   DevEcdf e;
-  e.values = c->d_ev.as<uint32_t>();
-  e.cum = c->d_ec.as<uint32_t>();
-  e.off = c->d_eoff.as<int32_t>();
+  e.tab = c->d_tab.as<uint16_t>();
+  e.tab_off = c->d_tab_off.as<int32_t>();
+  e.n_obs = c->d_nobs.as<uint32_t>();
   e.model_of_node = c->d_mnode.as<int32_t>();
   e.l_max_of_node = c->d_lmax.as<uint32_t>();
+  e.smem_tab_bytes = c->smem_tab_bytes;
   for (size_t w = 0; w < c->waves.size(); ++w)
     CK(c, samu_count(c, launch_sample(a, e, c->d_waves[w].as<int32_t>(), (int32_t)c->waves[w].size(), seed, trial_begin, n_trials,
                         out_l_out, out_l_in_eff, c->stream)));

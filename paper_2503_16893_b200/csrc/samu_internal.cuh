@@ -22,13 +22,15 @@ struct DevApp {
   const uint8_t* cross;        // [n] 1 if pred is in another node
 };
 
-// eCDF tables for the sampler: per model offset into packed knot arrays
+// eCDF tables for the sampler: per model the sorted multiset of its n observed lengths as a u16
+// table (reading c2), packed, each model's table padded to 8 entries (16-byte TMA granularity)
 struct DevEcdf {
-  const uint32_t* values;      // packed knots, all models
-  const uint32_t* cum;
-  const int32_t* off;          // [n_models + 1]
+  const uint16_t* tab;         // packed tables
+  const int32_t* tab_off;      // [SAMU_MAX_NODES + 1] entry offsets
+  const uint32_t* n_obs;       // [SAMU_MAX_NODES] n = cum[K-1]
   const int32_t* model_of_node;  // [n_nodes]
   const uint32_t* l_max_of_node; // [n_nodes]
+  int32_t smem_tab_bytes;      // dynamic shared memory reserved for one staged table
 };
 
 // One candidate (node, plan) as the simulation kernel sees it.
@@ -77,6 +79,8 @@ struct SimLaunch {
 cudaError_t launch_sample(const DevApp& app, const DevEcdf& e, const int32_t* seq_head, int32_t n_seq,
                           uint64_t seed, int32_t trial_begin, int32_t n_trials, uint16_t* l_out,
                           uint16_t* l_in, cudaStream_t s);
+cudaError_t launch_ecdf_table(const uint32_t* values, const uint32_t* cum, int32_t K, uint32_t n, uint16_t* tab,
+                              cudaStream_t s);
 cudaError_t launch_dense_coeff(const uint32_t* bucket_B, int32_t nb, const double* coeff_slot,
                                uint32_t max_seqs, double* out, cudaStream_t s);
 cudaError_t launch_simulate(const SimLaunch& L, int32_t n_blocks, bool pow2_block, cudaStream_t s);
