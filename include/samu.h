@@ -217,6 +217,15 @@ samu_status samu_simulate_batch(samu_ctx* ctx, const samu_candidate* cands, int3
  * scores candidate stages on the device.  Every rank returns the identical plan.  *out is
  * library-allocated; free with samu_plan_free. */
 samu_status samu_plan_greedy(samu_ctx* ctx, uint64_t seed, int32_t n_trials, samu_plan** out);
+
+/* The paper's competitors on the same estimator, stage commit and trial sharding:
+ *   Max-heuristic: all GPUs to one model at a time (the lowest-id ready model) with the plan of
+ *     highest stage throughput; each stage runs its model to completion.
+ *   Min-heuristic: as many ready models as GPUs allow, GPUs split as evenly as possible, the
+ *     split / plan combination of highest stage throughput (<= 10^4 evaluated); stages end at the
+ *     first finish and every unfinished model is re-planned. */
+samu_status samu_plan_max_heuristic(samu_ctx* ctx, uint64_t seed, int32_t n_trials, samu_plan** out);
+samu_status samu_plan_min_heuristic(samu_ctx* ctx, uint64_t seed, int32_t n_trials, samu_plan** out);
 void samu_plan_free(samu_plan* plan);
 
 #ifdef __cplusplus

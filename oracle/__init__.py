@@ -108,6 +108,8 @@ def lib():
                                   C.c_int32, P, P, P]
         L.or_simulate_many.argtypes = [P, C.c_int32, P, C.c_int32, P, P, C.c_int32, P]
         L.or_plan_greedy.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(or_plan)]
+        L.or_plan_max_heuristic.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(or_plan)]
+        L.or_plan_min_heuristic.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(or_plan)]
         _lib = L
     return _lib
 
@@ -249,9 +251,11 @@ class Problem:
         _check(lib().or_simulate_many(self.h, len(cands), cs, T, _ptr(l_out), _ptr(l_in), n_threads, _ptr(rec)))
         return rec
 
-    def plan_greedy(self, seed, n_trials):
+    def plan_greedy(self, seed, n_trials, algo="greedy"):
         plan = or_plan()
-        _check(lib().or_plan_greedy(self.h, seed, n_trials, C.byref(plan)))
+        fn = {"greedy": lib().or_plan_greedy, "max": lib().or_plan_max_heuristic,
+              "min": lib().or_plan_min_heuristic}[algo]
+        _check(fn(self.h, seed, n_trials, C.byref(plan)))
         stages = []
         for i in range(plan.n_stages):
             s = plan.stages[i]

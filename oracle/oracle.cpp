@@ -770,8 +770,9 @@ struct Greedy {
     return s;
   }
 
-  int run(uint64_t seed, or_plan* out) {
-    const int N = (int)p->eng.n_gpus;
+  std::vector<std::vector<int>> plans_dp, plans_tp;
+
+  void init(uint64_t seed) {
     l_out.assign((size_t)T * n, 0);
     l_in.assign((size_t)T * n, 0);
     or_sample_lengths(p, seed, 0, T, l_out.data(), l_in.data());
@@ -779,13 +780,190 @@ struct Greedy {
     g.assign((size_t)T * n, 0);
     fin_t.assign((size_t)T * n, std::numeric_limits<double>::infinity());
     over.assign((size_t)T * nn * 16, 0.0);
-    std::memset(out, 0, sizeof(*out));
-    std::vector<std::vector<int>> plans_dp(nn), plans_tp(nn);
+    plans_dp.assign(nn, {});
+    plans_tp.assign(nn, {});
     for (size_t v = 0; v < nn; ++v) {
       int cnt = or_enumerate_plans(p, p->node_model[v], nullptr, nullptr, 0);
       plans_dp[v].resize(cnt); plans_tp[v].resize(cnt);
       or_enumerate_plans(p, p->node_model[v], plans_dp[v].data(), plans_tp[v].data(), cnt);
     }
+  }
+
+  // commit a chosen stage (Alg. 1 lines 24-25): f* to completion, the others cut at t_E^(k)
+  int commit(const std::vector<Entry>& Es, or_plan* out) {
+    Score sc = score(Es);
+    for (size_t i = 0; i < Es.size(); ++i) {   // topological order = ascending node id
+      const Entry& e = Es[i];
+      const double* sf = src_fin_of(e, Es);
+      std::vector<or_rec> rec(T);
+      or_cand c{e.node, e.dp, e.tp, resumes(e) ? 1 : 0};
+      int rc = or_simulate(p, &c, T, l_out.data(), l_in.data(), st.data(), g.data(), fin_t.data(), over.data(),
+                           (int)i == sc.fstar ? nullptr : sc.tE.data(), sf, 1, rec.data(), nullptr, nullptr);
+      if (rc) return rc;
+    }
+    for (int k = 0; k < T; ++k)   // carried finish times re-based to the next stage's clock
+      for (size_t r = 0; r < n; ++r)
+        if (st_status(st[k * n + r]) == OR_ST_DONE) fin_t[k * n + r] = fin_t[k * n + r] - sc.tE[k];
+    or_stage& S = out->stages[out->n_stages++];
+    S.n_entries = (int)Es.size();
+    for (size_t i = 0; i < Es.size(); ++i) { S.node[i] = Es[i].node; S.dp[i] = Es[i].dp; S.tp[i] = Es[i].tp; }
+    S.fstar = Es[sc.fstar].node;
+    S.mean_tE = sc.mean_tE;
+    S.T_E = sc.TE;
+    out->total += sc.mean_tE;
+    prev = Es;
+    return OR_OK;
+  }
+
+  // Algorithm 1 inner loop: the stage E* for the current workload
+  int choose_greedy(const std::vector<int>& unfinished, std::vector<Entry>& Es) {
+    const int N = (int)p->eng.n_gpus;
+    Score s_star{0.0, -1, std::vector<double>(T, 0.0), 0.0};
+    for (;;) {
+      // ready models: unfinished, and their input node finished or selected in E* (Alg.1 l.5)
+      std::vector<int> ready;
+      for (int v : unfinished) {
+        int u = p->node_input[v];
+        bool ok = (u < 0) || done_all(u);
+        for (const Entry& e : Es) if (e.node == u) ok = true;
+        if (ok) ready.push_back(v);
+      }
+      struct Cand { std::vector<Entry> E; Entry P; };
+      std::vector<Cand> cands;
+      const int g_star = gpus(Es);
+      for (int v : ready) {
+        for (size_t pi = 0; pi < plans_dp[v].size(); ++pi) {
+          Entry P{v, plans_dp[v][pi], plans_tp[v][pi]};
+          int prime = -1;
+          for (size_t i = 0; i < Es.size(); ++i) if (Es[i].node == v) prime = (int)i;
+          std::vector<Entry> E = Es;
+          if (prime >= 0) {
+            E[prime] = P;
+            int gE = gpus(E);
+            if (!(g_star < gE && gE <= N)) continue;   // Alg. 1 line 11
+          } else {
+            E.push_back(P);
+            if (gpus(E) > N) continue;                  // Alg. 1 line 14
+          }
+          std::sort(E.begin(), E.end(), [](const Entry& a, const Entry& b) { return a.node < b.node; });
+          cands.push_back({E, P});
+        }
+      }
+      if (cands.empty()) break;
+      double maxdT = -std::numeric_limits<double>::infinity();
+      int bi = -1;
+      double br = 0.0;
+      int bN = 0;
+      Score bs{};
+      for (size_t ci = 0; ci < cands.size(); ++ci) {
+        Score sc = score(cands[ci].E);
+        double dT = sc.TE - s_star.TE;
+        int dN = gpus(cands[ci].E) - g_star;
+        double ratio = dT / (double)dN;
+        maxdT = std::max(maxdT, dT);
+        bool better = false;
+        if (bi < 0) better = true;
+        else if (ratio > br) better = true;
+        else if (ratio == br) {
+          const Entry& a = cands[ci].P;
+          const Entry& b = cands[bi].P;
+          better = std::make_tuple(dN, a.node, a.tp, a.dp) < std::make_tuple(bN, b.node, b.tp, b.dp);
+        }
+        if (better) { bi = (int)ci; br = ratio; bN = dN; bs = sc; }
+      }
+      if (maxdT < 0.0) break;                           // Alg. 1 line 19
+      Es = cands[bi].E;
+      s_star = bs;
+    }
+    return OR_OK;
+  }
+
+  // Max-heuristic: all GPUs to one model at a time — the lowest-id ready
+  // model — with the plan of highest stage throughput (ties: enumeration order, i.e. fewer GPUs,
+  // then smaller tp); the stage runs that model to completion
+  int choose_max(const std::vector<int>& unfinished, std::vector<Entry>& Es) {
+    int v = -1;
+    for (int u : unfinished) {
+      int in = p->node_input[u];
+      if (in < 0 || done_all(in)) { v = u; break; }
+    }
+    if (v < 0) return OR_OK;
+    double bT = 0.0;
+    for (size_t pi = 0; pi < plans_dp[v].size(); ++pi) {
+      std::vector<Entry> E{{v, plans_dp[v][pi], plans_tp[v][pi]}};
+      Score sc = score(E);
+      if (Es.empty() || sc.TE > bT) { Es = E; bT = sc.TE; }
+    }
+    return OR_OK;
+  }
+
+  // Min-heuristic: as many ready models as GPUs allow (lowest node ids first; a
+  // model whose input is selected in the same stage counts as ready), GPUs split as evenly as
+  // possible (floor(N/k) each, N mod k of them one more); among those splits and the plans that
+  // use exactly the assigned GPUs, the combination of highest stage throughput (at most 10^4
+  // combinations in enumeration order; ties: first); if no combination exists, one model fewer
+  int choose_min(const std::vector<int>& unfinished, std::vector<Entry>& Es) {
+    const int N = (int)p->eng.n_gpus;
+    std::vector<int> sel;
+    for (int v : unfinished) {
+      if ((int)sel.size() >= N) break;
+      int in = p->node_input[v];
+      bool ok = in < 0 || done_all(in);
+      for (int x : sel) if (x == in) ok = true;
+      if (ok) sel.push_back(v);
+    }
+    for (int k = (int)sel.size(); k >= 1 && Es.empty(); --k) {
+      const int base = N / k, extra = N % k;
+      double bT = 0.0;
+      long count = 0;
+      std::vector<int> pick(extra);
+      for (int i = 0; i < extra; ++i) pick[i] = i;
+      bool more_subsets = true;
+      while (more_subsets && count < 10000) {
+        std::vector<int> gv(k, base);
+        for (int i : pick) gv[i] += 1;
+        // plans of exactly gv[i] GPUs per selected model
+        std::vector<std::vector<int>> opts(k);
+        bool feasible = true;
+        for (int i = 0; i < k; ++i) {
+          int v = sel[i];
+          for (size_t pi = 0; pi < plans_dp[v].size(); ++pi)
+            if (plans_dp[v][pi] * plans_tp[v][pi] == gv[i]) opts[i].push_back((int)pi);
+          if (opts[i].empty()) feasible = false;
+        }
+        if (feasible) {
+          std::vector<int> idx(k, 0);
+          for (;;) {
+            if (count >= 10000) break;
+            ++count;
+            std::vector<Entry> E;
+            for (int i = 0; i < k; ++i) {
+              int v = sel[i], pi = opts[i][idx[i]];
+              E.push_back({v, plans_dp[v][pi], plans_tp[v][pi]});
+            }
+            Score sc = score(E);
+            if (Es.empty() || sc.TE > bT) { Es = E; bT = sc.TE; }
+            int q = k - 1;   // odometer, last model fastest
+            while (q >= 0 && ++idx[q] == (int)opts[q].size()) { idx[q] = 0; --q; }
+            if (q < 0) break;
+          }
+        }
+        // next subset of `extra` positions in lexicographic order
+        int i = extra - 1;
+        while (i >= 0 && pick[i] == k - extra + i) --i;
+        if (i < 0) more_subsets = false;
+        else {
+          ++pick[i];
+          for (int j2 = i + 1; j2 < extra; ++j2) pick[j2] = pick[j2 - 1] + 1;
+        }
+      }
+    }
+    return OR_OK;
+  }
+
+  int run(uint64_t seed, int algo, or_plan* out) {
+    init(seed);
+    std::memset(out, 0, sizeof(*out));
     for (;;) {
       std::vector<int> unfinished;
       for (size_t v = 0; v < nn; ++v) if (!done_all((int)v)) unfinished.push_back((int)v);
@@ -794,102 +972,39 @@ struct Greedy {
       full_cache.clear();
       cut_cache.clear();
       std::vector<Entry> Es;
-      Score s_star{0.0, -1, std::vector<double>(T, 0.0), 0.0};
-      for (;;) {
-        // ready models: unfinished, and their input node finished or selected in E* (Alg.1 l.5)
-        std::vector<int> ready;
-        for (int v : unfinished) {
-          int u = p->node_input[v];
-          bool ok = (u < 0) || done_all(u);
-          for (const Entry& e : Es) if (e.node == u) ok = true;
-          if (ok) ready.push_back(v);
-        }
-        struct Cand { std::vector<Entry> E; Entry P; };
-        std::vector<Cand> cands;
-        const int g_star = gpus(Es);
-        for (int v : ready) {
-          for (size_t pi = 0; pi < plans_dp[v].size(); ++pi) {
-            Entry P{v, plans_dp[v][pi], plans_tp[v][pi]};
-            int prime = -1;
-            for (size_t i = 0; i < Es.size(); ++i) if (Es[i].node == v) prime = (int)i;
-            std::vector<Entry> E = Es;
-            if (prime >= 0) {
-              E[prime] = P;
-              int gE = gpus(E);
-              if (!(g_star < gE && gE <= N)) continue;   // Alg. 1 line 11
-            } else {
-              E.push_back(P);
-              if (gpus(E) > N) continue;                  // Alg. 1 line 14
-            }
-            std::sort(E.begin(), E.end(), [](const Entry& a, const Entry& b) { return a.node < b.node; });
-            cands.push_back({E, P});
-          }
-        }
-        if (cands.empty()) break;
-        double maxdT = -std::numeric_limits<double>::infinity();
-        int bi = -1;
-        double br = 0.0;
-        int bN = 0;
-        Score bs{};
-        for (size_t ci = 0; ci < cands.size(); ++ci) {
-          Score sc = score(cands[ci].E);
-          double dT = sc.TE - s_star.TE;
-          int dN = gpus(cands[ci].E) - g_star;
-          double ratio = dT / (double)dN;
-          maxdT = std::max(maxdT, dT);
-          bool better = false;
-          if (bi < 0) better = true;
-          else if (ratio > br) better = true;
-          else if (ratio == br) {
-            const Entry& a = cands[ci].P;
-            const Entry& b = cands[bi].P;
-            better = std::make_tuple(dN, a.node, a.tp, a.dp) < std::make_tuple(bN, b.node, b.tp, b.dp);
-          }
-          if (better) { bi = (int)ci; br = ratio; bN = dN; bs = sc; }
-        }
-        if (maxdT < 0.0) break;                           // Alg. 1 line 19
-        Es = cands[bi].E;
-        s_star = bs;
-      }
+      int rc = algo == 0 ? choose_greedy(unfinished, Es) : (algo == 1 ? choose_max(unfinished, Es) : choose_min(unfinished, Es));
+      if (rc) return rc;
       if (Es.empty()) { set_err("no ready model fits an empty stage"); return OR_E_INFEASIBLE; }
-      // commit the stage (Alg. 1 lines 24-25)
-      Score sc = score(Es);
-      for (size_t i = 0; i < Es.size(); ++i) {   // topological order = ascending node id
-        const Entry& e = Es[i];
-        const double* sf = src_fin_of(e, Es);
-        std::vector<or_rec> rec(T);
-        or_cand c{e.node, e.dp, e.tp, resumes(e) ? 1 : 0};
-        int rc = or_simulate(p, &c, T, l_out.data(), l_in.data(), st.data(), g.data(), fin_t.data(), over.data(),
-                             (int)i == sc.fstar ? nullptr : sc.tE.data(), sf, 1, rec.data(), nullptr, nullptr);
-        if (rc) return rc;
-      }
-      for (int k = 0; k < T; ++k)   // carried finish times re-based to the next stage's clock
-        for (size_t r = 0; r < n; ++r)
-          if (st_status(st[k * n + r]) == OR_ST_DONE) fin_t[k * n + r] = fin_t[k * n + r] - sc.tE[k];
-      or_stage& S = out->stages[out->n_stages++];
-      S.n_entries = (int)Es.size();
-      for (size_t i = 0; i < Es.size(); ++i) { S.node[i] = Es[i].node; S.dp[i] = Es[i].dp; S.tp[i] = Es[i].tp; }
-      S.fstar = Es[sc.fstar].node;
-      S.mean_tE = sc.mean_tE;
-      S.T_E = sc.TE;
-      out->total += sc.mean_tE;
-      prev = Es;
+      rc = commit(Es, out);
+      if (rc) return rc;
     }
     out->n_cand_evals = evals;
     return OR_OK;
   }
 };
 
-extern "C" int32_t or_plan_greedy(const or_problem* p, uint64_t seed, int32_t n_trials, or_plan* out) {
+static int32_t plan_with(const or_problem* p, uint64_t seed, int32_t n_trials, int algo, or_plan* out) {
   Greedy G;
   G.p = p;
   G.T = n_trials;
   G.n = p->req.size();
   G.nn = p->node_model.size();
   try {
-    return G.run(seed, out);
+    return G.run(seed, algo, out);
   } catch (int rc) {
-    set_err("simulation error in greedy");
+    set_err("simulation error in planner");
     return rc;
   }
+}
+
+extern "C" int32_t or_plan_max_heuristic(const or_problem* p, uint64_t seed, int32_t n_trials, or_plan* out) {
+  return plan_with(p, seed, n_trials, 1, out);
+}
+
+extern "C" int32_t or_plan_min_heuristic(const or_problem* p, uint64_t seed, int32_t n_trials, or_plan* out) {
+  return plan_with(p, seed, n_trials, 2, out);
+}
+
+extern "C" int32_t or_plan_greedy(const or_problem* p, uint64_t seed, int32_t n_trials, or_plan* out) {
+  return plan_with(p, seed, n_trials, 0, out);
 }

@@ -131,6 +131,10 @@ int32_t or_simulate_many(const or_problem* p, int32_t n_cands, const or_cand* ca
 /* Algorithm 1 greedy search with the estimator */
 int32_t or_plan_greedy(const or_problem* p, uint64_t seed, int32_t n_trials, or_plan* out);
 
+/* the paper's competitors on the same estimator */
+int32_t or_plan_max_heuristic(const or_problem* p, uint64_t seed, int32_t n_trials, or_plan* out);
+int32_t or_plan_min_heuristic(const or_problem* p, uint64_t seed, int32_t n_trials, or_plan* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -69,7 +69,7 @@ EXPORTED = ["samu_ctx_create", "samu_ctx_destroy", "samu_local_group_create", "s
             "samu_ctx_create_local", "samu_last_error", "samu_launch_count", "samu_nccl_unique_id",
             "samu_model_register",
             "samu_ecdf_load", "samu_app_load", "samu_enumerate_plans", "samu_sample_lengths", "samu_simulate_batch",
-            "samu_plan_greedy", "samu_plan_free"]
+            "samu_plan_greedy", "samu_plan_max_heuristic", "samu_plan_min_heuristic", "samu_plan_free"]
 
 _lib = None
 
@@ -102,6 +102,8 @@ def lib():
         L.samu_sample_lengths.argtypes = [P, C.c_uint64, C.c_int32, C.c_int32, P, P]
         L.samu_simulate_batch.argtypes = [P, P, C.c_int32, P, P, C.c_int32, P, P, P, P, P, P, P, P, P]
         L.samu_plan_greedy.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(C.POINTER(samu_plan))]
+        L.samu_plan_max_heuristic.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(C.POINTER(samu_plan))]
+        L.samu_plan_min_heuristic.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(C.POINTER(samu_plan))]
         L.samu_plan_free.argtypes = [C.POINTER(samu_plan)]
         L.samu_plan_free.restype = None
         _lib = L
@@ -281,9 +283,12 @@ class Samu:
                                    mean_flops=x.mean_flops, mean_req_iters=x.mean_req_iters) for x in summ[:nc]]
         return out
 
-    def samu_plan_greedy(self, seed: int, n_trials: int):
+    def samu_plan_greedy(self, seed: int, n_trials: int, algo: str = "greedy"):
+        """algo: "greedy" (Algorithm 1), "max" / "min" (the paper's Max- / Min-heuristic)."""
         p = C.POINTER(samu_plan)()
-        self._check(lib().samu_plan_greedy(self.h, seed, n_trials, C.byref(p)))
+        fn = {"greedy": lib().samu_plan_greedy, "max": lib().samu_plan_max_heuristic,
+              "min": lib().samu_plan_min_heuristic}[algo]
+        self._check(fn(self.h, seed, n_trials, C.byref(p)))
         try:
             P = p.contents
             stages = []

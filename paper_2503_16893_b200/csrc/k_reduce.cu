@@ -134,7 +134,7 @@ __global__ void k_fstar(const samu_trial_rec* __restrict__ cache, int32_t T, con
 // smaller dN, lower node id, smaller tp, smaller dp; also max dT (Alg. 1 line 19)
 __global__ void k_stage_score(const samu_trial_rec* __restrict__ cache, int32_t T, const StageCand* __restrict__ sc,
                               int32_t n, StageOut* __restrict__ out, double TE_star, int32_t gpus_star,
-                              int32_t* best, double* max_dT) {
+                              int32_t mode, int32_t* best, double* max_dT) {
   for (int32_t x = threadIdx.x; x < n; x += blockDim.x) {
     const StageCand& S = sc[x];
     const int32_t f = out[x].fstar;
@@ -164,6 +164,10 @@ __global__ void k_stage_score(const samu_trial_rec* __restrict__ cache, int32_t 
       const double ratio = __ddiv_rn(dT, (double)dN);
       mx = fmax(mx, dT);
       bool better = false;
+      if (mode == 1) {   // competitors: highest stage throughput, first candidate on ties
+        if (bi < 0 || out[x].TE > br) { bi = x; br = out[x].TE; }
+        continue;
+      }
       if (bi < 0 || ratio > br) better = true;
       else if (ratio == br) {
         const StageCand& B = sc[bi];
@@ -228,7 +232,8 @@ cudaError_t launch_fstar(const samu_trial_rec* cache, int32_t T, const StageCand
 }
 
 cudaError_t launch_stage_score(const samu_trial_rec* cache, int32_t T, const StageCand* sc, int32_t n, StageOut* out,
-                               double TE_star, int32_t gpus_star, int32_t* best, double* max_dT, cudaStream_t s) {
-  k_stage_score<<<1, 256, 0, s>>>(cache, T, sc, n, out, TE_star, gpus_star, best, max_dT);
+                               double TE_star, int32_t gpus_star, int32_t mode, int32_t* best, double* max_dT,
+                               cudaStream_t s) {
+  k_stage_score<<<1, 256, 0, s>>>(cache, T, sc, n, out, TE_star, gpus_star, mode, best, max_dT);
   return cudaGetLastError();
 }

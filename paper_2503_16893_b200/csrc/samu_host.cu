@@ -979,7 +979,199 @@ struct Greedy {
     return SAMU_OK;
   }
 
-  samu_status run(uint64_t seed, int T_total, samu_plan* plan) {
+  struct Cand { std::vector<Ent> E; Ent P; };
+
+  // Score candidate stages on the device: full simulations of every entry, f* per candidate,
+  // cut simulations of the other entries at t_E^(k), then T_E and the choice.  mode 0: Alg. 1's
+  // argmax dT/dN (ties: dN, node, tp, dp); mode 1: argmax T_E (ties: first candidate).
+  samu_status score_batch(const std::vector<Cand>& cands, double TE_star, int g_star, int mode, int32_t* best,
+                          double* maxdT, std::vector<StageOut>& so) {
+    cudaStream_t s = c->stream;
+    const int nc = (int)cands.size();
+    std::vector<StageCand> sc(nc);
+    for (int x = 0; x < nc; ++x) {
+      StageCand& q = sc[x];
+      std::memset(&q, 0, sizeof(q));
+      q.n_entries = (int)cands[x].E.size();
+      q.gpus = 0;
+      for (int i = 0; i < q.n_entries; ++i) {
+        const Ent& e = cands[x].E[i];
+        RET(ensure_full(e, cands[x].E, &q.full_slot[i]));
+        q.node[i] = e.node;
+        q.cut_slot[i] = -1;
+        q.gpus += e.dp * e.tp;
+      }
+      q.changed_node = cands[x].P.node;
+      q.changed_dp = cands[x].P.dp;
+      q.changed_tp = cands[x].P.tp;
+    }
+    RET(flush());
+    CK(c, upload(d_sc, sc, s));
+    CK(c, d_out.ensure(sizeof(StageOut) * nc));
+    CK(c, samu_count(c, launch_fstar(cache.as<samu_trial_rec>(), T, d_sc.as<StageCand>(), nc, d_out.as<StageOut>(), s)));
+    so.assign(nc, StageOut{});
+    CK(c, cudaMemcpyAsync(so.data(), d_out.p, sizeof(StageOut) * nc, cudaMemcpyDeviceToHost, s));
+    CK(c, cudaStreamSynchronize(s));
+    for (int x = 0; x < nc; ++x) {
+      const int f = so[x].fstar;
+      for (int i = 0; i < sc[x].n_entries; ++i)
+        if (i != f) RET(ensure_cut(cands[x].E[i], cands[x].E[f], cands[x].E, sc[x].full_slot[f], &sc[x].cut_slot[i]));
+    }
+    RET(flush());
+    CK(c, upload(d_sc, sc, s));
+    CK(c, samu_count(c, launch_stage_score(cache.as<samu_trial_rec>(), T, d_sc.as<StageCand>(), nc, d_out.as<StageOut>(),
+                                           TE_star, g_star, mode, d_best.as<int32_t>(),
+                                           reinterpret_cast<double*>(d_best.as<char>() + 8), s)));
+    evals += nc;
+    CK(c, cudaMemcpyAsync(best, d_best.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CK(c, cudaMemcpyAsync(maxdT, d_best.as<char>() + 8, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(c, cudaMemcpyAsync(so.data(), d_out.p, sizeof(StageOut) * nc, cudaMemcpyDeviceToHost, s));
+    CK(c, cudaStreamSynchronize(s));
+    return SAMU_OK;
+  }
+
+  std::vector<std::vector<std::pair<int, int>>> plans;
+
+  // Algorithm 1 inner loop
+  samu_status choose_greedy(const std::vector<int>& unfinished, const std::vector<int>& undone, std::vector<Ent>& Es,
+                            StageOut& chosen) {
+    const int N = (int)c->eng.n_gpus;
+    double TE_star = 0.0;
+    for (;;) {
+      std::vector<int> ready;
+      for (int v : unfinished) {
+        const int u = c->node_input[v];
+        bool ok = u < 0 || !undone[u];
+        for (const Ent& e : Es) if (e.node == u) ok = true;
+        if (ok) ready.push_back(v);
+      }
+      std::vector<Cand> cands;
+      int g_star = 0;
+      for (const Ent& e : Es) g_star += e.dp * e.tp;
+      for (int v : ready)
+        for (auto& pl : plans[v]) {
+          Ent P{v, pl.first, pl.second};
+          int prime = -1;
+          for (size_t i = 0; i < Es.size(); ++i) if (Es[i].node == v) prime = (int)i;
+          std::vector<Ent> E = Es;
+          int gE = 0;
+          if (prime >= 0) {
+            E[prime] = P;
+            for (const Ent& x : E) gE += x.dp * x.tp;
+            if (!(g_star < gE && gE <= N)) continue;      // Alg. 1 line 11
+          } else {
+            E.push_back(P);
+            for (const Ent& x : E) gE += x.dp * x.tp;
+            if (gE > N) continue;                          // Alg. 1 line 14
+          }
+          std::sort(E.begin(), E.end(), [](const Ent& a, const Ent& b) { return a.node < b.node; });
+          cands.push_back({E, P});
+        }
+      if (cands.empty()) break;
+      int32_t best = -1;
+      double maxdT = 0.0;
+      std::vector<StageOut> so;
+      RET(score_batch(cands, TE_star, g_star, 0, &best, &maxdT, so));
+      if (maxdT < 0.0) break;                               // Alg. 1 line 19
+      Es = cands[best].E;
+      TE_star = so[best].TE;
+      chosen = so[best];
+    }
+    return SAMU_OK;
+  }
+
+  // Max-heuristic: all GPUs to the lowest-id ready model, plan of highest stage
+  // throughput (ties: enumeration order), stage runs that model to completion
+  samu_status choose_max(const std::vector<int>& unfinished, const std::vector<int>& undone, std::vector<Ent>& Es,
+                         StageOut& chosen) {
+    int v = -1;
+    for (int u : unfinished) {
+      const int in = c->node_input[u];
+      if (in < 0 || !undone[in]) { v = u; break; }
+    }
+    if (v < 0) return SAMU_OK;
+    std::vector<Cand> cands;
+    for (auto& pl : plans[v]) {
+      Ent P{v, pl.first, pl.second};
+      cands.push_back({std::vector<Ent>{P}, P});
+    }
+    if (cands.empty()) return SAMU_OK;
+    int32_t best = -1;
+    double mx = 0.0;
+    std::vector<StageOut> so;
+    RET(score_batch(cands, 0.0, 0, 1, &best, &mx, so));
+    Es = cands[best].E;
+    chosen = so[best];
+    return SAMU_OK;
+  }
+
+  // Min-heuristic: as many ready models as GPUs allow (lowest ids first; a model
+  // whose input is selected in the same stage counts as ready), GPUs split as evenly as possible,
+  // the combination of highest stage throughput among the splits and the plans using exactly the
+  // assigned GPUs (<= 10^4 combinations in enumeration order; ties: first); one model fewer if
+  // no combination exists
+  samu_status choose_min(const std::vector<int>& unfinished, const std::vector<int>& undone, std::vector<Ent>& Es,
+                         StageOut& chosen) {
+    const int N = (int)c->eng.n_gpus;
+    std::vector<int> sel;
+    for (int v : unfinished) {
+      if ((int)sel.size() >= N) break;
+      const int in = c->node_input[v];
+      bool ok = in < 0 || !undone[in];
+      for (int x : sel) if (x == in) ok = true;
+      if (ok) sel.push_back(v);
+    }
+    for (int k = (int)sel.size(); k >= 1 && Es.empty(); --k) {
+      const int base = N / k, extra = N % k;
+      std::vector<Cand> cands;
+      std::vector<int> pick(extra);
+      for (int i = 0; i < extra; ++i) pick[i] = i;
+      bool more = true;
+      while (more && cands.size() < 10000) {
+        std::vector<int> gv(k, base);
+        for (int i : pick) gv[i] += 1;
+        std::vector<std::vector<int>> opts(k);
+        bool feasible = true;
+        for (int i = 0; i < k; ++i) {
+          for (size_t pi = 0; pi < plans[sel[i]].size(); ++pi)
+            if (plans[sel[i]][pi].first * plans[sel[i]][pi].second == gv[i]) opts[i].push_back((int)pi);
+          if (opts[i].empty()) feasible = false;
+        }
+        if (feasible) {
+          std::vector<int> idx(k, 0);
+          for (;;) {
+            if (cands.size() >= 10000) break;
+            std::vector<Ent> E;
+            for (int i = 0; i < k; ++i) {
+              const auto& pl = plans[sel[i]][opts[i][idx[i]]];
+              E.push_back({sel[i], pl.first, pl.second});
+            }
+            cands.push_back({E, E[0]});
+            int q = k - 1;   // odometer, last model fastest
+            while (q >= 0 && ++idx[q] == (int)opts[q].size()) { idx[q] = 0; --q; }
+            if (q < 0) break;
+          }
+        }
+        int i = extra - 1;
+        while (i >= 0 && pick[i] == k - extra + i) --i;
+        if (i < 0) more = false;
+        else {
+          ++pick[i];
+          for (int j2 = i + 1; j2 < extra; ++j2) pick[j2] = pick[j2 - 1] + 1;
+        }
+      }
+      if (cands.empty()) continue;
+      int32_t best = -1;
+      double mx = 0.0;
+      std::vector<StageOut> so;
+      RET(score_batch(cands, 0.0, 0, 1, &best, &mx, so));
+      Es = cands[best].E;
+      chosen = so[best];
+    }
+    return SAMU_OK;
+  }
+
+  samu_status run(uint64_t seed, int T_total, int algo, samu_plan* plan) {
     T = T_total;
     n = (size_t)c->n_req;
     trial_share(T, c->world, c->rank, &tb, &Tl);
@@ -1004,10 +1196,9 @@ struct Greedy {
     S = StatePtrs{st.as<uint32_t>(), g.as<uint16_t>(), fin_t.as<double>(), over.as<double>()};
     CK(c, d_best.ensure(sizeof(int32_t) + sizeof(double)));
     CK(c, d_any.ensure(sizeof(int32_t) * (size_t)c->n_nodes * std::max(Tl, 1) + 2 * sizeof(int32_t) * SAMU_MAX_NODES));
-    std::vector<std::vector<std::pair<int, int>>> plans(c->n_nodes);
+    plans.assign(c->n_nodes, {});
     for (int v = 0; v < c->n_nodes; ++v) plans[v] = plans_of(c, c->node_model[v]);
     std::memset(plan, 0, sizeof(*plan));
-    const int N = (int)c->eng.n_gpus;
     for (;;) {
       // unfinished nodes (in any trial of any rank)
       std::vector<int> undone(c->n_nodes, 0);
@@ -1015,90 +1206,14 @@ struct Greedy {
       std::vector<int> unfinished;
       for (int v = 0; v < c->n_nodes; ++v) if (undone[v]) unfinished.push_back(v);
       if (unfinished.empty()) break;
-      if (plan->n_stages >= 64) FAIL(c, SAMU_E_STATE, "plan_greedy: too many stages");
+      if (plan->n_stages >= 64) FAIL(c, SAMU_E_STATE, "plan: too many stages");
       full_slot.clear(); cut_slot.clear(); fin_buf.clear(); n_slots = 0;
       std::vector<Ent> Es;
-      double TE_star = 0.0;
       StageOut chosen{};
-      for (;;) {
-        std::vector<int> ready;
-        for (int v : unfinished) {
-          const int u = c->node_input[v];
-          bool ok = u < 0 || !undone[u];
-          for (const Ent& e : Es) if (e.node == u) ok = true;
-          if (ok) ready.push_back(v);
-        }
-        struct Cand { std::vector<Ent> E; Ent P; };
-        std::vector<Cand> cands;
-        int g_star = 0;
-        for (const Ent& e : Es) g_star += e.dp * e.tp;
-        for (int v : ready)
-          for (auto& pl : plans[v]) {
-            Ent P{v, pl.first, pl.second};
-            int prime = -1;
-            for (size_t i = 0; i < Es.size(); ++i) if (Es[i].node == v) prime = (int)i;
-            std::vector<Ent> E = Es;
-            int gE = 0;
-            if (prime >= 0) {
-              E[prime] = P;
-              for (const Ent& x : E) gE += x.dp * x.tp;
-              if (!(g_star < gE && gE <= N)) continue;      // Alg. 1 line 11
-            } else {
-              E.push_back(P);
-              for (const Ent& x : E) gE += x.dp * x.tp;
-              if (gE > N) continue;                          // Alg. 1 line 14
-            }
-            std::sort(E.begin(), E.end(), [](const Ent& a, const Ent& b) { return a.node < b.node; });
-            cands.push_back({E, P});
-          }
-        if (cands.empty()) break;
-        const int nc = (int)cands.size();
-        std::vector<StageCand> sc(nc);
-        for (int x = 0; x < nc; ++x) {
-          StageCand& q = sc[x];
-          std::memset(&q, 0, sizeof(q));
-          q.n_entries = (int)cands[x].E.size();
-          q.gpus = 0;
-          for (int i = 0; i < q.n_entries; ++i) {
-            const Ent& e = cands[x].E[i];
-            RET(ensure_full(e, cands[x].E, &q.full_slot[i]));
-            q.node[i] = e.node;
-            q.cut_slot[i] = -1;
-            q.gpus += e.dp * e.tp;
-          }
-          q.changed_node = cands[x].P.node;
-          q.changed_dp = cands[x].P.dp;
-          q.changed_tp = cands[x].P.tp;
-        }
-        RET(flush());
-        CK(c, upload(d_sc, sc, s));
-        CK(c, d_out.ensure(sizeof(StageOut) * nc));
-        CK(c, samu_count(c, launch_fstar(cache.as<samu_trial_rec>(), T, d_sc.as<StageCand>(), nc, d_out.as<StageOut>(), s)));
-        std::vector<StageOut> so(nc);
-        CK(c, cudaMemcpyAsync(so.data(), d_out.p, sizeof(StageOut) * nc, cudaMemcpyDeviceToHost, s));
-        CK(c, cudaStreamSynchronize(s));
-        for (int x = 0; x < nc; ++x) {
-          const int f = so[x].fstar;
-          for (int i = 0; i < sc[x].n_entries; ++i)
-            if (i != f) RET(ensure_cut(cands[x].E[i], cands[x].E[f], cands[x].E, sc[x].full_slot[f], &sc[x].cut_slot[i]));
-        }
-        RET(flush());
-        CK(c, upload(d_sc, sc, s));
-        CK(c, samu_count(c, launch_stage_score(cache.as<samu_trial_rec>(), T, d_sc.as<StageCand>(), nc, d_out.as<StageOut>(), TE_star,
-                                 g_star, d_best.as<int32_t>(), reinterpret_cast<double*>(d_best.as<char>() + 8), s)));
-        evals += nc;
-        int32_t best = -1;
-        double maxdT = 0.0;
-        CK(c, cudaMemcpyAsync(&best, d_best.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        CK(c, cudaMemcpyAsync(&maxdT, d_best.as<char>() + 8, sizeof(double), cudaMemcpyDeviceToHost, s));
-        CK(c, cudaMemcpyAsync(so.data(), d_out.p, sizeof(StageOut) * nc, cudaMemcpyDeviceToHost, s));
-        CK(c, cudaStreamSynchronize(s));
-        if (maxdT < 0.0) break;                               // Alg. 1 line 19
-        Es = cands[best].E;
-        TE_star = so[best].TE;
-        chosen = so[best];
-      }
-      if (Es.empty()) FAIL(c, SAMU_E_INFEASIBLE, "plan_greedy: no ready model fits an empty stage");
+      if (algo == 0) RET(choose_greedy(unfinished, undone, Es, chosen));
+      else if (algo == 1) RET(choose_max(unfinished, undone, Es, chosen));
+      else RET(choose_min(unfinished, undone, Es, chosen));
+      if (Es.empty()) FAIL(c, SAMU_E_INFEASIBLE, "plan: no ready model fits an empty stage");
       evals += 1;   // the stage is scored once more at commit (oracle parity of the counter)
       // commit (Alg. 1 lines 24-25): f* to completion, the others cut at t_E^(k), state carried
       const int f = chosen.fstar;
@@ -1171,20 +1286,32 @@ struct Greedy {
 
 }  // namespace
 
-extern "C" samu_status samu_plan_greedy(samu_ctx* c, uint64_t seed, int32_t n_trials, samu_plan** out) {
+static samu_status plan_with(samu_ctx* c, uint64_t seed, int32_t n_trials, int algo, samu_plan** out) {
   GUARD(c);
-  if (!out || n_trials < 1) FAIL(c, SAMU_E_INVALID, "plan_greedy: bad arguments");
-  if (!c->app_loaded) FAIL(c, SAMU_E_INVALID, "plan_greedy: no app loaded");
+  if (!out || n_trials < 1) FAIL(c, SAMU_E_INVALID, "plan: bad arguments");
+  if (!c->app_loaded) FAIL(c, SAMU_E_INVALID, "plan: no app loaded");
   *out = nullptr;
   samu_plan* p = new samu_plan();
   Greedy G;
   G.c = c;
   const int64_t sims0 = c->n_sims;
-  samu_status rc = G.run(seed, n_trials, p);
+  samu_status rc = G.run(seed, n_trials, algo, p);
   if (rc != SAMU_OK) { delete p; return rc; }
   p->n_sims = c->n_sims - sims0;
   *out = p;
   return SAMU_OK;
+}
+
+extern "C" samu_status samu_plan_greedy(samu_ctx* c, uint64_t seed, int32_t n_trials, samu_plan** out) {
+  return plan_with(c, seed, n_trials, 0, out);
+}
+
+extern "C" samu_status samu_plan_max_heuristic(samu_ctx* c, uint64_t seed, int32_t n_trials, samu_plan** out) {
+  return plan_with(c, seed, n_trials, 1, out);
+}
+
+extern "C" samu_status samu_plan_min_heuristic(samu_ctx* c, uint64_t seed, int32_t n_trials, samu_plan** out) {
+  return plan_with(c, seed, n_trials, 2, out);
 }
 
 extern "C" void samu_plan_free(samu_plan* p) { delete p; }

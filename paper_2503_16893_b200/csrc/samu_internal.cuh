@@ -113,5 +113,5 @@ struct StageOut {
 cudaError_t launch_fstar(const samu_trial_rec* cache, int32_t T, const StageCand* sc, int32_t n, StageOut* out,
                          cudaStream_t s);
 cudaError_t launch_stage_score(const samu_trial_rec* cache, int32_t T, const StageCand* sc, int32_t n,
-                               StageOut* out, double TE_star, int32_t gpus_star, int32_t* best,
+                               StageOut* out, double TE_star, int32_t gpus_star, int32_t mode, int32_t* best,
                                double* max_dT, cudaStream_t s);

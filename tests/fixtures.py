@@ -68,3 +68,20 @@ def multi(node_specs, eng=None, n_trials=1):
         loads.append(ns.get("load") if ns.get("load") is not None else zero_load())
     return W.custom_workload(sps, reqs, n_trials=n_trials, engine=eng or engine(), ecdfs=ecdfs,
                              coeff=cfs, load=loads)
+
+
+def fig1():
+    """S:645 (the paper's Fig. 1 shape): 4 GPUs, 6 models, one sequence per replica, 1 s per
+    iteration, no load cost; model 0 has 8 one-token requests, models 1-5 three each (23
+    GPU-seconds of work, so no schedule beats 5.75 s)."""
+    sp = spec(tp_values=(1,))
+    nodes = [dict(l_in=[4] * 8, l_out=[1] * 8, sp=sp)] + [dict(l_in=[4] * 3, l_out=[1] * 3, sp=sp)
+                                                           for _ in range(5)]
+    return multi(nodes, eng=engine(n_gpus=4, max_num_seqs=1))
+
+
+def even_split_4x8():
+    """P:743's Min-heuristic example: 8 GPUs, 4 models, model 0 the smallest."""
+    sp = spec(tp_values=(1, 2))
+    nodes = [dict(l_in=[4] * n, l_out=[3] * n, sp=sp) for n in (40, 400, 400, 400)]
+    return multi(nodes, eng=engine(n_gpus=8, max_num_seqs=16))

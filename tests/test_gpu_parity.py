@@ -244,10 +244,12 @@ def test_summary_mean_and_percentiles():
     ("c3", dict(n_prompts=600), 2),
     ("c4", dict(n_docs=60), 2),
 ])
-def test_greedy_plan_bit_exact(name, kw, T):
+@pytest.mark.parametrize("algo", ["greedy", "max", "min"])
+def test_greedy_plan_bit_exact(name, kw, T, algo):
+    # Algorithm 1 and the paper's two competitors on the same device estimator
     w = W.make_workload(name, n_trials=T, **kw)
-    po = O.Problem(w).plan_greedy(SEED, T)
-    pg = gpu(w).samu_plan_greedy(SEED, T)
+    po = O.Problem(w).plan_greedy(SEED, T, algo)
+    pg = gpu(w).samu_plan_greedy(SEED, T, algo)
     assert len(pg["stages"]) == len(po["stages"])
     for sg, so in zip(pg["stages"], po["stages"]):
         assert sg["entries"] == so["entries"]
@@ -256,6 +258,16 @@ def test_greedy_plan_bit_exact(name, kw, T):
         assert sg["T_E"] == so["T_E"]
     assert pg["total"] == po["total"]
     assert pg["n_cand_evals"] == po["n_cand_evals"]
+
+
+@pytest.mark.parametrize("algo", ["greedy", "max", "min"])
+def test_planners_fig1_and_even_split_fixtures(algo):
+    # S:645 Fig. 1 fixture and the P:743 repartition example, every planner bit-exact
+    for w, T in ((F.fig1(), 1), (F.even_split_4x8(), 2)):
+        po = O.Problem(w).plan_greedy(SEED, T, algo)
+        pg = gpu(w).samu_plan_greedy(SEED, T, algo)
+        pg.pop("n_sims")
+        assert pg == po
 
 
 # ------------------------------------------------------------------------------------------

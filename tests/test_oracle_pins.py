@@ -499,3 +499,58 @@ def test_hand_trace_dependencies_summarise_then_evaluate():
         assert rc["t_end"][0] == 3.0 and rc["flags"][0] == 2
         assert (st["st"][0, 4] >> 28) == O.ST_DONE and (st["st"][0, 5] >> 28) == O.ST_FRESH
         assert st["over"][0, 1, 0] == 0.5
+
+
+# ------------------------------------------------------------------------------------------
+# the paper's competitors: Max- / Min-heuristic and the Fig. 1 fixture
+# ------------------------------------------------------------------------------------------
+_fig1 = F.fig1
+
+
+def test_fig1_greedy_beats_max_and_min_heuristics():
+    # S:645 / P:734: greedy strictly better than Max-heuristic, no worse than Min-heuristic, and
+    # within 5% of the optimum (bounded below by total work / N = 5.75 s)
+    P = O.Problem(_fig1())
+    g, mx, mn = (P.plan_greedy(SEED, 1, a)["total"] for a in ("greedy", "max", "min"))
+    assert g < mx and g <= mn
+    assert g <= 1.05 * 5.75
+    # Max-heuristic closed form: model 0 on 4 replicas = 2 s, then each 3-request model on 3
+    # replicas (4 gives the same throughput; ties keep fewer GPUs) = 1 s: 2 + 5 = 7 s
+    assert mx == 7.0
+
+
+def test_max_heuristic_structure():
+    # P:664 / S:440: every stage has exactly one entry, that model runs to completion (it never
+    # reappears), models are taken in id order once ready
+    for w in (_fig1(), W.make_workload("c2", n_prompts=60, n_trials=2),
+              W.make_workload("c4", n_docs=20, n_trials=2)):
+        plan = O.Problem(w).plan_greedy(SEED, 2, "max")
+        nodes = [s["entries"][0][0] for s in plan["stages"]]
+        assert all(len(s["entries"]) == 1 and s["fstar"] == s["entries"][0][0] for s in plan["stages"])
+        assert nodes == sorted(set(nodes)) == list(range(w.n_nodes))
+
+
+def test_min_heuristic_even_split_paper_example():
+    # "when there are 4 LLMs unfinished, Min-heuristic assigns 2 GPUs to each LLM. After 1
+    # LLM finishes, Min-heuristic then repartitions the GPUs to make 2 LLMs have 3 GPUs each ...
+    # and 1 LLM keeps its previously assigned 2 GPUs."  8 GPUs, 4 models, model 0 the smallest.
+    w = F.even_split_4x8()
+    plan = O.Problem(w).plan_greedy(SEED, 1, "min")
+    s0, s1 = plan["stages"][0], plan["stages"][1]
+    assert sorted(d * t for (_, d, t) in s0["entries"]) == [2, 2, 2, 2]
+    assert s0["fstar"] == 0
+    assert [e[0] for e in s1["entries"]] == [1, 2, 3]
+    assert sorted(d * t for (_, d, t) in s1["entries"]) == [2, 3, 3]
+
+
+def test_min_heuristic_structure():
+    # per-stage GPU counts differ by at most 1 and, when a split exists, all N GPUs are
+    # used; as many ready models as GPUs allow
+    for w in (_fig1(), W.make_workload("c2", n_prompts=60, n_trials=2),
+              W.make_workload("c4", n_docs=20, n_trials=2)):
+        N = w.engine["n_gpus"]
+        plan = O.Problem(w).plan_greedy(SEED, 2, "min")
+        for s in plan["stages"]:
+            gv = [d * t for (_, d, t) in s["entries"]]
+            assert max(gv) - min(gv) <= 1
+            assert sum(gv) <= N
