@@ -189,6 +189,12 @@ int32_t samu_enumerate_plans(samu_ctx* ctx, int32_t node, int32_t* dp, int32_t* 
 samu_status samu_sample_lengths(samu_ctx* ctx, uint64_t seed, int32_t trial_begin, int32_t n_trials,
                                 uint16_t* out_l_out, uint16_t* out_l_in_eff);
 
+/* Known output lengths in place of the sampler (the §5.5 cost-model ablation):
+ * host l_true [n_req] (copied before return) -> device out_l_out / out_l_in_eff [1][n_req] with
+ * the sampler's clamps and chained-prompt arithmetic.  Synchronises the context stream. */
+samu_status samu_known_lengths(samu_ctx* ctx, const uint32_t* l_true, uint16_t* out_l_out,
+                               uint16_t* out_l_in_eff);
+
 /* Simulate n_cands candidates over the n_trials local trials whose lengths are given
  * (device l_out / l_in_eff [n_trials][n_req], from samu_sample_lengths or known lengths).
  *   state       device WorkloadState or NULL (fresh, no commit):
@@ -226,6 +232,23 @@ samu_status samu_plan_greedy(samu_ctx* ctx, uint64_t seed, int32_t n_trials, sam
  *     first finish and every unfinished model is re-planned. */
 samu_status samu_plan_max_heuristic(samu_ctx* ctx, uint64_t seed, int32_t n_trials, samu_plan** out);
 samu_status samu_plan_min_heuristic(samu_ctx* ctx, uint64_t seed, int32_t n_trials, samu_plan** out);
+
+/* General planner entry (all of the above plus the §5.5 ablations):
+ *   algo              SAMU_ALGO_GREEDY / _MAX / _MIN
+ *   allow_preemption  0 = no-preemption variant: a model keeps its plan and GPUs from the stage
+ *                     it starts in until it finishes and is not re-planned (reading c29); the
+ *                     Max-heuristic is the same either way
+ *   known_l_out       host [n_req] true output lengths in place of the sampler, or NULL;
+ *                     requires n_trials == 1 (reading c30) */
+#define SAMU_ALGO_GREEDY 0
+#define SAMU_ALGO_MAX 1
+#define SAMU_ALGO_MIN 2
+typedef struct samu_plan_opts {
+  int32_t algo;
+  int32_t allow_preemption;
+  const uint32_t* known_l_out;
+} samu_plan_opts;
+samu_status samu_plan_run(samu_ctx* ctx, uint64_t seed, int32_t n_trials, const samu_plan_opts* opts, samu_plan** out);
 void samu_plan_free(samu_plan* plan);
 
 #ifdef __cplusplus

@@ -110,6 +110,8 @@ def lib():
         L.or_plan_greedy.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(or_plan)]
         L.or_plan_max_heuristic.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(or_plan)]
         L.or_plan_min_heuristic.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(or_plan)]
+        L.or_known_lengths.argtypes = [P, P, P, P]
+        L.or_plan_run.argtypes = [P, C.c_uint64, C.c_int32, C.c_int32, C.c_int32, P, C.POINTER(or_plan)]
         _lib = L
     return _lib
 
@@ -224,6 +226,14 @@ class Problem:
         _check(lib().or_sample_lengths(self.h, seed, trial_begin, n_trials, _ptr(lo), _ptr(li)))
         return lo, li
 
+    def known_lengths(self, l_true):
+        """Known output lengths in place of the sampler: one trial [1, n]."""
+        lt = np.ascontiguousarray(l_true, np.uint32).reshape(self.n_req)
+        lo = np.zeros((1, self.n_req), np.uint16)
+        li = np.zeros((1, self.n_req), np.uint16)
+        _check(lib().or_known_lengths(self.h, _ptr(lt), _ptr(lo), _ptr(li)))
+        return lo, li
+
     def fresh_state(self, n_trials):
         return dict(st=np.zeros((n_trials, self.n_req), np.uint32),
                     g=np.zeros((n_trials, self.n_req), np.uint16),
@@ -251,11 +261,13 @@ class Problem:
         _check(lib().or_simulate_many(self.h, len(cands), cs, T, _ptr(l_out), _ptr(l_in), n_threads, _ptr(rec)))
         return rec
 
-    def plan_greedy(self, seed, n_trials, algo="greedy"):
+    def plan_greedy(self, seed, n_trials, algo="greedy", preemption=True, known_l_out=None):
+        """algo greedy (Alg. 1) / max / min; preemption=False and known_l_out are the
+        §5.5 ablations (known_l_out needs n_trials == 1)."""
         plan = or_plan()
-        fn = {"greedy": lib().or_plan_greedy, "max": lib().or_plan_max_heuristic,
-              "min": lib().or_plan_min_heuristic}[algo]
-        _check(fn(self.h, seed, n_trials, C.byref(plan)))
+        lt = None if known_l_out is None else np.ascontiguousarray(known_l_out, np.uint32)
+        _check(lib().or_plan_run(self.h, seed, n_trials, {"greedy": 0, "max": 1, "min": 2}[algo],
+                             1 if preemption else 0, _ptr(lt), C.byref(plan)))
         stages = []
         for i in range(plan.n_stages):
             s = plan.stages[i]

@@ -205,6 +205,24 @@ extern "C" int32_t or_sample_lengths(const or_problem* p, uint64_t seed, int32_t
   return OR_OK;
 }
 
+// Known output lengths ("replace the output lengths generated by the output sampler
+// in the cost model with the real output lengths"; reading c30): l_true[r] takes the place of the
+// sampled X, with the same clamps (cap, l_max - l_in) and the same chained prompt arithmetic.
+extern "C" int32_t or_known_lengths(const or_problem* p, const uint32_t* l_true, uint16_t* l_out, uint16_t* l_in_eff) {
+  const int n = (int)p->req.size();
+  for (int r = 0; r < n; ++r) {
+    const Req& q = p->req[r];
+    const Model& M = p->models[p->node_model[q.node]];
+    uint32_t lin = q.l_in_base;
+    if (q.pred >= 0) lin += std::max<uint32_t>(l_out[q.pred], 1u);
+    lin = std::min(lin, M.l_max);
+    uint32_t out = std::min(std::min(l_true[r], q.cap_y), M.l_max - lin);
+    l_out[r] = (uint16_t)out;
+    l_in_eff[r] = (uint16_t)lin;
+  }
+  return OR_OK;
+}
+
 // ---------------------------------------------------------------------------------------------
 // Cost model pieces
 // ---------------------------------------------------------------------------------------------
@@ -658,6 +676,8 @@ struct Greedy {
   std::vector<double> fin_t, over;
   std::vector<Entry> prev;   // previous committed stage
   int64_t evals = 0;
+  bool preempt = true;              // false: the no-preemption ablation (reading c29)
+  const uint32_t* known = nullptr;  // known output lengths (reading c30)
 
   bool done_in(int node, int k) const {
     for (int r = p->node_begin[node]; r < p->node_end[node]; ++r)
@@ -775,7 +795,8 @@ struct Greedy {
   void init(uint64_t seed) {
     l_out.assign((size_t)T * n, 0);
     l_in.assign((size_t)T * n, 0);
-    or_sample_lengths(p, seed, 0, T, l_out.data(), l_in.data());
+    if (known) or_known_lengths(p, known, l_out.data(), l_in.data());
+    else or_sample_lengths(p, seed, 0, T, l_out.data(), l_in.data());
     st.assign((size_t)T * n, st_make(OR_ST_FRESH, 0));
     g.assign((size_t)T * n, 0);
     fin_t.assign((size_t)T * n, std::numeric_limits<double>::infinity());
@@ -815,10 +836,26 @@ struct Greedy {
     return OR_OK;
   }
 
+  // No-preemption: "the execution plan of a model would not be changed once chosen and a
+  // running model would not be stopped once started" -- every model of the previous stage that is
+  // unfinished keeps its entry (reading c29)
+  std::vector<Entry> pinned() const {
+    std::vector<Entry> E;
+    if (preempt) return E;
+    for (const Entry& e : prev) if (!done_all(e.node)) E.push_back(e);
+    return E;
+  }
+  bool is_pinned(const std::vector<Entry>& pin, int v) const {
+    for (const Entry& e : pin) if (e.node == v) return true;
+    return false;
+  }
+
   // Algorithm 1 inner loop: the stage E* for the current workload
   int choose_greedy(const std::vector<int>& unfinished, std::vector<Entry>& Es) {
     const int N = (int)p->eng.n_gpus;
+    const std::vector<Entry> pin = pinned();
     Score s_star{0.0, -1, std::vector<double>(T, 0.0), 0.0};
+    if (!pin.empty()) { Es = pin; s_star = score(Es); }   // E* starts from the running models
     for (;;) {
       // ready models: unfinished, and their input node finished or selected in E* (Alg.1 l.5)
       std::vector<int> ready;
@@ -832,6 +869,7 @@ struct Greedy {
       std::vector<Cand> cands;
       const int g_star = gpus(Es);
       for (int v : ready) {
+        if (is_pinned(pin, v)) continue;
         for (size_t pi = 0; pi < plans_dp[v].size(); ++pi) {
           Entry P{v, plans_dp[v][pi], plans_tp[v][pi]};
           int prime = -1;
@@ -902,17 +940,24 @@ struct Greedy {
   // possible (floor(N/k) each, N mod k of them one more); among those splits and the plans that
   // use exactly the assigned GPUs, the combination of highest stage throughput (at most 10^4
   // combinations in enumeration order; ties: first); if no combination exists, one model fewer
+  // No-preemption (reading c29): the running models keep their entries; the free GPUs are split
+  // the same way among the other ready models.
   int choose_min(const std::vector<int>& unfinished, std::vector<Entry>& Es) {
-    const int N = (int)p->eng.n_gpus;
+    const std::vector<Entry> pin = pinned();
+    const int N = (int)p->eng.n_gpus - gpus(pin);
     std::vector<int> sel;
     for (int v : unfinished) {
       if ((int)sel.size() >= N) break;
+      if (is_pinned(pin, v)) continue;
       int in = p->node_input[v];
       bool ok = in < 0 || done_all(in);
       for (int x : sel) if (x == in) ok = true;
+      for (const Entry& e : pin) if (e.node == in) ok = true;
       if (ok) sel.push_back(v);
     }
-    for (int k = (int)sel.size(); k >= 1 && Es.empty(); --k) {
+    Es.clear();
+    bool found = false;
+    for (int k = (int)sel.size(); k >= 1 && !found; --k) {
       const int base = N / k, extra = N % k;
       double bT = 0.0;
       long count = 0;
@@ -936,13 +981,14 @@ struct Greedy {
           for (;;) {
             if (count >= 10000) break;
             ++count;
-            std::vector<Entry> E;
+            std::vector<Entry> E = pin;
             for (int i = 0; i < k; ++i) {
               int v = sel[i], pi = opts[i][idx[i]];
               E.push_back({v, plans_dp[v][pi], plans_tp[v][pi]});
             }
+            std::sort(E.begin(), E.end(), [](const Entry& a, const Entry& b) { return a.node < b.node; });
             Score sc = score(E);
-            if (Es.empty() || sc.TE > bT) { Es = E; bT = sc.TE; }
+            if (!found || sc.TE > bT) { Es = E; bT = sc.TE; found = true; }
             int q = k - 1;   // odometer, last model fastest
             while (q >= 0 && ++idx[q] == (int)opts[q].size()) { idx[q] = 0; --q; }
             if (q < 0) break;
@@ -958,6 +1004,7 @@ struct Greedy {
         }
       }
     }
+    if (!found) Es = pin;
     return OR_OK;
   }
 
@@ -983,10 +1030,14 @@ struct Greedy {
   }
 };
 
-static int32_t plan_with(const or_problem* p, uint64_t seed, int32_t n_trials, int algo, or_plan* out) {
+static int32_t plan_with(const or_problem* p, uint64_t seed, int32_t n_trials, int algo, or_plan* out,
+                         int preempt = 1, const uint32_t* known = nullptr) {
+  if (known && n_trials != 1) { set_err("known lengths: one trial"); return OR_E_INVALID; }
   Greedy G;
   G.p = p;
   G.T = n_trials;
+  G.preempt = preempt != 0;
+  G.known = known;
   G.n = p->req.size();
   G.nn = p->node_model.size();
   try {
@@ -1007,4 +1058,10 @@ extern "C" int32_t or_plan_min_heuristic(const or_problem* p, uint64_t seed, int
 
 extern "C" int32_t or_plan_greedy(const or_problem* p, uint64_t seed, int32_t n_trials, or_plan* out) {
   return plan_with(p, seed, n_trials, 0, out);
+}
+
+extern "C" int32_t or_plan_run(const or_problem* p, uint64_t seed, int32_t n_trials, int32_t algo, int32_t allow_preemption,
+                           const uint32_t* known_l_out, or_plan* out) {
+  if (algo < 0 || algo > 2) { set_err("bad algo"); return OR_E_INVALID; }
+  return plan_with(p, seed, n_trials, algo, out, allow_preemption, known_l_out);
 }

@@ -135,6 +135,13 @@ int32_t or_plan_greedy(const or_problem* p, uint64_t seed, int32_t n_trials, or_
 int32_t or_plan_max_heuristic(const or_problem* p, uint64_t seed, int32_t n_trials, or_plan* out);
 int32_t or_plan_min_heuristic(const or_problem* p, uint64_t seed, int32_t n_trials, or_plan* out);
 
+/* known output lengths in place of the sampler: l_true [n_req] */
+int32_t or_known_lengths(const or_problem* p, const uint32_t* l_true, uint16_t* l_out, uint16_t* l_in_eff);
+/* algo 0 greedy / 1 max / 2 min; allow_preemption = 0 is the §5.5 no-preemption ablation;
+ * known_l_out (NULL = sample) requires n_trials == 1 */
+int32_t or_plan_run(const or_problem* p, uint64_t seed, int32_t n_trials, int32_t algo, int32_t allow_preemption,
+                const uint32_t* known_l_out, or_plan* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -65,11 +65,19 @@ REC_DTYPE = np.dtype([("t_end", "<f8"), ("flops_lo", "<u8"), ("flops_hi", "<u8")
                       ("iters", "<u4"), ("flags", "<u4")])
 assert REC_DTYPE.itemsize == C.sizeof(samu_trial_rec) == 40
 
+
+class samu_plan_opts(C.Structure):
+    _fields_ = [("algo", C.c_int32), ("allow_preemption", C.c_int32), ("known_l_out", C.c_void_p)]
+
+
+ALGOS = {"greedy": 0, "max": 1, "min": 2}
+
 EXPORTED = ["samu_ctx_create", "samu_ctx_destroy", "samu_local_group_create", "samu_local_group_destroy",
             "samu_ctx_create_local", "samu_last_error", "samu_launch_count", "samu_nccl_unique_id",
             "samu_model_register",
             "samu_ecdf_load", "samu_app_load", "samu_enumerate_plans", "samu_sample_lengths", "samu_simulate_batch",
-            "samu_plan_greedy", "samu_plan_max_heuristic", "samu_plan_min_heuristic", "samu_plan_free"]
+            "samu_plan_greedy", "samu_plan_max_heuristic", "samu_plan_min_heuristic", "samu_plan_run", "samu_known_lengths",
+            "samu_plan_free"]
 
 _lib = None
 
@@ -104,6 +112,9 @@ def lib():
         L.samu_plan_greedy.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(C.POINTER(samu_plan))]
         L.samu_plan_max_heuristic.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(C.POINTER(samu_plan))]
         L.samu_plan_min_heuristic.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(C.POINTER(samu_plan))]
+        L.samu_plan_run.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(samu_plan_opts),
+                                    C.POINTER(C.POINTER(samu_plan))]
+        L.samu_known_lengths.argtypes = [P, P, P, P]
         L.samu_plan_free.argtypes = [C.POINTER(samu_plan)]
         L.samu_plan_free.restype = None
         _lib = L
@@ -247,6 +258,15 @@ class Samu:
         self._check(lib().samu_sample_lengths(self.h, seed, trial_begin, n_trials, _t_ptr(lo), _t_ptr(li)))
         return lo, li
 
+    def samu_known_lengths(self, l_true):
+        """Known output lengths in place of the sampler: [1, n_req] device tensors."""
+        torch = self.torch
+        lt = np.ascontiguousarray(np.asarray(l_true, dtype=np.uint32).reshape(self.n_req))
+        lo = torch.empty((1, self.n_req), dtype=torch.int16, device=self.device)
+        li = torch.empty((1, self.n_req), dtype=torch.int16, device=self.device)
+        self._check(lib().samu_known_lengths(self.h, lt.ctypes.data_as(C.c_void_p), _t_ptr(lo), _t_ptr(li)))
+        return lo, li
+
     def fresh_state(self, n_trials: int):
         torch = self.torch
         return dict(st=torch.zeros((n_trials, self.n_req), dtype=torch.int32, device=self.device),
@@ -283,12 +303,15 @@ class Samu:
                                    mean_flops=x.mean_flops, mean_req_iters=x.mean_req_iters) for x in summ[:nc]]
         return out
 
-    def samu_plan_greedy(self, seed: int, n_trials: int, algo: str = "greedy"):
-        """algo: "greedy" (Algorithm 1), "max" / "min" (the paper's Max- / Min-heuristic)."""
+    def samu_plan_greedy(self, seed: int, n_trials: int, algo: str = "greedy", preemption: bool = True,
+                         known_l_out=None):
+        """algo: "greedy" (Algorithm 1), "max" / "min" (the paper's Max- / Min-heuristic);
+        preemption=False / known_l_out are the §5.5 ablations (samu_plan_run)."""
         p = C.POINTER(samu_plan)()
-        fn = {"greedy": lib().samu_plan_greedy, "max": lib().samu_plan_max_heuristic,
-              "min": lib().samu_plan_min_heuristic}[algo]
-        self._check(fn(self.h, seed, n_trials, C.byref(p)))
+        lt = None if known_l_out is None else np.ascontiguousarray(np.asarray(known_l_out, dtype=np.uint32))
+        o = samu_plan_opts(ALGOS[algo], 1 if preemption else 0,
+                           None if lt is None else lt.ctypes.data_as(C.c_void_p).value)
+        self._check(lib().samu_plan_run(self.h, seed, n_trials, C.byref(o), C.byref(p)))
         try:
             P = p.contents
             stages = []

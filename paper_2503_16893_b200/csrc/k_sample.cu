@@ -39,8 +39,8 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 
 __global__ void __launch_bounds__(K1_THREADS) k_sample_lengths(DevApp app, DevEcdf e, const int32_t* __restrict__ seq_head,
                                                                int32_t n_seq, uint32_t k0, uint32_t k1, int32_t trial_begin,
-                                                               int32_t n_trials, uint16_t* __restrict__ l_out,
-                                                               uint16_t* __restrict__ l_in) {
+                                                               int32_t n_trials, const uint32_t* __restrict__ known,
+                                                               uint16_t* __restrict__ l_out, uint16_t* __restrict__ l_in) {
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) unsigned long long bar;
   __shared__ uint32_t s_lib[K1_THREADS], s_cap[K1_THREADS];
@@ -98,10 +98,15 @@ __global__ void __launch_bounds__(K1_THREADS) k_sample_lengths(DevApp app, DevEc
       const int32_t nd = first ? s_node[threadIdx.x] : __ldg(app.node + r);
       const int32_t m = __ldg(e.model_of_node + nd);
       const uint32_t l_max = __ldg(e.l_max_of_node + nd);
-      const uint32_t u = philox_word((uint32_t)r, (uint32_t)(trial_begin + k), (uint32_t)nd, k0, k1);
-      // inverse eCDF (c2): the t-th element of the sorted multiset, t = floor(u n / 2^32)
-      const uint32_t t = __umulhi(u, __ldg(e.n_obs + m));
-      const uint32_t X = (staged && m == bm) ? (uint32_t)tab[t] : (uint32_t)__ldg(e.tab + __ldg(e.tab_off + m) + t);
+      uint32_t X;
+      if (known) {   // known output lengths in place of the draw (reading c30)
+        X = __ldg(known + r);
+      } else {
+        const uint32_t u = philox_word((uint32_t)r, (uint32_t)(trial_begin + k), (uint32_t)nd, k0, k1);
+        // inverse eCDF (c2): the t-th element of the sorted multiset, t = floor(u n / 2^32)
+        const uint32_t t = __umulhi(u, __ldg(e.n_obs + m));
+        X = (staged && m == bm) ? (uint32_t)tab[t] : (uint32_t)__ldg(e.tab + __ldg(e.tab_off + m) + t);
+      }
       uint32_t lin = first ? s_lib[threadIdx.x] : __ldg(app.l_in_base + r);
       const int32_t p = first ? s_pred[threadIdx.x] : __ldg(app.pred + r);
       if (p >= 0) {
@@ -156,14 +161,14 @@ __global__ void k_dense_coeff(const uint32_t* __restrict__ bucket_B, int32_t nb,
 }  // namespace
 
 cudaError_t launch_sample(const DevApp& app, const DevEcdf& e, const int32_t* seq_head, int32_t n_seq,
-                          uint64_t seed, int32_t trial_begin, int32_t n_trials, uint16_t* l_out,
-                          uint16_t* l_in, cudaStream_t s) {
+                          uint64_t seed, int32_t trial_begin, int32_t n_trials, const uint32_t* known,
+                          uint16_t* l_out, uint16_t* l_in, cudaStream_t s) {
   if (n_seq == 0 || n_trials == 0) return cudaSuccess;
   cudaError_t err = cudaFuncSetAttribute(k_sample_lengths, cudaFuncAttributeMaxDynamicSharedMemorySize, e.smem_tab_bytes);
   if (err != cudaSuccess) return err;
   dim3 grid((n_seq + K1_THREADS - 1) / K1_THREADS, (n_trials + K1_TRIALS_PER_BLOCK - 1) / K1_TRIALS_PER_BLOCK);
   k_sample_lengths<<<grid, K1_THREADS, e.smem_tab_bytes, s>>>(app, e, seq_head, n_seq, (uint32_t)seed,
-                                                              (uint32_t)(seed >> 32), trial_begin, n_trials, l_out, l_in);
+                                                              (uint32_t)(seed >> 32), trial_begin, n_trials, known, l_out, l_in);
   return cudaGetLastError();
 }
 

@@ -107,7 +107,7 @@ struct samu_ctx {
   std::vector<uint8_t> cross;
   std::vector<std::vector<int32_t>> waves;
   DevBuf d_l_in_base, d_cap, d_pred, d_node, d_succ, d_cross;
-  DevBuf d_tab, d_tab_off, d_nobs, d_mnode, d_lmax;
+  DevBuf d_tab, d_tab_off, d_nobs, d_mnode, d_lmax, d_known;
   int32_t smem_tab_bytes = 0;
   std::vector<DevBuf> d_waves;
   std::map<std::pair<int, int>, DevBuf> coef;                      // (model, tp slot) -> dense table
@@ -543,13 +543,8 @@ static samu_status replicas(samu_ctx* c, int node, int dp, const uint32_t** off,
 // ---------------------------------------------------------------------------------------------
 // sampling
 // ---------------------------------------------------------------------------------------------
-extern "C" samu_status samu_sample_lengths(samu_ctx* c, uint64_t seed, int32_t trial_begin, int32_t n_trials,
-                                           uint16_t* out_l_out, uint16_t* out_l_in_eff) {
-  GUARD(c);
-  if (!c->app_loaded) FAIL(c, SAMU_E_INVALID, "sample_lengths: no app loaded");
-  if (n_trials < 0 || trial_begin < 0 || (n_trials && (!out_l_out || !out_l_in_eff)))
-    FAIL(c, SAMU_E_INVALID, "sample_lengths: bad arguments");
-  if (n_trials > 65535) FAIL(c, SAMU_E_INVALID, "sample_lengths: at most 65535 trials per call");
+static samu_status sample_or_known(samu_ctx* c, uint64_t seed, int32_t trial_begin, int32_t n_trials,
+                                   const uint32_t* known_dev, uint16_t* out_l_out, uint16_t* out_l_in_eff) {
   DevApp a = dev_app(c);
   DevEcdf e;
   e.tab = c->d_tab.as<uint16_t>();
@@ -559,8 +554,39 @@ extern "C" samu_status samu_sample_lengths(samu_ctx* c, uint64_t seed, int32_t t
   e.l_max_of_node = c->d_lmax.as<uint32_t>();
   e.smem_tab_bytes = c->smem_tab_bytes;
   for (size_t w = 0; w < c->waves.size(); ++w)
-    CK(c, samu_count(c, launch_sample(a, e, c->d_waves[w].as<int32_t>(), (int32_t)c->waves[w].size(), seed, trial_begin, n_trials,
-                        out_l_out, out_l_in_eff, c->stream)));
+    CK(c, samu_count(c, launch_sample(a, e, c->d_waves[w].as<int32_t>(), (int32_t)c->waves[w].size(), seed, trial_begin,
+                                      n_trials, known_dev, out_l_out, out_l_in_eff, c->stream)));
+  return SAMU_OK;
+}
+
+extern "C" samu_status samu_sample_lengths(samu_ctx* c, uint64_t seed, int32_t trial_begin, int32_t n_trials,
+                                           uint16_t* out_l_out, uint16_t* out_l_in_eff) {
+  GUARD(c);
+  if (!c->app_loaded) FAIL(c, SAMU_E_INVALID, "sample_lengths: no app loaded");
+  if (n_trials < 0 || trial_begin < 0 || (n_trials && (!out_l_out || !out_l_in_eff)))
+    FAIL(c, SAMU_E_INVALID, "sample_lengths: bad arguments");
+  if (n_trials > 65535) FAIL(c, SAMU_E_INVALID, "sample_lengths: at most 65535 trials per call");
+  return sample_or_known(c, seed, trial_begin, n_trials, nullptr, out_l_out, out_l_in_eff);
+}
+
+// host l_true [n_req] -> device scratch (kept in the context until the next call)
+static samu_status upload_known(samu_ctx* c, const uint32_t* l_true, const uint32_t** dev) {
+  CK(c, c->d_known.ensure(sizeof(uint32_t) * std::max<size_t>(c->n_req, 1)));
+  if (c->n_req)
+    CK(c, cudaMemcpyAsync(c->d_known.p, l_true, sizeof(uint32_t) * c->n_req, cudaMemcpyHostToDevice, c->stream));
+  *dev = c->d_known.as<uint32_t>();
+  return SAMU_OK;
+}
+
+extern "C" samu_status samu_known_lengths(samu_ctx* c, const uint32_t* l_true, uint16_t* out_l_out,
+                                          uint16_t* out_l_in_eff) {
+  GUARD(c);
+  if (!c->app_loaded) FAIL(c, SAMU_E_INVALID, "known_lengths: no app loaded");
+  if (c->n_req && (!l_true || !out_l_out || !out_l_in_eff)) FAIL(c, SAMU_E_INVALID, "known_lengths: bad arguments");
+  const uint32_t* d = nullptr;
+  RET(upload_known(c, l_true, &d));
+  RET(sample_or_known(c, 0, 0, 1, d, out_l_out, out_l_in_eff));
+  CK(c, cudaStreamSynchronize(c->stream));   // the host array may be released on return
   return SAMU_OK;
 }
 
@@ -870,6 +896,21 @@ struct Greedy {
   std::vector<int> pending_tau;            // f* full slot whose records give tau, or -1
   int64_t evals = 0;
   std::vector<bool> is_input;
+  bool preempt = true;                  // false: no-preemption ablation (reading c29)
+  const uint32_t* known = nullptr;      // device known output lengths (reading c30)
+  std::vector<int> undone_now;          // per node: unfinished in some trial (current stage)
+
+  // No-preemption: every model of the previous stage that is unfinished keeps its entry
+  std::vector<Ent> pinned() const {
+    std::vector<Ent> E;
+    if (preempt) return E;
+    for (const Ent& e : prev) if (undone_now[e.node]) E.push_back(e);
+    return E;
+  }
+  static bool is_pinned(const std::vector<Ent>& pin, int v) {
+    for (const Ent& e : pin) if (e.node == v) return true;
+    return false;
+  }
 
   bool resumes(const Ent& e) const {
     for (const Ent& x : prev) if (x == e) return true;
@@ -985,7 +1026,7 @@ struct Greedy {
   // cut simulations of the other entries at t_E^(k), then T_E and the choice.  mode 0: Alg. 1's
   // argmax dT/dN (ties: dN, node, tp, dp); mode 1: argmax T_E (ties: first candidate).
   samu_status score_batch(const std::vector<Cand>& cands, double TE_star, int g_star, int mode, int32_t* best,
-                          double* maxdT, std::vector<StageOut>& so) {
+                          double* maxdT, std::vector<StageOut>& so, bool count = true) {
     cudaStream_t s = c->stream;
     const int nc = (int)cands.size();
     std::vector<StageCand> sc(nc);
@@ -1022,7 +1063,7 @@ struct Greedy {
     CK(c, samu_count(c, launch_stage_score(cache.as<samu_trial_rec>(), T, d_sc.as<StageCand>(), nc, d_out.as<StageOut>(),
                                            TE_star, g_star, mode, d_best.as<int32_t>(),
                                            reinterpret_cast<double*>(d_best.as<char>() + 8), s)));
-    evals += nc;
+    if (count) evals += nc;
     CK(c, cudaMemcpyAsync(best, d_best.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     CK(c, cudaMemcpyAsync(maxdT, d_best.as<char>() + 8, sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(c, cudaMemcpyAsync(so.data(), d_out.p, sizeof(StageOut) * nc, cudaMemcpyDeviceToHost, s));
@@ -1036,7 +1077,17 @@ struct Greedy {
   samu_status choose_greedy(const std::vector<int>& unfinished, const std::vector<int>& undone, std::vector<Ent>& Es,
                             StageOut& chosen) {
     const int N = (int)c->eng.n_gpus;
+    const std::vector<Ent> pin = pinned();
     double TE_star = 0.0;
+    if (!pin.empty()) {   // E* starts from the running models
+      int32_t b = -1;
+      double mx = 0.0;
+      std::vector<StageOut> so;
+      RET(score_batch({Cand{pin, pin[0]}}, 0.0, 0, 1, &b, &mx, so));
+      Es = pin;
+      TE_star = so[0].TE;
+      chosen = so[0];
+    }
     for (;;) {
       std::vector<int> ready;
       for (int v : unfinished) {
@@ -1050,6 +1101,7 @@ struct Greedy {
       for (const Ent& e : Es) g_star += e.dp * e.tp;
       for (int v : ready)
         for (auto& pl : plans[v]) {
+          if (is_pinned(pin, v)) break;
           Ent P{v, pl.first, pl.second};
           int prime = -1;
           for (size_t i = 0; i < Es.size(); ++i) if (Es[i].node == v) prime = (int)i;
@@ -1112,16 +1164,21 @@ struct Greedy {
   // no combination exists
   samu_status choose_min(const std::vector<int>& unfinished, const std::vector<int>& undone, std::vector<Ent>& Es,
                          StageOut& chosen) {
-    const int N = (int)c->eng.n_gpus;
+    const std::vector<Ent> pin = pinned();   // no-preemption: running models keep their entries
+    int N = (int)c->eng.n_gpus;
+    for (const Ent& e : pin) N -= e.dp * e.tp;
     std::vector<int> sel;
     for (int v : unfinished) {
       if ((int)sel.size() >= N) break;
+      if (is_pinned(pin, v)) continue;
       const int in = c->node_input[v];
       bool ok = in < 0 || !undone[in];
       for (int x : sel) if (x == in) ok = true;
+      if (is_pinned(pin, in)) ok = true;
       if (ok) sel.push_back(v);
     }
-    for (int k = (int)sel.size(); k >= 1 && Es.empty(); --k) {
+    bool found = false;
+    for (int k = (int)sel.size(); k >= 1 && !found; --k) {
       const int base = N / k, extra = N % k;
       std::vector<Cand> cands;
       std::vector<int> pick(extra);
@@ -1141,11 +1198,12 @@ struct Greedy {
           std::vector<int> idx(k, 0);
           for (;;) {
             if (cands.size() >= 10000) break;
-            std::vector<Ent> E;
+            std::vector<Ent> E = pin;
             for (int i = 0; i < k; ++i) {
               const auto& pl = plans[sel[i]][opts[i][idx[i]]];
               E.push_back({sel[i], pl.first, pl.second});
             }
+            std::sort(E.begin(), E.end(), [](const Ent& a, const Ent& b) { return a.node < b.node; });
             cands.push_back({E, E[0]});
             int q = k - 1;   // odometer, last model fastest
             while (q >= 0 && ++idx[q] == (int)opts[q].size()) { idx[q] = 0; --q; }
@@ -1167,6 +1225,15 @@ struct Greedy {
       RET(score_batch(cands, 0.0, 0, 1, &best, &mx, so));
       Es = cands[best].E;
       chosen = so[best];
+      found = true;
+    }
+    if (!found && !pin.empty()) {   // nothing to add: the stage is the running models
+      int32_t b = -1;
+      double mx = 0.0;
+      std::vector<StageOut> so;
+      RET(score_batch({Cand{pin, pin[0]}}, 0.0, 0, 1, &b, &mx, so, false));
+      Es = pin;
+      chosen = so[0];
     }
     return SAMU_OK;
   }
@@ -1192,7 +1259,7 @@ struct Greedy {
       std::vector<double> inf(tn, std::numeric_limits<double>::infinity());
       CK(c, cudaMemcpyAsync(fin_t.p, inf.data(), sizeof(double) * tn, cudaMemcpyHostToDevice, s));
     }
-    if (Tl) RET(samu_sample_lengths(c, seed, tb, Tl, lo.as<uint16_t>(), li.as<uint16_t>()));
+    if (Tl) RET(sample_or_known(c, seed, tb, Tl, known, lo.as<uint16_t>(), li.as<uint16_t>()));
     S = StatePtrs{st.as<uint32_t>(), g.as<uint16_t>(), fin_t.as<double>(), over.as<double>()};
     CK(c, d_best.ensure(sizeof(int32_t) + sizeof(double)));
     CK(c, d_any.ensure(sizeof(int32_t) * (size_t)c->n_nodes * std::max(Tl, 1) + 2 * sizeof(int32_t) * SAMU_MAX_NODES));
@@ -1206,6 +1273,7 @@ struct Greedy {
       std::vector<int> unfinished;
       for (int v = 0; v < c->n_nodes; ++v) if (undone[v]) unfinished.push_back(v);
       if (unfinished.empty()) break;
+      undone_now = undone;
       if (plan->n_stages >= 64) FAIL(c, SAMU_E_STATE, "plan: too many stages");
       full_slot.clear(); cut_slot.clear(); fin_buf.clear(); n_slots = 0;
       std::vector<Ent> Es;
@@ -1286,32 +1354,47 @@ struct Greedy {
 
 }  // namespace
 
-static samu_status plan_with(samu_ctx* c, uint64_t seed, int32_t n_trials, int algo, samu_plan** out) {
+static samu_status plan_with(samu_ctx* c, uint64_t seed, int32_t n_trials, const samu_plan_opts* o, samu_plan** out) {
   GUARD(c);
-  if (!out || n_trials < 1) FAIL(c, SAMU_E_INVALID, "plan: bad arguments");
+  if (!out || n_trials < 1 || !o || o->algo < SAMU_ALGO_GREEDY || o->algo > SAMU_ALGO_MIN)
+    FAIL(c, SAMU_E_INVALID, "plan: bad arguments");
   if (!c->app_loaded) FAIL(c, SAMU_E_INVALID, "plan: no app loaded");
+  if (o->known_l_out && n_trials != 1) FAIL(c, SAMU_E_INVALID, "plan: known output lengths need n_trials == 1");
   *out = nullptr;
   samu_plan* p = new samu_plan();
   Greedy G;
   G.c = c;
+  G.preempt = o->allow_preemption != 0;
+  if (o->known_l_out) {
+    samu_status rk = upload_known(c, o->known_l_out, &G.known);
+    if (rk != SAMU_OK) { delete p; return rk; }
+  }
   const int64_t sims0 = c->n_sims;
-  samu_status rc = G.run(seed, n_trials, algo, p);
+  samu_status rc = G.run(seed, n_trials, o->algo, p);
   if (rc != SAMU_OK) { delete p; return rc; }
   p->n_sims = c->n_sims - sims0;
   *out = p;
   return SAMU_OK;
 }
 
+extern "C" samu_status samu_plan_run(samu_ctx* c, uint64_t seed, int32_t n_trials, const samu_plan_opts* opts,
+                                 samu_plan** out) {
+  return plan_with(c, seed, n_trials, opts, out);
+}
+
 extern "C" samu_status samu_plan_greedy(samu_ctx* c, uint64_t seed, int32_t n_trials, samu_plan** out) {
-  return plan_with(c, seed, n_trials, 0, out);
+  const samu_plan_opts o{SAMU_ALGO_GREEDY, 1, nullptr};
+  return plan_with(c, seed, n_trials, &o, out);
 }
 
 extern "C" samu_status samu_plan_max_heuristic(samu_ctx* c, uint64_t seed, int32_t n_trials, samu_plan** out) {
-  return plan_with(c, seed, n_trials, 1, out);
+  const samu_plan_opts o{SAMU_ALGO_MAX, 1, nullptr};
+  return plan_with(c, seed, n_trials, &o, out);
 }
 
 extern "C" samu_status samu_plan_min_heuristic(samu_ctx* c, uint64_t seed, int32_t n_trials, samu_plan** out) {
-  return plan_with(c, seed, n_trials, 2, out);
+  const samu_plan_opts o{SAMU_ALGO_MIN, 1, nullptr};
+  return plan_with(c, seed, n_trials, &o, out);
 }
 
 extern "C" void samu_plan_free(samu_plan* p) { delete p; }

@@ -270,6 +270,43 @@ def test_planners_fig1_and_even_split_fixtures(algo):
         assert pg == po
 
 
+# §5.5 ablations: no-preemption variants and known output lengths
+@pytest.mark.parametrize("algo", ["greedy", "min"])
+@pytest.mark.parametrize("name,kw,T", [
+    ("c2", dict(n_prompts=120), 3),
+    ("c4", dict(n_docs=60), 2),
+    ("c5", dict(n_prompts=40, n_docs=30), 2),
+])
+def test_no_preemption_plan_bit_exact(name, kw, T, algo):
+    w = W.make_workload(name, n_trials=T, **kw)
+    po = O.Problem(w).plan_greedy(SEED, T, algo, preemption=False)
+    pg = gpu(w).samu_plan_greedy(SEED, T, algo, preemption=False)
+    pg.pop("n_sims")
+    assert pg == po
+
+
+def test_known_lengths_bit_exact():
+    w = W.make_workload("c5", n_prompts=200, n_docs=60, n_trials=1)
+    rng = np.random.default_rng(7)
+    l_true = rng.integers(0, 5000, w.n_req).astype(np.uint32)
+    l_true[::17] = 0
+    S = gpu(w)
+    glo, gli = S.samu_known_lengths(l_true)
+    olo, oli = O.Problem(w).known_lengths(l_true)
+    assert (u16(glo) == olo).all() and (u16(gli) == oli).all()
+
+
+@pytest.mark.parametrize("algo", ["greedy", "max", "min"])
+def test_known_lengths_plan_bit_exact(algo):
+    w = W.make_workload("c5", n_prompts=40, n_docs=30, n_trials=1)
+    l_true = np.random.default_rng(11).integers(1, 700, w.n_req).astype(np.uint32)
+    for pre in (True, False):
+        po = O.Problem(w).plan_greedy(SEED, 1, algo, preemption=pre, known_l_out=l_true)
+        pg = gpu(w).samu_plan_greedy(SEED, 1, algo, preemption=pre, known_l_out=l_true)
+        pg.pop("n_sims")
+        assert pg == po
+
+
 # ------------------------------------------------------------------------------------------
 # full size, bench launch configuration: sampled (candidate, trial) pairs vs the oracle
 # ------------------------------------------------------------------------------------------

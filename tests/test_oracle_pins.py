@@ -554,3 +554,69 @@ def test_min_heuristic_structure():
             gv = [d * t for (_, d, t) in s["entries"]]
             assert max(gv) - min(gv) <= 1
             assert sum(gv) <= N
+
+
+# ------------------------------------------------------------------------------------------
+# §5.5 ablations: no-preemption and known output lengths
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("algo", ["greedy", "min"])
+def test_no_preemption_keeps_plans_until_finished(algo):
+    # "the execution plan of a model would not be changed once chosen and a running model
+    # would not be stopped once started": an entry either continues unchanged in the next stage
+    # or never appears again (it finished)
+    for w, T in ((F.fig1(), 1), (F.even_split_4x8(), 1), (W.make_workload("c5", n_prompts=40, n_docs=30, n_trials=2), 2)):
+        plan = O.Problem(w).plan_greedy(SEED, T, algo, preemption=False)
+        st = plan["stages"]
+        for k in range(len(st) - 1):
+            later = {e[0] for s in st[k + 1:] for e in s["entries"]}
+            for e in st[k]["entries"]:
+                assert e in st[k + 1]["entries"] or e[0] not in later
+        assert {e[0] for s in st for e in s["entries"]} == set(range(w.n_nodes))
+
+
+def test_max_heuristic_has_no_no_preemption_variant():
+    # "for Max-heuristic, there is no no-preemption version" -- it never preempts
+    w = W.make_workload("c2", n_prompts=60, n_trials=2)
+    P = O.Problem(w)
+    assert P.plan_greedy(SEED, 2, "max") == P.plan_greedy(SEED, 2, "max", preemption=False)
+
+
+@pytest.mark.parametrize("algo", ["greedy", "min"])
+def test_preemption_helps_on_zero_load_fixtures(algo):
+    # P:1099-1104 direction: with preemption, GPUs freed by a finished model go to the others.
+    # Zero load cost isolates that effect.  Fig. 1 fixture totals by hand (1 s per request):
+    #   greedy, no preemption: {0:dp2, 1, 2} 3 s | {0:dp2, 3:dp2} 1 s | {3:dp2, 4:dp2} 1 s |
+    #     {4:dp2, 5:dp2} 1 s | {5:dp2} 1 s = 7 s
+    #   min, no preemption: {0, 1, 2, 3} 3 s | {0, 4:dp2, 5} 2 s | {0, 5} 1 s | {0} 2 s = 8 s
+    P = O.Problem(F.fig1())
+    assert P.plan_greedy(SEED, 1, algo)["total"] == 6.0
+    assert P.plan_greedy(SEED, 1, algo, preemption=False)["total"] == {"greedy": 7.0, "min": 8.0}[algo]
+    # P:743 fixture (8 GPUs, 4 models): direction only
+    P = O.Problem(F.even_split_4x8())
+    assert P.plan_greedy(SEED, 1, algo)["total"] < P.plan_greedy(SEED, 1, algo, preemption=False)["total"]
+
+
+def test_known_lengths_follow_the_sampler_arithmetic():
+    # the true lengths replace the sampler's draw; caps and the chained
+    # prompt are applied the same way.  l_true = the sampled trial reproduces it.
+    w = W.make_workload("c4", n_docs=30, n_trials=1)
+    P = O.Problem(w)
+    lo, li = P.sample(SEED, 3, 1)
+    klo, kli = P.known_lengths(lo[0])
+    assert (klo == lo).all() and (kli == li).all()
+    # lengths above every cap clamp to min(cap, l_max - l_in)
+    big = np.full(w.n_req, 60000, np.uint32)
+    klo, kli = P.known_lengths(big)
+    lmax = np.array([W.arch_spec(w.models[m])["l_max"] if isinstance(w.models[m], str) else w.models[m]["l_max"]
+                     for m in w.node_model])[w.node]
+    assert (klo[0] == np.minimum(w.cap_y, lmax - kli[0])).all()
+
+
+def test_known_lengths_plan_equals_single_trial_plan():
+    # a plan on known lengths equal to trial 0's draw is the 1-trial sampled plan (Alg. 1 with
+    # T = 1 sees only the lengths), for all three planners
+    w = W.make_workload("c2", n_prompts=60, n_trials=1)
+    P = O.Problem(w)
+    lo, _ = P.sample(SEED, 0, 1)
+    for algo in ("greedy", "max", "min"):
+        assert P.plan_greedy(SEED, 1, algo) == P.plan_greedy(12345, 1, algo, known_l_out=lo[0])
