@@ -251,6 +251,38 @@ typedef struct samu_plan_opts {
 samu_status samu_plan_run(samu_ctx* ctx, uint64_t seed, int32_t n_trials, const samu_plan_opts* opts, samu_plan** out);
 void samu_plan_free(samu_plan* plan);
 
+/* Runtime replay with the dynamic scheduler (reading c33): executes `plan` against
+ * true output lengths -- known_l_out host [n_req], or NULL = trial 0 of the sampler with `seed`
+ * (a different seed than the plan's stands in for the real run) -- one trial on the device.
+ * Each actual stage is the set of running (model, plan) pairs and ends at the first actual model
+ * finish; then: an unfinished running pair keeps running if the current planned stage is its
+ * model's last, or if it is in the next planned stage; next-stage pairs are placed first; other
+ * running pairs keep running only if the whole next stage is placed and their GPUs are free,
+ * else they are stopped (state carried).  GPU placement is trivial on NVSwitch (continuing pairs
+ * keep their GPUs, new pairs take the lowest free ids).  `out` is caller-owned. */
+typedef struct samu_replay_stage {
+  int32_t n_entries;
+  int32_t node[16], dp[16], tp[16];
+  uint32_t gpu_mask[16];        /* GPU ids of each pair */
+  int32_t resumed[16];          /* 1 = continued from the previous actual stage (no reload) */
+  int32_t planned_stage;        /* planned stage being executed */
+  int32_t first_finisher;       /* node whose finish ended this actual stage */
+  int32_t idle_gpus;            /* GPUs with no pair during this actual stage */
+  double t_start, duration;     /* seconds, replay clock */
+} samu_replay_stage;
+
+typedef struct samu_replay {
+  int32_t n_stages;
+  samu_replay_stage stages[64];
+  double total;                 /* replayed running time */
+  double planned_total;         /* the plan's estimate */
+  double idle_gpu_seconds;      /* sum of idle_gpus x duration */
+  int32_t n_kept_last, n_kept_room, n_stopped;
+} samu_replay;
+
+samu_status samu_replay_plan(samu_ctx* ctx, const samu_plan* plan, uint64_t seed, const uint32_t* known_l_out,
+                             samu_replay* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -78,6 +78,19 @@ class or_plan(C.Structure):
                 ("n_cand_evals", C.c_int64)]
 
 
+class or_replay_stage(C.Structure):
+    _fields_ = [("n_entries", C.c_int32), ("node", C.c_int32 * 16), ("dp", C.c_int32 * 16), ("tp", C.c_int32 * 16),
+                ("gpu_mask", C.c_uint32 * 16), ("resumed", C.c_int32 * 16), ("planned_stage", C.c_int32),
+                ("first_finisher", C.c_int32), ("idle_gpus", C.c_int32), ("t_start", C.c_double),
+                ("duration", C.c_double)]
+
+
+class or_replay(C.Structure):
+    _fields_ = [("n_stages", C.c_int32), ("stages", or_replay_stage * 64), ("total", C.c_double),
+                ("planned_total", C.c_double), ("idle_gpu_seconds", C.c_double), ("n_kept_last", C.c_int32),
+                ("n_kept_room", C.c_int32), ("n_stopped", C.c_int32)]
+
+
 _lib = None
 
 
@@ -111,6 +124,7 @@ def lib():
         L.or_plan_max_heuristic.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(or_plan)]
         L.or_plan_min_heuristic.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(or_plan)]
         L.or_known_lengths.argtypes = [P, P, P, P]
+        L.or_replay_plan.argtypes = [P, C.POINTER(or_plan), C.c_uint64, P, C.POINTER(or_replay)]
         L.or_plan_run.argtypes = [P, C.c_uint64, C.c_int32, C.c_int32, C.c_int32, P, C.POINTER(or_plan)]
         _lib = L
     return _lib
@@ -260,6 +274,33 @@ class Problem:
         rec = np.zeros((len(cands), T), REC_DTYPE)
         _check(lib().or_simulate_many(self.h, len(cands), cs, T, _ptr(l_out), _ptr(l_in), n_threads, _ptr(rec)))
         return rec
+
+    def replay(self, plan, seed, known_l_out=None):
+        """Run `plan` (a dict from plan_greedy) against true lengths with the dynamic scheduler
+        (P:620-627): known_l_out [n_req], or trial 0 of the sampler with `seed`."""
+        P = or_plan()
+        P.n_stages = len(plan["stages"])
+        for i, s in enumerate(plan["stages"]):
+            S = P.stages[i]
+            S.n_entries = len(s["entries"])
+            for j, (v, d, t) in enumerate(s["entries"]):
+                S.node[j], S.dp[j], S.tp[j] = v, d, t
+            S.fstar, S.mean_tE, S.T_E = s["fstar"], s["mean_tE"], s["T_E"]
+        P.total = plan["total"]
+        lt = None if known_l_out is None else np.ascontiguousarray(known_l_out, np.uint32)
+        out = or_replay()
+        _check(lib().or_replay_plan(self.h, C.byref(P), seed, _ptr(lt), C.byref(out)))
+        stages = []
+        for i in range(out.n_stages):
+            s = out.stages[i]
+            n = s.n_entries
+            stages.append(dict(entries=[(s.node[j], s.dp[j], s.tp[j]) for j in range(n)],
+                               gpu_mask=list(s.gpu_mask[:n]), resumed=list(s.resumed[:n]),
+                               planned_stage=s.planned_stage, first_finisher=s.first_finisher,
+                               idle_gpus=s.idle_gpus, t_start=s.t_start, duration=s.duration))
+        return dict(stages=stages, total=out.total, planned_total=out.planned_total,
+                    idle_gpu_seconds=out.idle_gpu_seconds, n_kept_last=out.n_kept_last,
+                    n_kept_room=out.n_kept_room, n_stopped=out.n_stopped)
 
     def plan_greedy(self, seed, n_trials, algo="greedy", preemption=True, known_l_out=None):
         """algo greedy (Alg. 1) / max / min; preemption=False and known_l_out are the

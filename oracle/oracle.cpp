@@ -811,8 +811,8 @@ struct Greedy {
   }
 
   // commit a chosen stage (Alg. 1 lines 24-25): f* to completion, the others cut at t_E^(k)
-  int commit(const std::vector<Entry>& Es, or_plan* out) {
-    Score sc = score(Es);
+  int commit_stage(const std::vector<Entry>& Es, Score& sc) {
+    sc = score(Es);
     for (size_t i = 0; i < Es.size(); ++i) {   // topological order = ascending node id
       const Entry& e = Es[i];
       const double* sf = src_fin_of(e, Es);
@@ -825,6 +825,15 @@ struct Greedy {
     for (int k = 0; k < T; ++k)   // carried finish times re-based to the next stage's clock
       for (size_t r = 0; r < n; ++r)
         if (st_status(st[k * n + r]) == OR_ST_DONE) fin_t[k * n + r] = fin_t[k * n + r] - sc.tE[k];
+    prev = Es;
+    full_cache.clear();
+    cut_cache.clear();
+    return OR_OK;
+  }
+  int commit(const std::vector<Entry>& Es, or_plan* out) {
+    Score sc;
+    int rc = commit_stage(Es, sc);
+    if (rc) return rc;
     or_stage& S = out->stages[out->n_stages++];
     S.n_entries = (int)Es.size();
     for (size_t i = 0; i < Es.size(); ++i) { S.node[i] = Es[i].node; S.dp[i] = Es[i].dp; S.tp[i] = Es[i].tp; }
@@ -832,7 +841,6 @@ struct Greedy {
     S.mean_tE = sc.mean_tE;
     S.T_E = sc.TE;
     out->total += sc.mean_tE;
-    prev = Es;
     return OR_OK;
   }
 
@@ -1064,4 +1072,217 @@ extern "C" int32_t or_plan_run(const or_problem* p, uint64_t seed, int32_t n_tri
                            const uint32_t* known_l_out, or_plan* out) {
   if (algo < 0 || algo > 2) { set_err("bad algo"); return OR_E_INVALID; }
   return plan_with(p, seed, n_trials, algo, out, allow_preemption, known_l_out);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Runtime replay with the dynamic scheduler (reading c33).  The plan is executed
+// against "true" lengths (known, or a differently seeded draw): the actual stage is the set of
+// running (model, plan) pairs; it lasts until the first model actually finishes (same f* / cut
+// commit as the planner, one trial).  At that event stage `cur` ends and the next planned stage
+// nxt is scheduled:
+//   - an unfinished running (M, P) keeps running if E_cur is the last stage M is planned in, or
+//     if (M, P) is in E_nxt;
+//   - if M is in E_nxt with another plan, (M, P) gives way (M reloads with its E_nxt plan);
+//   - E_nxt's pairs are placed first (first fit in entry order); the other running pairs then
+//     keep running, in node order, only if every E_nxt pair was placed and GPUs remain;
+//     otherwise they are stopped (state carried, reloaded when next scheduled);
+//   - E_nxt's pairs that do not fit wait (no stage after nxt is considered until they are placed
+//     or their models finish), and are placed at later finish events as GPUs free up;
+//   - a pair whose input model is unfinished and not running is not started (it waits / stops).
+// Placement on NVSwitch is trivial: a continuing pair keeps its GPUs, a new pair takes the
+// lowest free GPU ids; reload costs follow reading c18 (resume iff the same pair ran in the
+// previous actual stage).
+// ---------------------------------------------------------------------------------------------
+struct Replay : Greedy {
+  const or_plan* plan = nullptr;
+  std::vector<int> last_stage;      // last planned stage index containing each node
+  std::vector<Entry> R, Q;
+  std::vector<uint32_t> mask;       // GPU mask of each pair in R
+  uint32_t used = 0;
+  uint32_t soft = 0;                // GPUs of running pairs that may keep running: taken last
+
+  static bool has(const std::vector<Entry>& E, const Entry& e) {
+    for (const Entry& x : E) if (x == e) return true;
+    return false;
+  }
+  static bool has_node(const std::vector<Entry>& E, int v) {
+    for (const Entry& x : E) if (x.node == v) return true;
+    return false;
+  }
+  bool place(const Entry& e) {      // lowest free GPU ids, sparing `soft` ones while possible
+    const int N = (int)p->eng.n_gpus, need = e.dp * e.tp;
+    int freeg = 0;
+    for (int i = 0; i < N; ++i) if (!(used >> i & 1u)) ++freeg;
+    if (freeg < need) return false;
+    uint32_t m = 0;
+    int k = 0;
+    for (int i = 0; i < N && k < need; ++i)
+      if (!(used >> i & 1u) && !(soft >> i & 1u)) { m |= 1u << i; ++k; }
+    for (int i = 0; i < N && k < need; ++i)
+      if (!(used >> i & 1u) && (soft >> i & 1u)) { m |= 1u << i; ++k; }
+    used |= m;
+    R.push_back(e);
+    mask.push_back(m);
+    return true;
+  }
+  void place_from_Q() {
+    std::vector<Entry> rest;
+    for (const Entry& e : Q) if (done_all(e.node) || !place(e)) { if (!done_all(e.node)) rest.push_back(e); }
+    Q = rest;
+  }
+  std::vector<Entry> stage_entries(int k) const {
+    std::vector<Entry> E;
+    const or_stage& S = plan->stages[k];
+    for (int i = 0; i < S.n_entries; ++i) E.push_back({S.node[i], S.dp[i], S.tp[i]});
+    return E;
+  }
+  // drop pairs whose input model is unfinished and not running (fixpoint); returns dropped ones
+  std::vector<Entry> drop_blocked() {
+    std::vector<Entry> dropped;
+    for (bool changed = true; changed;) {
+      changed = false;
+      for (size_t i = 0; i < R.size(); ++i) {
+        const int src = p->node_input[R[i].node];
+        if (src >= 0 && !done_all(src) && !has_node(R, src)) {
+          dropped.push_back(R[i]);
+          used &= ~mask[i];
+          R.erase(R.begin() + i);
+          mask.erase(mask.begin() + i);
+          changed = true;
+          break;
+        }
+      }
+    }
+    return dropped;
+  }
+
+  int run_replay(uint64_t seed, or_replay* out) {
+    init(seed);
+    std::memset(out, 0, sizeof(*out));
+    const int N = (int)p->eng.n_gpus;
+    const int S_n = plan->n_stages;
+    if (S_n < 1) { set_err("replay: empty plan"); return OR_E_INVALID; }
+    last_stage.assign(nn, -1);
+    for (int k = 0; k < S_n; ++k)
+      for (const Entry& e : stage_entries(k)) last_stage[e.node] = k;
+    for (size_t v = 0; v < nn; ++v)
+      if (last_stage[v] < 0 && !done_all((int)v)) { set_err("replay: plan misses a model"); return OR_E_INVALID; }
+    int cur = 0;
+    Q = stage_entries(0);
+    place_from_Q();
+    for (const Entry& e : drop_blocked()) Q.insert(Q.begin(), e);
+    double clock = 0.0;
+    for (;;) {
+      bool any = false;
+      for (size_t v = 0; v < nn; ++v) if (!done_all((int)v)) any = true;
+      if (!any) break;
+      if (R.empty()) { set_err("replay: nothing can run"); return OR_E_STATE; }
+      if (out->n_stages >= 64) { set_err("replay: too many stages"); return OR_E_STATE; }
+      // the actual stage: running pairs in node order
+      std::vector<size_t> ord(R.size());
+      for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
+      std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return R[a].node < R[b].node; });
+      std::vector<Entry> Es;
+      std::vector<uint32_t> Ms;
+      for (size_t i : ord) { Es.push_back(R[i]); Ms.push_back(mask[i]); }
+      or_replay_stage& RS = out->stages[out->n_stages++];
+      RS.n_entries = (int)Es.size();
+      int g_used = 0;
+      for (size_t i = 0; i < Es.size(); ++i) {
+        RS.node[i] = Es[i].node; RS.dp[i] = Es[i].dp; RS.tp[i] = Es[i].tp;
+        RS.gpu_mask[i] = Ms[i];
+        RS.resumed[i] = resumes(Es[i]) ? 1 : 0;
+        g_used += Es[i].dp * Es[i].tp;
+      }
+      RS.planned_stage = cur;
+      Score sc;
+      {
+        // the first actual finisher must really finish (all its requests done)
+        Score probe = score(Es);
+        const Full& ff = full(Es[probe.fstar], Es);
+        if (!(ff.rec[0].flags & 1u)) { set_err("replay: first finisher is blocked"); return OR_E_STATE; }
+      }
+      int rc = commit_stage(Es, sc);
+      if (rc) return rc;
+      RS.first_finisher = Es[sc.fstar].node;
+      RS.t_start = clock;
+      RS.duration = sc.tE[0];
+      RS.idle_gpus = N - g_used;
+      clock += sc.tE[0];
+      out->idle_gpu_seconds += (double)(N - g_used) * sc.tE[0];
+      // transition (dynamic scheduler)
+      std::vector<Entry> R_unf;
+      std::vector<uint32_t> M_unf;
+      for (size_t i = 0; i < R.size(); ++i)
+        if (!done_all(R[i].node)) { R_unf.push_back(R[i]); M_unf.push_back(mask[i]); }
+      R.clear(); mask.clear(); used = 0;
+      auto keep = [&](size_t i) { R.push_back(R_unf[i]); mask.push_back(M_unf[i]); used |= M_unf[i]; };
+      if (!Q.empty()) {          // stage cur is still being scheduled
+        for (size_t i = 0; i < R_unf.size(); ++i) keep(i);
+        place_from_Q();
+      } else {
+        int nxt = cur + 1;
+        while (nxt < S_n) {
+          bool live = false;
+          for (const Entry& e : stage_entries(nxt)) if (!done_all(e.node)) live = true;
+          if (live) break;
+          ++nxt;
+        }
+        if (nxt >= S_n) {
+          for (size_t i = 0; i < R_unf.size(); ++i) keep(i);
+        } else {
+          const std::vector<Entry> En = stage_entries(nxt);
+          std::vector<size_t> maybe;
+          std::vector<size_t> ordu(R_unf.size());
+          for (size_t i = 0; i < ordu.size(); ++i) ordu[i] = i;
+          std::sort(ordu.begin(), ordu.end(), [&](size_t a, size_t b) { return R_unf[a].node < R_unf[b].node; });
+          for (size_t i : ordu) {
+            const Entry& e = R_unf[i];
+            if (last_stage[e.node] <= cur) { keep(i); out->n_kept_last++; }
+            else if (has(En, e)) keep(i);
+            else if (has_node(En, e.node)) { /* gives way to its E_nxt plan */ }
+            else maybe.push_back(i);
+          }
+          Q.clear();
+          for (const Entry& e : En) if (!done_all(e.node) && !has(R, e)) Q.push_back(e);
+          soft = 0;
+          for (size_t i : maybe) soft |= M_unf[i];
+          place_from_Q();
+          soft = 0;
+          for (size_t i : maybe) {
+            // keeps running (on its own GPUs: moving would be a reload) only if the whole of
+            // E_nxt is placed and its GPUs are still free
+            if (Q.empty() && !(used & M_unf[i])) { keep(i); out->n_kept_room++; }
+            else out->n_stopped++;
+          }
+          cur = nxt;
+        }
+      }
+      for (const Entry& e : drop_blocked()) {
+        if (last_stage[e.node] >= cur && has(stage_entries(cur), e)) Q.insert(Q.begin(), e);
+        else out->n_stopped++;
+      }
+    }
+    out->total = clock;
+    out->planned_total = plan->total;
+    return OR_OK;
+  }
+};
+
+extern "C" int32_t or_replay_plan(const or_problem* p, const or_plan* plan, uint64_t seed, const uint32_t* known_l_out,
+                                  or_replay* out) {
+  if (!plan || !out) { set_err("replay: bad arguments"); return OR_E_INVALID; }
+  Replay G;
+  G.p = p;
+  G.T = 1;
+  G.known = known_l_out;
+  G.n = p->req.size();
+  G.nn = p->node_model.size();
+  G.plan = plan;
+  try {
+    return G.run_replay(seed, out);
+  } catch (int rc) {
+    set_err("simulation error in replay");
+    return rc;
+  }
 }

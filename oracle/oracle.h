@@ -142,6 +142,31 @@ int32_t or_known_lengths(const or_problem* p, const uint32_t* l_true, uint16_t* 
 int32_t or_plan_run(const or_problem* p, uint64_t seed, int32_t n_trials, int32_t algo, int32_t allow_preemption,
                 const uint32_t* known_l_out, or_plan* out);
 
+/* runtime replay of a plan against true lengths with the dynamic scheduler */
+typedef struct or_replay_stage {
+  int32_t n_entries;
+  int32_t node[16], dp[16], tp[16];
+  uint32_t gpu_mask[16];       /* GPU ids of each pair (NVSwitch: any set) */
+  int32_t resumed[16];         /* 1 = continued from the previous actual stage (no reload) */
+  int32_t planned_stage;       /* index of the planned stage being executed */
+  int32_t first_finisher;      /* node whose finish ended this actual stage */
+  int32_t idle_gpus;
+  double t_start, duration;
+} or_replay_stage;
+
+typedef struct or_replay {
+  int32_t n_stages;
+  or_replay_stage stages[64];
+  double total;                /* simulated running time with the true lengths */
+  double planned_total;        /* the plan's estimate */
+  double idle_gpu_seconds;     /* sum over actual stages of unassigned GPUs x duration */
+  int32_t n_kept_last, n_kept_room, n_stopped;
+} or_replay;
+
+/* true lengths: known_l_out [n_req], or NULL = trial 0 of the sampler with `seed` */
+int32_t or_replay_plan(const or_problem* p, const or_plan* plan, uint64_t seed, const uint32_t* known_l_out,
+                       or_replay* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,19 @@ REC_DTYPE = np.dtype([("t_end", "<f8"), ("flops_lo", "<u8"), ("flops_hi", "<u8")
 assert REC_DTYPE.itemsize == C.sizeof(samu_trial_rec) == 40
 
 
+class samu_replay_stage(C.Structure):
+    _fields_ = [("n_entries", C.c_int32), ("node", C.c_int32 * 16), ("dp", C.c_int32 * 16), ("tp", C.c_int32 * 16),
+                ("gpu_mask", C.c_uint32 * 16), ("resumed", C.c_int32 * 16), ("planned_stage", C.c_int32),
+                ("first_finisher", C.c_int32), ("idle_gpus", C.c_int32), ("t_start", C.c_double),
+                ("duration", C.c_double)]
+
+
+class samu_replay(C.Structure):
+    _fields_ = [("n_stages", C.c_int32), ("stages", samu_replay_stage * 64), ("total", C.c_double),
+                ("planned_total", C.c_double), ("idle_gpu_seconds", C.c_double), ("n_kept_last", C.c_int32),
+                ("n_kept_room", C.c_int32), ("n_stopped", C.c_int32)]
+
+
 class samu_plan_opts(C.Structure):
     _fields_ = [("algo", C.c_int32), ("allow_preemption", C.c_int32), ("known_l_out", C.c_void_p)]
 
@@ -77,7 +90,7 @@ EXPORTED = ["samu_ctx_create", "samu_ctx_destroy", "samu_local_group_create", "s
             "samu_model_register",
             "samu_ecdf_load", "samu_app_load", "samu_enumerate_plans", "samu_sample_lengths", "samu_simulate_batch",
             "samu_plan_greedy", "samu_plan_max_heuristic", "samu_plan_min_heuristic", "samu_plan_run", "samu_known_lengths",
-            "samu_plan_free"]
+            "samu_replay_plan", "samu_plan_free"]
 
 _lib = None
 
@@ -115,6 +128,7 @@ def lib():
         L.samu_plan_run.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(samu_plan_opts),
                                     C.POINTER(C.POINTER(samu_plan))]
         L.samu_known_lengths.argtypes = [P, P, P, P]
+        L.samu_replay_plan.argtypes = [P, C.POINTER(samu_plan), C.c_uint64, P, C.POINTER(samu_replay)]
         L.samu_plan_free.argtypes = [C.POINTER(samu_plan)]
         L.samu_plan_free.restype = None
         _lib = L
@@ -322,6 +336,33 @@ class Samu:
             return dict(stages=stages, total=P.total, n_cand_evals=P.n_cand_evals, n_sims=P.n_sims)
         finally:
             lib().samu_plan_free(p)
+
+    def samu_replay_plan(self, plan: dict, seed: int, known_l_out=None):
+        """Replay a plan (dict from samu_plan_greedy) against true lengths with the dynamic
+        scheduler: known_l_out [n_req], or trial 0 of the sampler with `seed`."""
+        P = samu_plan()
+        P.n_stages = len(plan["stages"])
+        for i, st in enumerate(plan["stages"]):
+            S = P.stages[i]
+            S.n_entries = len(st["entries"])
+            for j, (v, d, t) in enumerate(st["entries"]):
+                S.node[j], S.dp[j], S.tp[j] = v, d, t
+            S.fstar, S.mean_tE, S.T_E = st["fstar"], st["mean_tE"], st["T_E"]
+        P.total = plan["total"]
+        lt = None if known_l_out is None else np.ascontiguousarray(np.asarray(known_l_out, dtype=np.uint32))
+        out = samu_replay()
+        self._check(lib().samu_replay_plan(self.h, C.byref(P), seed, _np_ptr(lt), C.byref(out)))
+        stages = []
+        for i in range(out.n_stages):
+            st = out.stages[i]
+            k = st.n_entries
+            stages.append(dict(entries=[(st.node[j], st.dp[j], st.tp[j]) for j in range(k)],
+                               gpu_mask=list(st.gpu_mask[:k]), resumed=list(st.resumed[:k]),
+                               planned_stage=st.planned_stage, first_finisher=st.first_finisher,
+                               idle_gpus=st.idle_gpus, t_start=st.t_start, duration=st.duration))
+        return dict(stages=stages, total=out.total, planned_total=out.planned_total,
+                    idle_gpu_seconds=out.idle_gpu_seconds, n_kept_last=out.n_kept_last,
+                    n_kept_room=out.n_kept_room, n_stopped=out.n_stopped)
 
 
 def recs_to_numpy(recs) -> np.ndarray:

@@ -1238,7 +1238,7 @@ struct Greedy {
     return SAMU_OK;
   }
 
-  samu_status run(uint64_t seed, int T_total, int algo, samu_plan* plan) {
+  samu_status setup(uint64_t seed, int T_total) {
     T = T_total;
     n = (size_t)c->n_req;
     trial_share(T, c->world, c->rank, &tb, &Tl);
@@ -1258,6 +1258,7 @@ struct Greedy {
     {
       std::vector<double> inf(tn, std::numeric_limits<double>::infinity());
       CK(c, cudaMemcpyAsync(fin_t.p, inf.data(), sizeof(double) * tn, cudaMemcpyHostToDevice, s));
+      CK(c, cudaStreamSynchronize(s));
     }
     if (Tl) RET(sample_or_known(c, seed, tb, Tl, known, lo.as<uint16_t>(), li.as<uint16_t>()));
     S = StatePtrs{st.as<uint32_t>(), g.as<uint16_t>(), fin_t.as<double>(), over.as<double>()};
@@ -1265,6 +1266,52 @@ struct Greedy {
     CK(c, d_any.ensure(sizeof(int32_t) * (size_t)c->n_nodes * std::max(Tl, 1) + 2 * sizeof(int32_t) * SAMU_MAX_NODES));
     plans.assign(c->n_nodes, {});
     for (int v = 0; v < c->n_nodes; ++v) plans[v] = plans_of(c, c->node_model[v]);
+    return SAMU_OK;
+  }
+
+  // commit a stage (Alg. 1 lines 24-25): f* to completion, the others cut at t_E^(k), state
+  // carried, finish times re-based; `chosen` is the stage's score (f*, mean t_E, T_E)
+  samu_status commit_stage(const std::vector<Ent>& Es, const StageOut& chosen) {
+    cudaStream_t s = c->stream;
+    const int f = chosen.fstar;
+    int fslot = -1;
+    RET(ensure_full(Es[f], Es, &fslot));
+    std::vector<SimJob> jobs;
+    CK(c, local_rec.ensure(sizeof(samu_trial_rec) * Es.size() * std::max(Tl, 1)));
+    for (size_t i = 0; i < Es.size(); ++i) {
+      const Ent& e = Es[i];
+      SimJob J;
+      J.cand = samu_candidate{e.node, e.dp, e.tp, resumes(e) ? 1 : 0, -1, 1};
+      J.phase = 0;
+      const int src = c->node_input[e.node];
+      for (size_t q = 0; q < Es.size(); ++q)
+        if (Es[q].node == src) {
+          int ss;
+          RET(ensure_full(Es[q], Es, &ss));
+          J.src_fin = fin_buf.at(ss).as<double>();
+          J.phase = 1;
+        }
+      J.tau_rec = ((int)i == f) ? nullptr : rec(fslot) + tb;
+      J.out_rec = local_rec.as<samu_trial_rec>() + i * Tl;
+      jobs.push_back(J);
+    }
+    RET(flush());
+    // depth > 1 chains of dependencies commit in topological (node id) order
+    for (size_t i = 0; i < jobs.size(); ++i) {
+      int d = 0, v = Es[i].node;
+      while (c->node_input[v] >= 0) { ++d; v = c->node_input[v]; }
+      jobs[i].phase = d;
+    }
+    RET(run_jobs(c, jobs, lo.as<uint16_t>(), li.as<uint16_t>(), Tl, S));
+    CK(c, samu_count(c, launch_rebase(st.as<uint32_t>(), fin_t.as<double>(), (int64_t)Tl * n, rec(fslot) + tb, (int32_t)n, s)));
+    prev = Es;
+    return SAMU_OK;
+  }
+
+  void new_stage_caches() { full_slot.clear(); cut_slot.clear(); fin_buf.clear(); n_slots = 0; }
+
+  samu_status run(uint64_t seed, int T_total, int algo, samu_plan* plan) {
+    RET(setup(seed, T_total));
     std::memset(plan, 0, sizeof(*plan));
     for (;;) {
       // unfinished nodes (in any trial of any rank)
@@ -1275,7 +1322,7 @@ struct Greedy {
       if (unfinished.empty()) break;
       undone_now = undone;
       if (plan->n_stages >= 64) FAIL(c, SAMU_E_STATE, "plan: too many stages");
-      full_slot.clear(); cut_slot.clear(); fin_buf.clear(); n_slots = 0;
+      new_stage_caches();
       std::vector<Ent> Es;
       StageOut chosen{};
       if (algo == 0) RET(choose_greedy(unfinished, undone, Es, chosen));
@@ -1283,52 +1330,19 @@ struct Greedy {
       else RET(choose_min(unfinished, undone, Es, chosen));
       if (Es.empty()) FAIL(c, SAMU_E_INFEASIBLE, "plan: no ready model fits an empty stage");
       evals += 1;   // the stage is scored once more at commit (oracle parity of the counter)
-      // commit (Alg. 1 lines 24-25): f* to completion, the others cut at t_E^(k), state carried
-      const int f = chosen.fstar;
-      int fslot = -1;
-      RET(ensure_full(Es[f], Es, &fslot));
-      std::vector<SimJob> jobs;
-      CK(c, local_rec.ensure(sizeof(samu_trial_rec) * Es.size() * std::max(Tl, 1)));
-      for (size_t i = 0; i < Es.size(); ++i) {
-        const Ent& e = Es[i];
-        SimJob J;
-        J.cand = samu_candidate{e.node, e.dp, e.tp, resumes(e) ? 1 : 0, -1, 1};
-        J.phase = 0;
-        const int src = c->node_input[e.node];
-        for (size_t q = 0; q < Es.size(); ++q)
-          if (Es[q].node == src) {
-            int ss;
-            RET(ensure_full(Es[q], Es, &ss));
-            J.src_fin = fin_buf.at(ss).as<double>();
-            J.phase = 1;
-          }
-        J.tau_rec = ((int)i == f) ? nullptr : rec(fslot) + tb;
-        J.out_rec = local_rec.as<samu_trial_rec>() + i * Tl;
-        jobs.push_back(J);
-      }
-      RET(flush());
-      // depth > 1 chains of dependencies commit in topological (node id) order
-      for (size_t i = 0; i < jobs.size(); ++i) {
-        int d = 0, v = Es[i].node;
-        while (c->node_input[v] >= 0) { ++d; v = c->node_input[v]; }
-        jobs[i].phase = d;
-      }
-      RET(run_jobs(c, jobs, lo.as<uint16_t>(), li.as<uint16_t>(), Tl, S));
-      CK(c, samu_count(c, launch_rebase(st.as<uint32_t>(), fin_t.as<double>(), (int64_t)Tl * n, rec(fslot) + tb, (int32_t)n, s)));
+      RET(commit_stage(Es, chosen));
       samu_plan_stage& PS = plan->stages[plan->n_stages++];
       PS.n_entries = (int)Es.size();
       for (size_t i = 0; i < Es.size(); ++i) { PS.node[i] = Es[i].node; PS.dp[i] = Es[i].dp; PS.tp[i] = Es[i].tp; }
-      PS.fstar = Es[f].node;
+      PS.fstar = Es[chosen.fstar].node;
       PS.mean_tE = chosen.mean_tE;
       PS.T_E = chosen.TE;
       plan->total += chosen.mean_tE;
-      prev = Es;
     }
     plan->n_cand_evals = evals;
     return SAMU_OK;
   }
 
-  // undone[v] = 1 if node v has an unfinished request in any trial (OR over ranks)
   samu_status node_status(std::vector<int>& undone) {
     cudaStream_t s = c->stream;
     int32_t* any = d_any.as<int32_t>();
@@ -1348,6 +1362,196 @@ struct Greedy {
       CK(c, cudaStreamSynchronize(s));
     }
     for (int v = 0; v < c->n_nodes; ++v) undone[v] = flag[v];
+    return SAMU_OK;
+  }
+};
+
+// Runtime replay with the dynamic scheduler (reading c33): the plan runs against true
+// lengths (known, or another seed's draw, one trial); each actual stage = the running pairs, ended
+// by the first actual finish (device-scored f*, cut commit); then the dynamic scheduler picks the
+// next running set.  NVSwitch placement: continuing pairs keep their GPUs, new pairs take the
+// lowest free ids, sparing the GPUs of pairs that may keep running.
+struct Replay : Greedy {
+  const samu_plan* plan = nullptr;
+  std::vector<int> last_stage, undone;
+  std::vector<Ent> R, Q;
+  std::vector<uint32_t> mask;
+  uint32_t used = 0, soft = 0;
+
+  static bool has(const std::vector<Ent>& E, const Ent& e) {
+    for (const Ent& x : E) if (x == e) return true;
+    return false;
+  }
+  static bool has_node(const std::vector<Ent>& E, int v) {
+    for (const Ent& x : E) if (x.node == v) return true;
+    return false;
+  }
+  bool done(int v) const { return !undone[v]; }
+  bool place(const Ent& e) {
+    const int N = (int)c->eng.n_gpus, need = e.dp * e.tp;
+    const uint32_t all = N >= 32 ? 0xFFFFFFFFu : ((1u << N) - 1u);
+    const uint32_t freem = all & ~used;
+    if (__builtin_popcount(freem) < need) return false;
+    uint32_t m = 0;
+    int k = 0;
+    for (int pass = 0; pass < 2; ++pass)
+      for (int i = 0; i < N && k < need; ++i) {
+        const bool sp = (soft >> i) & 1u;
+        if (((freem >> i) & 1u) && (pass == 0 ? !sp : sp)) { m |= 1u << i; ++k; }
+      }
+    used |= m;
+    R.push_back(e);
+    mask.push_back(m);
+    return true;
+  }
+  void place_from_Q() {
+    std::vector<Ent> rest;
+    for (const Ent& e : Q)
+      if (!done(e.node) && !place(e)) rest.push_back(e);
+    Q = rest;
+  }
+  std::vector<Ent> stage_entries(int k) const {
+    std::vector<Ent> E;
+    const samu_plan_stage& P = plan->stages[k];
+    for (int i = 0; i < P.n_entries; ++i) E.push_back(Ent{P.node[i], P.dp[i], P.tp[i]});
+    return E;
+  }
+  std::vector<Ent> drop_blocked() {
+    std::vector<Ent> dropped;
+    for (bool changed = true; changed;) {
+      changed = false;
+      for (size_t i = 0; i < R.size(); ++i) {
+        const int src = c->node_input[R[i].node];
+        if (src >= 0 && !done(src) && !has_node(R, src)) {
+          dropped.push_back(R[i]);
+          used &= ~mask[i];
+          R.erase(R.begin() + i);
+          mask.erase(mask.begin() + i);
+          changed = true;
+          break;
+        }
+      }
+    }
+    return dropped;
+  }
+
+  samu_status run_replay(uint64_t seed, samu_replay* out) {
+    RET(setup(seed, 1));
+    std::memset(out, 0, sizeof(*out));
+    const int N = (int)c->eng.n_gpus;
+    const int S_n = plan->n_stages;
+    undone.assign(c->n_nodes, 0);
+    RET(node_status(undone));
+    last_stage.assign(c->n_nodes, -1);
+    for (int k = 0; k < S_n; ++k)
+      for (const Ent& e : stage_entries(k)) {
+        if (e.node < 0 || e.node >= c->n_nodes) FAIL(c, SAMU_E_INVALID, "replay: plan node out of range");
+        last_stage[e.node] = k;
+      }
+    for (int v = 0; v < c->n_nodes; ++v)
+      if (last_stage[v] < 0 && !done(v)) FAIL(c, SAMU_E_INVALID, "replay: plan misses a model");
+    int cur = 0;
+    Q = stage_entries(0);
+    place_from_Q();
+    for (const Ent& e : drop_blocked()) Q.insert(Q.begin(), e);
+    double clock = 0.0;
+    for (;;) {
+      bool any = false;
+      for (int v = 0; v < c->n_nodes; ++v) if (!done(v)) any = true;
+      if (!any) break;
+      if (R.empty()) FAIL(c, SAMU_E_STATE, "replay: nothing can run");
+      if (out->n_stages >= 64) FAIL(c, SAMU_E_STATE, "replay: too many stages");
+      std::vector<size_t> ord(R.size());
+      for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
+      std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return R[a].node < R[b].node; });
+      std::vector<Ent> Es;
+      std::vector<uint32_t> Ms;
+      for (size_t i : ord) { Es.push_back(R[i]); Ms.push_back(mask[i]); }
+      samu_replay_stage& RS = out->stages[out->n_stages++];
+      RS.n_entries = (int)Es.size();
+      int g_used = 0;
+      for (size_t i = 0; i < Es.size(); ++i) {
+        RS.node[i] = Es[i].node; RS.dp[i] = Es[i].dp; RS.tp[i] = Es[i].tp;
+        RS.gpu_mask[i] = Ms[i];
+        RS.resumed[i] = resumes(Es[i]) ? 1 : 0;
+        g_used += Es[i].dp * Es[i].tp;
+      }
+      RS.planned_stage = cur;
+      // score the actual stage on the device (f* = first finisher), then commit it
+      new_stage_caches();
+      int32_t b = -1;
+      double mx = 0.0;
+      std::vector<StageOut> so;
+      RET(score_batch({Cand{Es, Es[0]}}, 0.0, 0, 1, &b, &mx, so, false));
+      const StageOut chosen = so[0];
+      {
+        int fslot = -1;
+        RET(ensure_full(Es[chosen.fstar], Es, &fslot));
+        samu_trial_rec r0;
+        CK(c, cudaMemcpyAsync(&r0, rec(fslot), sizeof(r0), cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaStreamSynchronize(c->stream));
+        if (!(r0.flags & 1u)) FAIL(c, SAMU_E_STATE, "replay: first finisher is blocked");
+      }
+      RET(commit_stage(Es, chosen));
+      RET(node_status(undone));
+      RS.first_finisher = Es[chosen.fstar].node;
+      RS.t_start = clock;
+      RS.duration = chosen.mean_tE;
+      RS.idle_gpus = N - g_used;
+      clock += chosen.mean_tE;
+      out->idle_gpu_seconds += (double)(N - g_used) * chosen.mean_tE;
+      // dynamic scheduler transition
+      std::vector<Ent> R_unf;
+      std::vector<uint32_t> M_unf;
+      for (size_t i = 0; i < R.size(); ++i)
+        if (!done(R[i].node)) { R_unf.push_back(R[i]); M_unf.push_back(mask[i]); }
+      R.clear(); mask.clear(); used = 0;
+      auto keep = [&](size_t i) { R.push_back(R_unf[i]); mask.push_back(M_unf[i]); used |= M_unf[i]; };
+      if (!Q.empty()) {
+        for (size_t i = 0; i < R_unf.size(); ++i) keep(i);
+        place_from_Q();
+      } else {
+        int nxt = cur + 1;
+        while (nxt < S_n) {
+          bool live = false;
+          for (const Ent& e : stage_entries(nxt)) if (!done(e.node)) live = true;
+          if (live) break;
+          ++nxt;
+        }
+        if (nxt >= S_n) {
+          for (size_t i = 0; i < R_unf.size(); ++i) keep(i);
+        } else {
+          const std::vector<Ent> En = stage_entries(nxt);
+          std::vector<size_t> maybe, ordu(R_unf.size());
+          for (size_t i = 0; i < ordu.size(); ++i) ordu[i] = i;
+          std::sort(ordu.begin(), ordu.end(), [&](size_t a2, size_t b2) { return R_unf[a2].node < R_unf[b2].node; });
+          for (size_t i : ordu) {
+            const Ent& e = R_unf[i];
+            if (last_stage[e.node] <= cur) { keep(i); out->n_kept_last++; }
+            else if (has(En, e)) keep(i);
+            else if (has_node(En, e.node)) { /* gives way to its E_nxt plan */ }
+            else maybe.push_back(i);
+          }
+          Q.clear();
+          for (const Ent& e : En) if (!done(e.node) && !has(R, e)) Q.push_back(e);
+          soft = 0;
+          for (size_t i : maybe) soft |= M_unf[i];
+          place_from_Q();
+          soft = 0;
+          for (size_t i : maybe) {
+            if (Q.empty() && !(used & M_unf[i])) { keep(i); out->n_kept_room++; }
+            else out->n_stopped++;
+          }
+          cur = nxt;
+        }
+      }
+      for (const Ent& e : drop_blocked()) {
+        if (last_stage[e.node] >= cur && has(stage_entries(cur), e)) Q.insert(Q.begin(), e);
+        else out->n_stopped++;
+      }
+    }
+    out->total = clock;
+    out->planned_total = plan->total;
     return SAMU_OK;
   }
 };
@@ -1395,6 +1599,20 @@ extern "C" samu_status samu_plan_max_heuristic(samu_ctx* c, uint64_t seed, int32
 extern "C" samu_status samu_plan_min_heuristic(samu_ctx* c, uint64_t seed, int32_t n_trials, samu_plan** out) {
   const samu_plan_opts o{SAMU_ALGO_MIN, 1, nullptr};
   return plan_with(c, seed, n_trials, &o, out);
+}
+
+extern "C" samu_status samu_replay_plan(samu_ctx* c, const samu_plan* plan, uint64_t seed, const uint32_t* known_l_out,
+                                        samu_replay* out) {
+  GUARD(c);
+  if (!plan || !out || plan->n_stages < 1 || plan->n_stages > 64) FAIL(c, SAMU_E_INVALID, "replay: bad arguments");
+  if (!c->app_loaded) FAIL(c, SAMU_E_INVALID, "replay: no app loaded");
+  for (int k = 0; k < plan->n_stages; ++k)
+    if (plan->stages[k].n_entries < 1 || plan->stages[k].n_entries > 16) FAIL(c, SAMU_E_INVALID, "replay: bad stage");
+  Replay G;
+  G.c = c;
+  G.plan = plan;
+  if (known_l_out) RET(upload_known(c, known_l_out, &G.known));
+  return G.run_replay(seed, out);
 }
 
 extern "C" void samu_plan_free(samu_plan* p) { delete p; }

@@ -39,11 +39,24 @@ def test_binding_names_match_abi():
     assert set(binding.EXPORTED) == set(declared_functions())
 
 
-def test_struct_layouts():
+def test_struct_layouts(tmp_path):
+    # every struct the binding marshals has the C compiler's size (and a few pinned ones)
+    import subprocess
     from paper_2503_16893_b200 import binding as B
     assert ctypes.sizeof(B.samu_trial_rec) == 40
     assert ctypes.sizeof(B.samu_request) == 20
     assert ctypes.sizeof(B.samu_candidate) == 24
+    names = ["samu_model_spec", "samu_engine_cfg", "samu_request", "samu_trial_rec", "samu_candidate",
+             "samu_cand_summary", "samu_plan_stage", "samu_plan", "samu_plan_opts", "samu_replay_stage",
+             "samu_replay"]
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include "samu.h"\nint main(void){\n' +
+                   "".join(f'printf("%zu\\n", sizeof({n}));\n' for n in names) + "return 0;}\n")
+    exe = tmp_path / "sz"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    sizes = [int(x) for x in subprocess.check_output([str(exe)]).split()]
+    for n, sz in zip(names, sizes):
+        assert ctypes.sizeof(getattr(B, n)) == sz, n
 
 
 def test_no_cpu_fallback():

@@ -307,6 +307,35 @@ def test_known_lengths_plan_bit_exact(algo):
         assert pg == po
 
 
+# runtime replay with the dynamic scheduler
+@pytest.mark.parametrize("algo", ["greedy", "max", "min"])
+@pytest.mark.parametrize("name,kw", [
+    ("c2", dict(n_prompts=120)),
+    ("c4", dict(n_docs=60)),
+    ("c5", dict(n_prompts=40, n_docs=30)),
+])
+def test_replay_bit_exact(name, kw, algo):
+    w = W.make_workload(name, n_trials=1, **kw)
+    P = O.Problem(w)
+    plan = P.plan_greedy(SEED, 1, algo)
+    S = gpu(w)
+    for seed in (SEED, 4242):                       # own lengths, then mispredicted lengths
+        assert S.samu_replay_plan(plan, seed) == P.replay(plan, seed)
+    l_true = np.random.default_rng(5).integers(1, 600, w.n_req).astype(np.uint32)
+    assert S.samu_replay_plan(plan, 0, known_l_out=l_true) == P.replay(plan, 0, known_l_out=l_true)
+
+
+def test_replay_hand_fixtures_bit_exact():
+    from tests.test_oracle_pins import _hand_plan, _replay_fixture
+    cases = [(_replay_fixture([2, 3, 4], 4, cap=8), [[(0, 1, 1), (1, 1, 1), (2, 1, 1)], [(1, 1, 1), (2, 2, 1)]],
+              np.array([5, 5] + [1] * 7, np.uint32))]
+    for n_gpus in (2, 3):
+        cases.append((_replay_fixture([2, 4, 4], n_gpus), [[(0, 1, 1), (1, 1, 1)], [(2, 2, 1)], [(1, 1, 1)]], None))
+    for w, stages, lt in cases:
+        plan = _hand_plan(stages)
+        assert gpu(w).samu_replay_plan(plan, SEED, known_l_out=lt) == O.Problem(w).replay(plan, SEED, known_l_out=lt)
+
+
 # ------------------------------------------------------------------------------------------
 # full size, bench launch configuration: sampled (candidate, trial) pairs vs the oracle
 # ------------------------------------------------------------------------------------------
@@ -422,6 +451,20 @@ def test_local_ranks_greedy_plan_identical(world):
         assert [s["mean_tE"] for s in pg["stages"]] == [s["mean_tE"] for s in ref["stages"]]
         assert [s["T_E"] for s in pg["stages"]] == [s["T_E"] for s in ref["stages"]]
         assert pg["total"] == ref["total"]
+
+
+def test_local_ranks_replay_identical():
+    w = W.make_workload("c5", n_prompts=40, n_docs=30, n_trials=1)
+    P = O.Problem(w)
+    plan = P.plan_greedy(SEED, 1, "greedy")
+    ref = P.replay(plan, 4242)
+
+    def fn(S, r, st):
+        S.load_workload(w)
+        return S.samu_replay_plan(plan, 4242)
+
+    for rp in _run_ranks(2, fn):
+        assert rp == ref
 
 
 def test_local_ranks_sharded_summary_identical():

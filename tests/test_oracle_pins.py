@@ -620,3 +620,119 @@ def test_known_lengths_plan_equals_single_trial_plan():
     lo, _ = P.sample(SEED, 0, 1)
     for algo in ("greedy", "max", "min"):
         assert P.plan_greedy(SEED, 1, algo) == P.plan_greedy(12345, 1, algo, known_l_out=lo[0])
+
+
+# ------------------------------------------------------------------------------------------
+# runtime replay with the dynamic scheduler (reading c33)
+# ------------------------------------------------------------------------------------------
+def _hand_plan(stages):
+    return dict(stages=[dict(entries=E, fstar=E[0][0], mean_tE=1.0, T_E=1.0) for E in stages],
+                total=float(len(stages)))
+
+
+def _replay_fixture(counts, n_gpus, cap=1):
+    sp = F.spec(tp_values=(1,))
+    nodes = [dict(l_in=[4] * c, l_out=[cap] * c, sp=sp) for c in counts]
+    return F.multi(nodes, eng=F.engine(n_gpus=n_gpus, max_num_seqs=1))
+
+
+@pytest.mark.parametrize("algo", ["greedy", "max", "min"])
+def test_replay_with_the_plans_own_lengths_reproduces_it(algo):
+    # "oracle identical to the planner's sampled lengths -> measured total equals planned
+    # total exactly" (one-trial plan: the replay finds the planned first finishers).  Exception
+    # required by P:626: when a planned stage leaves GPUs free, a running pair absent from it
+    # keeps running ("then consider (M, P) if there are still available GPUs"), so the replay
+    # may diverge there -- and only by such kept pairs.
+    diverged = 0
+    for w in (F.fig1(), W.make_workload("c2", n_prompts=120, n_trials=1),
+              W.make_workload("c5", n_prompts=40, n_docs=30, n_trials=1)):
+        P = O.Problem(w)
+        plan = P.plan_greedy(SEED, 1, algo)
+        r = P.replay(plan, SEED)
+        rs, ps = r["stages"], plan["stages"]
+        i = 0
+        while i < len(ps) and i < len(rs) and rs[i]["entries"] == ps[i]["entries"]:
+            assert rs[i]["duration"] == ps[i]["mean_tE"] and rs[i]["first_finisher"] == ps[i]["fstar"]
+            i += 1
+        if i == len(ps):
+            assert len(rs) == len(ps) and r["total"] == plan["total"] and r["n_kept_room"] == 0
+        else:
+            diverged += 1
+            extra = set(rs[i]["entries"]) - set(ps[i]["entries"])
+            assert set(ps[i]["entries"]) <= set(rs[i]["entries"]) and extra
+            assert extra <= set(rs[i - 1]["entries"]) and r["n_kept_room"] >= 1
+    assert diverged <= 1
+
+
+def test_replay_misprediction_keeps_last_stage_model_running():
+    # P:622-625 hand trace (1 s per iteration, one sequence per replica, 4 GPUs): planned
+    # E1 = {A, B, C} ending with A, E2 = {B, C on 2 GPUs}.  True lengths make A's two requests
+    # 5 tokens (10 s): B finishes first at 3 s.  A's last planned stage is E1 -> keeps running
+    # (resumed); C's plan changes -> reloaded on 2 GPUs, its 1 remaining request takes 1 s;
+    # A then runs alone for the remaining 10 - 4 = 6 s.  Total 3 + 1 + 6 = 10 s.
+    w = _replay_fixture([2, 3, 4], 4, cap=8)
+    plan = _hand_plan([[(0, 1, 1), (1, 1, 1), (2, 1, 1)], [(1, 1, 1), (2, 2, 1)]])
+    l_true = np.array([5, 5] + [1] * 7, np.uint32)
+    r = O.Problem(w).replay(plan, SEED, known_l_out=l_true)
+    st = r["stages"]
+    assert [s["entries"] for s in st] == [[(0, 1, 1), (1, 1, 1), (2, 1, 1)], [(0, 1, 1), (2, 2, 1)], [(0, 1, 1)]]
+    assert [s["first_finisher"] for s in st] == [1, 2, 0]
+    assert [s["duration"] for s in st] == [3.0, 1.0, 6.0]
+    assert st[1]["resumed"] == [1, 0] and st[2]["resumed"] == [1]
+    assert st[0]["gpu_mask"] == [0b0001, 0b0010, 0b0100] and st[1]["gpu_mask"] == [0b0001, 0b0110]
+    assert r["total"] == 10.0 and r["n_kept_last"] == 1
+    assert r["idle_gpu_seconds"] == 1 * 3.0 + 1 * 1.0 + 3 * 6.0
+
+
+@pytest.mark.parametrize("n_gpus", [2, 3])
+def test_replay_pair_absent_from_next_stage(n_gpus):
+    # P:625-626 hand traces.  Planned E1 = {0, 1}, E2 = {2 on 2 GPUs}, E3 = {1}.  Model 0 ends
+    # E1 at 2 s; model 1 (2 of 4 requests left) is not in E2.
+    #  N = 2: E2 takes every GPU -> model 1 is stopped and reloaded in E3: 2 + 2 + 2 = 6 s.
+    #  N = 3: E2 is placed on GPUs {0, 2} (sparing model 1's GPU 1) and model 1 keeps running
+    #         beside it; both end at 2 s: 2 + 2 = 4 s ("if GPUs remain").
+    w = _replay_fixture([2, 4, 4], n_gpus)
+    plan = _hand_plan([[(0, 1, 1), (1, 1, 1)], [(2, 2, 1)], [(1, 1, 1)]])
+    r = O.Problem(w).replay(plan, SEED)
+    st = r["stages"]
+    if n_gpus == 2:
+        assert [s["entries"] for s in st] == [[(0, 1, 1), (1, 1, 1)], [(2, 2, 1)], [(1, 1, 1)]]
+        assert st[2]["resumed"] == [0] and r["n_stopped"] == 1
+        assert r["total"] == 6.0 and r["idle_gpu_seconds"] == 2.0
+    else:
+        assert [s["entries"] for s in st] == [[(0, 1, 1), (1, 1, 1)], [(1, 1, 1), (2, 2, 1)]]
+        assert st[1]["resumed"] == [1, 0] and st[1]["gpu_mask"] == [0b010, 0b101]
+        assert r["n_kept_room"] == 1 and r["total"] == 4.0 and r["idle_gpu_seconds"] == 2.0
+
+
+def test_replay_idle_time_fig1_max_heuristic():
+    # S:553 interval arithmetic: Max-heuristic on the Fig. 1 fixture runs models 1-5 on 3 of
+    # the 4 GPUs for 1 s each -> 5 idle GPU-seconds; greedy and Min keep every GPU busy
+    P = O.Problem(F.fig1())
+    for algo, idle in (("max", 5.0), ("greedy", 0.0), ("min", 0.0)):
+        r = P.replay(P.plan_greedy(SEED, 1, algo), 99)
+        assert r["idle_gpu_seconds"] == idle
+
+
+def test_replay_invariants_under_mispredicted_lengths():
+    # no GPU over-commit (disjoint masks of the right size), planned stages visited in
+    # order, every model finishes, clock = sum of durations
+    w = W.make_workload("c5", n_prompts=40, n_docs=30, n_trials=1)
+    P = O.Problem(w)
+    for algo in ("greedy", "min"):
+        plan = P.plan_greedy(SEED, 1, algo)
+        r = P.replay(plan, 4242)
+        last = -1
+        t = 0.0
+        for s in r["stages"]:
+            used = 0
+            for (v, d, tp), m in zip(s["entries"], s["gpu_mask"]):
+                assert bin(m).count("1") == d * tp and (used & m) == 0
+                used |= m
+            assert used < (1 << w.engine["n_gpus"])
+            assert s["planned_stage"] >= last
+            last = s["planned_stage"]
+            assert s["t_start"] == t
+            t += s["duration"]
+        assert r["total"] == t
+        assert {s["first_finisher"] for s in r["stages"]} <= set(range(w.n_nodes))
