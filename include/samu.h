@@ -251,6 +251,19 @@ typedef struct samu_plan_opts {
 samu_status samu_plan_run(samu_ctx* ctx, uint64_t seed, int32_t n_trials, const samu_plan_opts* opts, samu_plan** out);
 void samu_plan_free(samu_plan* plan);
 
+/* Per-iteration cost-model coefficients from profiled iterations (reading c34): for
+ * each bucket k (one (model, tp, phase, B) combination), the samples [off[k], off[k+1]) of
+ * (x, latency) -- x = FLOPs, B*s or S per phase -- are fitted by least squares, latency = a x + b
+ * (a < 0 clamped to 0, b = mean latency).  trim_permille > 0 drops the floor(n * trim / 1000)
+ * samples of largest |residual| (ties: lower index) and refits ("noise points", Fig. 5).
+ * All arrays are device memory: off [n_buckets + 1] i64, x / y [off[n_buckets]] f64, out_a /
+ * out_b [n_buckets] f64, out_n_used (samples kept) / out_flags (bit0 degenerate, bit1 a
+ * clamped) [n_buckets] i32.  SAMU_E_INVALID if a bucket has fewer than two distinct x (its
+ * outputs are 0).  Synchronises the context stream. */
+samu_status samu_fit_coeffs(samu_ctx* ctx, int32_t n_buckets, const int64_t* off, const double* x, const double* y,
+                            int32_t trim_permille, double* out_a, double* out_b, int32_t* out_n_used,
+                            int32_t* out_flags);
+
 /* Runtime replay with the dynamic scheduler (reading c33): executes `plan` against
  * true output lengths -- known_l_out host [n_req], or NULL = trial 0 of the sampler with `seed`
  * (a different seed than the plan's stands in for the real run) -- one trial on the device.

@@ -124,6 +124,7 @@ def lib():
         L.or_plan_max_heuristic.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(or_plan)]
         L.or_plan_min_heuristic.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(or_plan)]
         L.or_known_lengths.argtypes = [P, P, P, P]
+        L.or_fit_coeffs.argtypes = [C.c_int32, P, P, P, C.c_int32, P, P, P, P]
         L.or_replay_plan.argtypes = [P, C.POINTER(or_plan), C.c_uint64, P, C.POINTER(or_replay)]
         L.or_plan_run.argtypes = [P, C.c_uint64, C.c_int32, C.c_int32, C.c_int32, P, C.POINTER(or_plan)]
         _lib = L
@@ -315,6 +316,19 @@ class Problem:
             stages.append(dict(entries=[(s.node[j], s.dp[j], s.tp[j]) for j in range(s.n_entries)],
                                fstar=s.fstar, mean_tE=s.mean_tE, T_E=s.T_E))
         return dict(stages=stages, total=plan.total, n_cand_evals=plan.n_cand_evals)
+
+
+def fit_coeffs(off, x, y, trim_permille=10):
+    """Per-bucket least-squares (a, b) with top-residual trimming (reading c34).
+    Returns (a, b, n_used, flags, rc): rc != 0 if a bucket has < 2 distinct x."""
+    off = np.ascontiguousarray(off, np.int64)
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.ascontiguousarray(y, np.float64)
+    nb = len(off) - 1
+    a, b = np.zeros(nb), np.zeros(nb)
+    n_used, flags = np.zeros(nb, np.int32), np.zeros(nb, np.int32)
+    rc = lib().or_fit_coeffs(nb, _ptr(off), _ptr(x), _ptr(y), trim_permille, _ptr(a), _ptr(b), _ptr(n_used), _ptr(flags))
+    return a, b, n_used, flags, rc
 
 
 def rec_flops(rec) -> np.ndarray:

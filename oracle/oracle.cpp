@@ -1286,3 +1286,78 @@ extern "C" int32_t or_replay_plan(const or_problem* p, const or_plan* plan, uint
     return rc;
   }
 }
+
+// ---------------------------------------------------------------------------------------------
+// Per-iteration cost-model coefficients ("We profile the per-iteration computation
+// with different inference workloads to compute the constants"; reading c34).  For each bucket
+// (model, tp, phase, B) the least-squares line latency = a x + b over its samples (x = FLOPs,
+// B s or S): means, then centred sums Sxx = sum (x - mx)^2, Sxy = sum (x - mx)(y - my), a =
+// Sxy / Sxx, b = my - a mx; a < 0 is clamped to 0 with b = my.  Noise points (P: Fig. 5, "we
+// can ignore them"): after a first fit the floor(n * trim_permille / 1000) samples of largest
+// |residual| (ties: lower sample index first) are dropped and the line is refitted.  A bucket
+// with fewer than two distinct x (before or after trimming) is an error.
+// ---------------------------------------------------------------------------------------------
+static int fit_line(const std::vector<double>& X, const std::vector<double>& Y, double* a, double* b, int* clamped) {
+  const size_t n = X.size();
+  if (n < 2) return 1;
+  double xmin = X[0], xmax = X[0];
+  for (double v : X) { xmin = std::min(xmin, v); xmax = std::max(xmax, v); }
+  if (!(xmin < xmax)) return 1;
+  double sx = 0.0, sy = 0.0;
+  for (size_t i = 0; i < n; ++i) { sx += X[i]; sy += Y[i]; }
+  const double mx = sx / (double)n, my = sy / (double)n;
+  double sxx = 0.0, sxy = 0.0;
+  for (size_t i = 0; i < n; ++i) {
+    const double dx = X[i] - mx, dy = Y[i] - my;
+    sxx += dx * dx;
+    sxy += dx * dy;
+  }
+  double A = sxy / sxx;
+  double B = my - A * mx;
+  *clamped = 0;
+  if (A < 0.0) { A = 0.0; B = my; *clamped = 1; }
+  *a = A;
+  *b = B;
+  return 0;
+}
+
+extern "C" int32_t or_fit_coeffs(int32_t n_buckets, const int64_t* off, const double* x, const double* y,
+                                 int32_t trim_permille, double* out_a, double* out_b, int32_t* out_n_used,
+                                 int32_t* out_flags) {
+  if (n_buckets < 0 || !off || trim_permille < 0 || trim_permille > 500) { set_err("fit: bad arguments"); return OR_E_INVALID; }
+  int bad = -1;
+  for (int k = 0; k < n_buckets; ++k) {
+    std::vector<double> X(x + off[k], x + off[k + 1]), Y(y + off[k], y + off[k + 1]);
+    double a = 0.0, b = 0.0;
+    int cl = 0;
+    int32_t flags = 0;
+    if (fit_line(X, Y, &a, &b, &cl)) flags |= 1;
+    else {
+      const size_t n = X.size();
+      const size_t drop = (size_t)((int64_t)n * trim_permille / 1000);
+      if (drop > 0) {
+        std::vector<std::pair<double, size_t>> r(n);
+        for (size_t i = 0; i < n; ++i) r[i] = {std::fabs(Y[i] - (a * X[i] + b)), i};
+        std::sort(r.begin(), r.end(), [](const std::pair<double, size_t>& p, const std::pair<double, size_t>& q) {
+          if (p.first != q.first) return p.first > q.first;
+          return p.second < q.second;
+        });
+        std::vector<char> gone(n, 0);
+        for (size_t i = 0; i < drop; ++i) gone[r[i].second] = 1;
+        std::vector<double> X2, Y2;
+        for (size_t i = 0; i < n; ++i) if (!gone[i]) { X2.push_back(X[i]); Y2.push_back(Y[i]); }
+        if (fit_line(X2, Y2, &a, &b, &cl)) flags |= 1;
+        out_n_used[k] = (int32_t)X2.size();
+      } else {
+        out_n_used[k] = (int32_t)n;
+      }
+    }
+    if (flags & 1) { a = 0.0; b = 0.0; out_n_used[k] = 0; if (bad < 0) bad = k; }
+    if (cl && !(flags & 1)) flags |= 2;
+    out_a[k] = a;
+    out_b[k] = b;
+    out_flags[k] = flags;
+  }
+  if (bad >= 0) { set_err("fit: bucket " + std::to_string(bad) + " has fewer than two distinct x"); return OR_E_INVALID; }
+  return OR_OK;
+}

@@ -167,6 +167,11 @@ typedef struct or_replay {
 int32_t or_replay_plan(const or_problem* p, const or_plan* plan, uint64_t seed, const uint32_t* known_l_out,
                        or_replay* out);
 
+/* least-squares coefficient fit per bucket with top-residual trimming; samples of
+ * bucket k are [off[k], off[k+1]); flags bit0 = degenerate bucket (error), bit1 = a clamped */
+int32_t or_fit_coeffs(int32_t n_buckets, const int64_t* off, const double* x, const double* y, int32_t trim_permille,
+                      double* out_a, double* out_b, int32_t* out_n_used, int32_t* out_flags);
+
 #ifdef __cplusplus
 }
 #endif

@@ -90,7 +90,7 @@ EXPORTED = ["samu_ctx_create", "samu_ctx_destroy", "samu_local_group_create", "s
             "samu_model_register",
             "samu_ecdf_load", "samu_app_load", "samu_enumerate_plans", "samu_sample_lengths", "samu_simulate_batch",
             "samu_plan_greedy", "samu_plan_max_heuristic", "samu_plan_min_heuristic", "samu_plan_run", "samu_known_lengths",
-            "samu_replay_plan", "samu_plan_free"]
+            "samu_replay_plan", "samu_fit_coeffs", "samu_plan_free"]
 
 _lib = None
 
@@ -129,6 +129,7 @@ def lib():
                                     C.POINTER(C.POINTER(samu_plan))]
         L.samu_known_lengths.argtypes = [P, P, P, P]
         L.samu_replay_plan.argtypes = [P, C.POINTER(samu_plan), C.c_uint64, P, C.POINTER(samu_replay)]
+        L.samu_fit_coeffs.argtypes = [P, C.c_int32, P, P, P, C.c_int32, P, P, P, P]
         L.samu_plan_free.argtypes = [C.POINTER(samu_plan)]
         L.samu_plan_free.restype = None
         _lib = L
@@ -363,6 +364,36 @@ class Samu:
         return dict(stages=stages, total=out.total, planned_total=out.planned_total,
                     idle_gpu_seconds=out.idle_gpu_seconds, n_kept_last=out.n_kept_last,
                     n_kept_room=out.n_kept_room, n_stopped=out.n_stopped)
+
+    def samu_fit_coeffs(self, off, x, y, trim_permille: int = 10):
+        """Per-bucket least-squares cost coefficients with noise-point trimming.
+        off [nb + 1] / x / y: host arrays or device tensors.  Returns numpy (a, b, n_used, flags)."""
+        torch = self.torch
+
+        def dev(v, dt):
+            if isinstance(v, torch.Tensor):
+                return v.to(device=self.device, dtype=dt).contiguous()
+            return torch.as_tensor(np.asarray(v), dtype=dt).to(self.device)
+
+        o, xd, yd = dev(off, torch.int64), dev(x, torch.float64), dev(y, torch.float64)
+        nb = o.numel() - 1
+        a = torch.zeros(nb, dtype=torch.float64, device=self.device)
+        b = torch.zeros_like(a)
+        nu = torch.zeros(nb, dtype=torch.int32, device=self.device)
+        fl = torch.zeros_like(nu)
+        self._check(lib().samu_fit_coeffs(self.h, nb, _t_ptr(o), _t_ptr(xd), _t_ptr(yd), trim_permille, _t_ptr(a),
+                                          _t_ptr(b), _t_ptr(nu), _t_ptr(fl)))
+        return a.cpu().numpy(), b.cpu().numpy(), nu.cpu().numpy(), fl.cpu().numpy()
+
+
+def coeff_table(bucket, a, b, n_buckets_B: int) -> np.ndarray:
+    """Fitted (a, b) per (slot, phase, B index) bucket -> the [5][3][2][nb] table
+    samu_model_register takes (tp slots without samples stay 0)."""
+    out = np.zeros((N_TP_SLOTS, 3, 2, n_buckets_B), dtype=np.float64)
+    for k, (slot, ph, bi) in enumerate(bucket):
+        out[slot, ph, 0, bi] = a[k]
+        out[slot, ph, 1, bi] = b[k]
+    return out
 
 
 def recs_to_numpy(recs) -> np.ndarray:

@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libsamu.so")
-SOURCES = ["k_sample.cu", "k_simulate.cu", "k_reduce.cu", "samu_host.cu"]
+SOURCES = ["k_sample.cu", "k_simulate.cu", "k_reduce.cu", "k_fit.cu", "samu_host.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

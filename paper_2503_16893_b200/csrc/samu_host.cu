@@ -107,7 +107,7 @@ struct samu_ctx {
   std::vector<uint8_t> cross;
   std::vector<std::vector<int32_t>> waves;
   DevBuf d_l_in_base, d_cap, d_pred, d_node, d_succ, d_cross;
-  DevBuf d_tab, d_tab_off, d_nobs, d_mnode, d_lmax, d_known;
+  DevBuf d_tab, d_tab_off, d_nobs, d_mnode, d_lmax, d_known, d_fit_gone;
   int32_t smem_tab_bytes = 0;
   std::vector<DevBuf> d_waves;
   std::map<std::pair<int, int>, DevBuf> coef;                      // (model, tp slot) -> dense table
@@ -1613,6 +1613,29 @@ extern "C" samu_status samu_replay_plan(samu_ctx* c, const samu_plan* plan, uint
   G.plan = plan;
   if (known_l_out) RET(upload_known(c, known_l_out, &G.known));
   return G.run_replay(seed, out);
+}
+
+extern "C" samu_status samu_fit_coeffs(samu_ctx* c, int32_t n_buckets, const int64_t* off, const double* x,
+                                       const double* y, int32_t trim_permille, double* out_a, double* out_b,
+                                       int32_t* out_n_used, int32_t* out_flags) {
+  GUARD(c);
+  if (n_buckets < 0 || (n_buckets && (!off || !x || !y || !out_a || !out_b || !out_n_used || !out_flags)) ||
+      trim_permille < 0 || trim_permille > 500)
+    FAIL(c, SAMU_E_INVALID, "fit_coeffs: bad arguments");
+  if (!n_buckets) return SAMU_OK;
+  int64_t n_total = 0;
+  CK(c, cudaMemcpyAsync(&n_total, off + n_buckets, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  if (n_total < 0) FAIL(c, SAMU_E_INVALID, "fit_coeffs: bad offsets");
+  CK(c, c->d_fit_gone.ensure(std::max<int64_t>(n_total, 1)));
+  CK(c, samu_count(c, launch_fit(off, n_buckets, x, y, trim_permille, c->d_fit_gone.as<uint8_t>(), out_a, out_b,
+                                 out_n_used, out_flags, c->stream)));
+  std::vector<int32_t> flags(n_buckets);
+  CK(c, cudaMemcpyAsync(flags.data(), out_flags, sizeof(int32_t) * n_buckets, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  for (int k = 0; k < n_buckets; ++k)
+    if (flags[k] & 1) FAIL(c, SAMU_E_INVALID, "fit_coeffs: bucket " + std::to_string(k) + " has fewer than two distinct x");
+  return SAMU_OK;
 }
 
 extern "C" void samu_plan_free(samu_plan* p) { delete p; }

@@ -115,3 +115,6 @@ cudaError_t launch_fstar(const samu_trial_rec* cache, int32_t T, const StageCand
 cudaError_t launch_stage_score(const samu_trial_rec* cache, int32_t T, const StageCand* sc, int32_t n,
                                StageOut* out, double TE_star, int32_t gpus_star, int32_t mode, int32_t* best,
                                double* max_dT, cudaStream_t s);
+cudaError_t launch_fit(const int64_t* off, int32_t n_buckets, const double* x, const double* y, int32_t trim_permille,
+                       uint8_t* gone, double* out_a, double* out_b, int32_t* out_n_used, int32_t* out_flags,
+                       cudaStream_t s);

@@ -142,6 +142,43 @@ def make_coeff(rng: np.random.Generator, spec: Dict[str, int], coeff_B: np.ndarr
     return out
 
 
+def make_profile(w: "Workload", model: int, n_per_bucket: int = 200, noise: float = 0.002,
+                 outlier_frac: float = 0.005, seed: int = WORKLOAD_SEED):
+    """Synthetic per-iteration profile of one model (the input of the coefficient fit):
+    for every allowed tp slot, phase and profiled batch size B, n_per_bucket iterations with x
+    spread over the phase's range (FLOPs of B sequences of 16..2048 context tokens; B*s with
+    s in 1..2048; S in 16B..4096B), latency = the workload's (a, b) line x (1 + noise N(0,1)),
+    and a fraction of 'noise points' (Fig. 5) slowed 2-5x.  Buckets are laid out
+    (slot, phase, B index) in that order; returns dict(off, x, y, bucket) with bucket
+    (slot, phase, bi) per bucket row."""
+    rng = np.random.default_rng([seed, model, 489])
+    spec = w.models[model]
+    cf = w.coeff[model]
+    xs, ys, off, bucket = [], [], [0], []
+    for slot in range(N_TP_SLOTS):
+        if not (spec["tp_mask"] >> slot) & 1:
+            continue
+        tp = 1 << slot
+        for ph in range(N_PHASES):
+            for bi, B in enumerate(w.coeff_B.astype(np.float64)):
+                if ph == 0:
+                    ctx = rng.uniform(16, 2048, n_per_bucket) * B
+                    x = spec["L"] * (spec["c"] * B + 2.0 * spec["h"] * ctx / tp)
+                elif ph == 1:
+                    x = B * rng.integers(1, 2049, n_per_bucket).astype(np.float64)
+                else:
+                    x = rng.uniform(16 * B, 4096 * B, n_per_bucket)
+                a, b = cf[slot, ph, 0, bi], cf[slot, ph, 1, bi]
+                y = (a * x + b) * (1.0 + noise * rng.standard_normal(n_per_bucket))
+                out = rng.random(n_per_bucket) < outlier_frac
+                y[out] *= rng.uniform(2.0, 5.0, int(out.sum()))
+                xs.append(x)
+                ys.append(y)
+                off.append(off[-1] + n_per_bucket)
+                bucket.append((slot, ph, bi))
+    return dict(off=np.array(off, np.int64), x=np.concatenate(xs), y=np.concatenate(ys), bucket=bucket)
+
+
 def make_load(rng: np.random.Generator, spec: Dict[str, int]):
     """Loading cost table in seconds, 11-47 s, per (tp slot, dp)."""
     out = np.zeros((N_TP_SLOTS, MAX_DP), dtype=np.float64)

@@ -336,6 +336,47 @@ def test_replay_hand_fixtures_bit_exact():
         assert gpu(w).samu_replay_plan(plan, SEED, known_l_out=lt) == O.Problem(w).replay(plan, SEED, known_l_out=lt)
 
 
+# cost-model coefficient fit
+def _close(g, o, rel=1e-9):
+    return np.all(np.abs(g - o) <= rel * np.maximum(np.abs(o), 1e-300))
+
+
+@pytest.mark.parametrize("trim", [0, 10, 50])
+def test_fit_coeffs_parity_on_profiles(trim):
+    w = W.make_workload("c5", n_prompts=10, n_docs=5, n_trials=1)
+    S = gpu(w)
+    for m in range(len(w.models)):
+        pr = W.make_profile(w, m, n_per_bucket=300 + 37 * m)
+        a, b, nu, fl = S.samu_fit_coeffs(pr["off"], pr["x"], pr["y"], trim)
+        oa, ob, onu, ofl, rc = O.fit_coeffs(pr["off"], pr["x"], pr["y"], trim)
+        assert rc == 0
+        assert (nu == onu).all() and (fl == ofl).all()
+        assert _close(a, oa) and _close(b, ob)
+
+
+def test_fit_coeffs_edge_cases():
+    from paper_2503_16893_b200 import SamuError
+    S = gpu(W.make_workload("c1", n_trials=1))
+    rng = np.random.default_rng(9)
+    # ragged buckets incl. 2-sample, constant-y, negative slope, large bucket (several CTAs' work)
+    sizes = [2, 3, 5, 1000, 70000, 1]
+    xs = [rng.uniform(0, 10, n) for n in sizes[:-1]] + [np.array([1.0])]
+    ys = [2 * xs[0] + 1, np.full(3, 4.0), 10 - xs[2], 1e-3 * xs[3] + 0.5 + rng.standard_normal(1000),
+          3e-2 * xs[4] + rng.standard_normal(70000), np.array([1.0])]
+    x, y = np.concatenate(xs[:-1]), np.concatenate(ys[:-1])
+    off = np.r_[0, np.cumsum(sizes[:-1])]
+    for trim in (0, 10, 300):
+        g = S.samu_fit_coeffs(off, x, y, trim)
+        o = O.fit_coeffs(off, x, y, trim)
+        assert o[4] == 0
+        assert (g[2] == o[2]).all() and (g[3] == o[3]).all() and _close(g[0], o[0]) and _close(g[1], o[1])
+    # degenerate bucket -> error, same flags as the oracle
+    off2 = np.r_[off, off[-1] + 1]
+    x2, y2 = np.r_[x, 1.0], np.r_[y, 1.0]
+    with pytest.raises(SamuError):
+        S.samu_fit_coeffs(off2, x2, y2, 0)
+
+
 # ------------------------------------------------------------------------------------------
 # full size, bench launch configuration: sampled (candidate, trial) pairs vs the oracle
 # ------------------------------------------------------------------------------------------

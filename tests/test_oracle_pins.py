@@ -736,3 +736,68 @@ def test_replay_invariants_under_mispredicted_lengths():
             t += s["duration"]
         assert r["total"] == t
         assert {s["first_finisher"] for s in r["stages"]} <= set(range(w.n_nodes))
+
+
+# ------------------------------------------------------------------------------------------
+# cost-model coefficient fit (reading c34)
+# ------------------------------------------------------------------------------------------
+def test_fit_exact_lines_and_round_trip():
+    # S:134 exact data latency = 2x + 1 -> (2, 1); S:150 / S:642 round trip: samples generated
+    # from known per-bucket (a, b) with zero noise refit within 1e-6 relative
+    a, b, nu, fl, rc = O.fit_coeffs([0, 10], np.arange(10.0), 2 * np.arange(10.0) + 1, 0)
+    assert rc == 0 and abs(a[0] - 2) <= 1e-12 and abs(b[0] - 1) <= 1e-12 and nu[0] == 10 and fl[0] == 0
+    w = W.make_workload("c2", n_prompts=10, n_trials=1)
+    pr = W.make_profile(w, 1, noise=0.0, outlier_frac=0.0)
+    a, b, nu, fl, rc = O.fit_coeffs(pr["off"], pr["x"], pr["y"], 0)
+    assert rc == 0 and (fl == 0).all()
+    for k, (s, p, i) in enumerate(pr["bucket"]):
+        assert abs(a[k] / w.coeff[1][s, p, 0, i] - 1) <= 1e-6
+        assert abs(b[k] / w.coeff[1][s, p, 1, i] - 1) <= 1e-6
+
+
+def test_fit_matches_independent_least_squares():
+    # closed-form normal equations vs numpy.polyfit (an independent LAPACK least-squares)
+    rng = np.random.default_rng(3)
+    off = [0]
+    xs, ys = [], []
+    for n in (2, 3, 17, 256, 1000):
+        x = rng.uniform(1e9, 5e12, n)
+        xs.append(x)
+        ys.append(3e-15 * x + 2e-3 + 1e-4 * rng.standard_normal(n))
+        off.append(off[-1] + n)
+    x, y = np.concatenate(xs), np.concatenate(ys)
+    a, b, nu, fl, rc = O.fit_coeffs(off, x, y, 0)
+    assert rc == 0
+    for k in range(len(off) - 1):
+        pa, pb = np.polyfit(x[off[k]:off[k + 1]], y[off[k]:off[k + 1]], 1)
+        if pa > 0:
+            assert abs(a[k] / pa - 1) <= 1e-9 and abs(b[k] / pb - 1) <= 1e-9
+
+
+def test_fit_trimming_drops_the_noise_points():
+    # Fig. 5 noise points: n = 1000, trim 1 % -> the 10 samples of largest residual go; 10
+    # gross outliers are exactly those, so the fit equals least squares on the clean samples
+    rng = np.random.default_rng(4)
+    x = rng.uniform(1.0, 100.0, 1000)
+    y = 0.5 * x + 3.0 + 0.01 * rng.standard_normal(1000)
+    bad = rng.choice(1000, 10, replace=False)
+    y[bad] += 500.0
+    a, b, nu, fl, rc = O.fit_coeffs([0, 1000], x, y, 10)
+    keep = np.setdiff1d(np.arange(1000), bad)
+    pa, pb = np.polyfit(x[keep], y[keep], 1)
+    assert rc == 0 and nu[0] == 990
+    assert abs(a[0] / pa - 1) <= 1e-9 and abs(b[0] / pb - 1) <= 1e-9
+    a0, _, nu0, _, _ = O.fit_coeffs([0, 1000], x, y, 0)
+    assert nu0[0] == 1000 and abs(a0[0] - 0.5) > abs(a[0] - 0.5)
+
+
+def test_fit_clamps_negative_slope_and_rejects_degenerate_buckets():
+    # negative fitted a clamped to 0 (b = mean latency, the least-squares constant);
+    # a bucket with < 2 distinct x is an error
+    x = np.arange(5.0)
+    a, b, nu, fl, rc = O.fit_coeffs([0, 5], x, 10.0 - x, 0)
+    assert rc == 0 and a[0] == 0.0 and b[0] == 8.0 and fl[0] == 2
+    a, b, nu, fl, rc = O.fit_coeffs([0, 5, 8], np.r_[x, 7.0, 7.0, 7.0], np.r_[x, 1.0, 2.0, 3.0], 0)
+    assert rc != 0 and fl.tolist() == [0, 1] and a[1] == 0.0 and nu[1] == 0
+    a, b, nu, fl, rc = O.fit_coeffs([0, 1], [1.0], [1.0], 0)
+    assert rc != 0 and fl[0] == 1
