@@ -35,6 +35,7 @@ struct WarpSm {
   uint32_t hist[32];         // running requests per phase
   uint32_t adm_req[32], adm_meta[32];
   int2 adm_fo[32];
+  double cbuf[32];           // per-iteration costs of a decode-run chunk (lane j = iteration j)
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -401,11 +402,21 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
           const bool valid = (uint32_t)lane < wn;
           const uint32_t p = valid ? w_p : 0u;
           const uint32_t nb = valid ? bs.cdiv(p) : 0u;
-          const uint32_t sp = warp_incl_scan(p, lane), sb = warp_incl_scan(nb, lane);
-          const bool ok = valid && (m.B + k_adm + lane + 1 <= ms) && (tok + sp <= C.budget) &&
-                          ((int32_t)(blk + sb) <= m.F);
-          const uint32_t bal = __ballot_sync(FULL, ok);
-          const uint32_t mm = (bal == FULL) ? 32u : (uint32_t)(__ffs(~bal) - 1);
+          uint32_t sp, sb, mm;
+          if (min(wn, ms - m.B - k_adm) <= 1u) {
+            // at most the head can enter (one free slot or one waiting request): no scans
+            sp = p;
+            sb = nb;
+            const uint32_t p0 = __shfl_sync(FULL, p, 0);
+            mm = (wn > 0 && m.B + k_adm < ms && tok + p0 <= C.budget && (int32_t)(blk + bs.cdiv(p0)) <= m.F) ? 1u : 0u;
+          } else {
+            sp = warp_incl_scan(p, lane);
+            sb = warp_incl_scan(nb, lane);
+            const bool ok = valid && (m.B + k_adm + lane + 1 <= ms) && (tok + sp <= C.budget) &&
+                            ((int32_t)(blk + sb) <= m.F);
+            const uint32_t bal = __ballot_sync(FULL, ok);
+            mm = (bal == FULL) ? 32u : (uint32_t)(__ffs(~bal) - 1);
+          }
           if (mm == 0) break;
           const bool adm = (uint32_t)lane < mm;
           const bool finish_now = adm && w_rem <= 1u;
@@ -529,6 +540,22 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
       } else {
         if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; m.site = 9; break; }
         // ================= decode run (c9): uniform iterations until an event ===============
+        const uint32_t need1 = W.hist[m.needidx];
+        if (m.next_fin == m.d + 1 && (int32_t)need1 <= m.F) {
+          // one decode that retires requests and needs no preemption: the run below with
+          // m_run = 1, without its search and closed forms (same arithmetic)
+          const uint32_t B1 = m.B;
+          const uint32_t smax = (uint32_t)((int32_t)m.d + m.maxO);
+          const uint64_t fl = LC * B1 + K1 * (uint64_t)m.S;
+          m.t = __dadd_rn(m.t, iter_cost(C.coef, ms, B1, fl, B1 * smax, m.S));
+          add_flops(m, fl);
+          m.reqit += B1;
+          m.iter += 1;
+          m.F -= (int32_t)need1;
+          m.S += B1;
+          m.d += 1;
+          m.needidx = m.needidx == 0 ? bs.v - 1 : m.needidx - 1;
+        } else {
         const uint32_t B = m.B;
         const double stop_t = fmin(m.tau, m.next_ready);
         // KV need of the run's decodes: histogram rotated to start at needidx, prefix sums
@@ -556,7 +583,47 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
           const double as_ = __ldg(cb + 4 * ms), bs_ = __ldg(cb + 5 * ms);
           const uint64_t f_last = K0 + K1 * ((uint64_t)m.S + (uint64_t)B * (m_run - 1));
           double t = m.t;
-          if (f_last < (1ull << 53)) {
+          if (m_run > 4) {
+            // lane j evaluates iteration done_it + j of a 32-iteration chunk (the x of every
+            // iteration are exact integers, so their conversions equal the sequential
+            // increments), then the chunk's costs are added to t one by one in iteration order
+            // (c23, c24: bit-identical to the sequential loop)
+            const bool exact = f_last < (1ull << 53);
+            bool stopped = false;
+            while (done_it < m_run && !stopped) {
+              const uint32_t cnt = min(32u, m_run - done_it);
+              double cj = 0.0;
+              if ((uint32_t)lane < cnt) {
+                const uint64_t jj = done_it + (uint32_t)lane;
+                const uint64_t S_j = (uint64_t)m.S + (uint64_t)B * jj;
+                const double xc = exact ? (double)(K0 + K1 * S_j) : __ull2double_rn(K0 + K1 * S_j);
+                const double xp = __ull2double_rn((uint64_t)B * (smax0 + jj));
+                const double xs = __ull2double_rn(S_j);
+                cj = __dadd_rn(__dadd_rn(__fma_rn(ac, xc, bc), __fma_rn(ap, xp, bp)), __fma_rn(as_, xs, bs_));
+              }
+              W.cbuf[lane] = cj;
+              const bool mono = __all_sync(FULL, !(cj < 0.0));
+              __syncwarp();
+              double acc = t;
+#pragma unroll 8
+              for (uint32_t q2 = 0; q2 < cnt; ++q2) acc = __dadd_rn(acc, W.cbuf[q2]);
+              if (mono && acc < stop_t) {
+                t = acc;
+                done_it += cnt;
+              } else {   // the chunk reaches stop_t (or costs are not monotone): step and check
+                acc = t;
+                uint32_t q2 = 0;
+                do {
+                  acc = __dadd_rn(acc, W.cbuf[q2]);
+                  ++q2;
+                } while (q2 < cnt && acc < stop_t);
+                t = acc;
+                done_it += q2;
+                stopped = acc >= stop_t;
+              }
+              __syncwarp();
+            }
+          } else if (f_last < (1ull << 53)) {
             // every x of the run is an integer below 2^53: exact fp64 increments == RN conversions
             double xc = (double)(K0 + K1 * (uint64_t)m.S);
             const double dxc = (double)(K1 * B), dB = (double)B;
@@ -679,6 +746,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
           m.S += B2;
           m.d += 1;
           m.needidx = m.needidx == 0 ? bs.v - 1 : m.needidx - 1;
+        }
         }
         if (m.d == m.next_fin) {
           // ---- retire the finishers (ballot / REDUX) ----
