@@ -157,7 +157,11 @@ __device__ const uint64_t* warp_radix_sort(uint64_t* ka, uint32_t* ia, uint64_t*
 
 // ---------------------------------------------------------------------------------------------
 template <bool POW2>
+#ifdef SAMU_K2_MINB   // occupancy experiments only: the default (122 registers, 2 blocks / SM) is fastest
+__global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_simulate(SimLaunch P) {
+#else
 __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunch P) {
+#endif
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpSm& W = reinterpret_cast<WarpSm*>(smem_raw)[warp];
@@ -350,7 +354,8 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
     m.maxO = __reduce_max_sync(FULL, lmaxo);
     // window: register cache of the first wn (<= 32) entries of W (lane i = position i):
     // request, prompt tokens p = l_in + g, tokens still to generate incl. the prefill's (L - g)
-    uint32_t w_r = 0, w_p = 0, w_rem = 0, wn = 0;
+    // (raw loads kept unconsumed until needed: the window refill does not wait on them)
+    uint32_t w_r = 0, w_li = 0, w_lo = 0, w_g = 0, wn = 0;
 
     // ---- main loop (c25) ----
     while (!m.err) {
@@ -384,14 +389,15 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
               g = qp < m.n_front ? (uint32_t)gst[r] : 0u;   // recompute front keeps its tokens
             }
             w_r = r;
-            w_p = (uint32_t)li[r] + g;
-            w_rem = max((uint32_t)lo[r], 1u) - g;
+            w_li = li[r];
+            w_lo = lo[r];
+            w_g = g;
           }
           wn = want;
         }
       }
       // does the head of W fit? (slots, token budget, blocks)
-      const uint32_t hp = __shfl_sync(FULL, w_p, 0);
+      const uint32_t hp = __shfl_sync(FULL, w_li + w_g, 0);
       const bool fits = wlen > 0 && m.B < ms && hp <= C.budget && (int32_t)bs.cdiv(hp) <= m.F;
       uint32_t n_fin = 0;
       if (fits) {
@@ -400,7 +406,8 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
         int32_t blk = 0, freed = 0;
         for (;;) {
           const bool valid = (uint32_t)lane < wn;
-          const uint32_t p = valid ? w_p : 0u;
+          const uint32_t p = valid ? w_li + w_g : 0u;
+          const uint32_t w_rem = max(w_lo, 1u) - w_g;   // tokens still to generate incl. the prefill's
           const uint32_t nb = valid ? bs.cdiv(p) : 0u;
           uint32_t sp, sb, mm;
           if (min(wn, ms - m.B - k_adm) <= 1u) {
@@ -498,8 +505,9 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
           m.q_head += mm - take;
           // shift the window by mm and refill it
           w_r = __shfl_down_sync(FULL, w_r, mm == 32 ? 0 : mm);
-          w_p = __shfl_down_sync(FULL, w_p, mm == 32 ? 0 : mm);
-          w_rem = __shfl_down_sync(FULL, w_rem, mm == 32 ? 0 : mm);
+          w_li = __shfl_down_sync(FULL, w_li, mm == 32 ? 0 : mm);
+          w_lo = __shfl_down_sync(FULL, w_lo, mm == 32 ? 0 : mm);
+          w_g = __shfl_down_sync(FULL, w_g, mm == 32 ? 0 : mm);
           wn -= mm;
           const uint32_t wl2 = m.stack_cnt + (m.q_tail - m.q_head);
           const uint32_t want = min(32u, wl2);
@@ -513,8 +521,9 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
                 g = qp < m.n_front ? (uint32_t)gst[r] : 0u;
               }
               w_r = r;
-              w_p = (uint32_t)li[r] + g;
-              w_rem = max((uint32_t)lo[r], 1u) - g;
+              w_li = li[r];
+              w_lo = lo[r];
+              w_g = g;
             }
             wn = want;
           }
@@ -719,10 +728,10 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunc
             // the victim is the new front of W: shift the window up by one
             {
               const uint32_t Lv = max((uint32_t)lo[vr], 1u);
-              const uint32_t pr = __shfl_up_sync(FULL, w_r, 1), pp = __shfl_up_sync(FULL, w_p, 1),
-                             pm = __shfl_up_sync(FULL, w_rem, 1);
-              if (lane == 0) { w_r = vr; w_p = l; w_rem = Lv - vg; }
-              else { w_r = pr; w_p = pp; w_rem = pm; }
+              const uint32_t pr = __shfl_up_sync(FULL, w_r, 1), pa = __shfl_up_sync(FULL, w_li, 1),
+                             pl = __shfl_up_sync(FULL, w_lo, 1), pg = __shfl_up_sync(FULL, w_g, 1);
+              if (lane == 0) { w_r = vr; w_li = l - vg; w_lo = Lv; w_g = vg; }
+              else { w_r = pr; w_li = pa; w_lo = pl; w_g = pg; }
               wn = min(wn + 1, 32u);
             }
             m.stack_cnt += 1;
