@@ -157,11 +157,13 @@ __device__ const uint64_t* warp_radix_sort(uint64_t* ka, uint32_t* ia, uint64_t*
 
 // ---------------------------------------------------------------------------------------------
 template <bool POW2>
-#ifdef SAMU_K2_MINB   // occupancy experiments only: the default (122 registers, 2 blocks / SM) is fastest
-__global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_simulate(SimLaunch P) {
-#else
-__global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK) k_simulate(SimLaunch P) {
+// Occupancy (profiles/r1_k2_v6_ncu.md): 5 blocks of 4 warps per SM caps registers at 96 (a
+// 28-byte spill) for 20 resident warps: 3-4 % faster than 2 x 8 warps at 122 registers; 24
+// warps (80 registers, 208-byte spill) and 8 warps are slower.  SAMU_DEFINES overrides both.
+#ifndef SAMU_K2_MINB
+#define SAMU_K2_MINB 5
 #endif
+__global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_simulate(SimLaunch P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpSm& W = reinterpret_cast<WarpSm*>(smem_raw)[warp];

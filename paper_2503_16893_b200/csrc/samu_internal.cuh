@@ -7,7 +7,9 @@
 #include "../../include/samu.h"
 
 #define SAMU_EMPTY 0xFFFFFFFFu
-#define SAMU_WARPS_PER_BLOCK 8
+#ifndef SAMU_WARPS_PER_BLOCK
+#define SAMU_WARPS_PER_BLOCK 4   // K2 block = 4 warps; 5 blocks / SM (96 registers): 20 warps per SM
+#endif
 
 // ------------------------------------------------------------------------------------------
 // Application tables on the device (uploaded by samu_app_load)
