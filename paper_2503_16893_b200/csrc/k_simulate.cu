@@ -19,6 +19,21 @@
 
 #include <math_constants.h>
 
+#ifdef SAMU_K2_STATS   // debug build only: event counters (scripts/k2_stats.py)
+__device__ unsigned long long g_k2_stats[16];
+#define K2STAT(i, v) do { if (lane == 0) atomicAdd(&g_k2_stats[i], (unsigned long long)(v)); } while (0)
+extern "C" int samu_debug_k2_stats(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, g_k2_stats, sizeof(g_k2_stats)) != cudaSuccess) return -1;
+  if (reset) {
+    unsigned long long z[16] = {0};
+    if (cudaMemcpyToSymbol(g_k2_stats, z, sizeof(z)) != cudaSuccess) return -1;
+  }
+  return 0;
+}
+#else
+#define K2STAT(i, v) do { } while (0)
+#endif
+
 namespace {
 
 constexpr uint32_t FULL = 0xFFFFFFFFu;
@@ -359,8 +374,10 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
     // (raw loads kept unconsumed until needed: the window refill does not wait on them)
     uint32_t w_r = 0, w_li = 0, w_lo = 0, w_g = 0, wn = 0;
 
+    K2STAT(0, 1);
     // ---- main loop (c25) ----
     while (!m.err) {
+      K2STAT(1, 1);
       if (m.t >= m.tau) { cut = true; break; }
       // pending cross-node arrivals with ready <= t join the back of W
       while (m.pend_ptr < m.n_pend && m.next_ready <= m.t) {
@@ -412,6 +429,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           const uint32_t w_rem = max(w_lo, 1u) - w_g;   // tokens still to generate incl. the prefill's
           const uint32_t nb = valid ? bs.cdiv(p) : 0u;
           uint32_t sp, sb, mm;
+          K2STAT(4, 1);
           if (min(wn, ms - m.B - k_adm) <= 1u) {
             // at most the head can enter (one free slot or one waiting request): no scans
             sp = p;
@@ -419,6 +437,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
             const uint32_t p0 = __shfl_sync(FULL, p, 0);
             mm = (wn > 0 && m.B + k_adm < ms && tok + p0 <= C.budget && (int32_t)(blk + bs.cdiv(p0)) <= m.F) ? 1u : 0u;
           } else {
+            K2STAT(5, 1);
             sp = warp_incl_scan(p, lane);
             sb = warp_incl_scan(nb, lane);
             const bool ok = valid && (m.B + k_adm + lane + 1 <= ms) && (tok + sp <= C.budget) &&
@@ -532,6 +551,8 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           if (mm < 32) break;
         }
         m.F -= blk;
+        K2STAT(2, 1);
+        K2STAT(3, k_adm);
         // Eq. prefill FLOPs: L (c B s + 2 B h s^2 / tp)
         const uint64_t Bp = k_adm, sp64 = smaxp;
         const uint64_t fl = LC * Bp * sp64 + (uint64_t)C.L * 2ull * Bp * C.h_tp * sp64 * sp64;
@@ -553,6 +574,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
         // ================= decode run (c9): uniform iterations until an event ===============
         const uint32_t need1 = W.hist[m.needidx];
         if (m.next_fin == m.d + 1 && (int32_t)need1 <= m.F) {
+          K2STAT(6, 1);
           // one decode that retires requests and needs no preemption: the run below with
           // m_run = 1, without its search and closed forms (same arithmetic)
           const uint32_t B1 = m.B;
@@ -567,6 +589,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           m.d += 1;
           m.needidx = m.needidx == 0 ? bs.v - 1 : m.needidx - 1;
         } else {
+        K2STAT(7, 1);
         const uint32_t B = m.B;
         const double stop_t = fmin(m.tau, m.next_ready);
         // KV need of the run's decodes: histogram rotated to start at needidx, prefix sums
@@ -664,6 +687,8 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
             done_it = jj;
           }
           m.t = t;
+          K2STAT(8, done_it);
+          if (m_run > 4) K2STAT(14, 1);
           // closed-form exact updates for the done_it iterations of the run
           const uint64_t mm = done_it;
           // sum_j (K0 + K1 (S + B j)) = mm K0 + K1 (mm S + B mm (mm - 1) / 2)
@@ -737,6 +762,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
               wn = min(wn + 1, 32u);
             }
             m.stack_cnt += 1;
+            K2STAT(9, 1);
             m.B -= 1;
             m.S -= l;
             if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; m.site = 10; break; }
@@ -745,6 +771,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           m.next_fin = __reduce_min_sync(FULL, lminf);
           m.maxO = __reduce_max_sync(FULL, lmaxo);
           // the preempting decode iteration itself
+          K2STAT(10, 1);
           const uint32_t B2 = m.B;
           const uint32_t smax = (uint32_t)((int32_t)m.d + m.maxO);
           m.F -= (int32_t)need;
@@ -763,6 +790,8 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           // ---- retire the finishers (ballot / REDUX) ----
           const uint32_t inv = __ballot_sync(FULL, lminf == m.d);
           const uint32_t ninv = __popc(inv);
+          K2STAT(11, 1);
+          if (ninv <= 4) K2STAT(13, 1);
           uint32_t cnt_l = 0, sfin_l = 0;
           int32_t fr_l = 0;
           if (ninv <= 4) {
@@ -833,6 +862,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
             }
           }
           n_fin = __reduce_add_sync(FULL, cnt_l);
+          K2STAT(12, n_fin);
           m.F += (int32_t)__reduce_add_sync(FULL, (uint32_t)fr_l);
           m.S -= __reduce_add_sync(FULL, sfin_l);
           m.B -= n_fin;
