@@ -121,20 +121,40 @@ def test_simulate_bit_exact_time_limits():
     assert np.all(g["flags"] & 2)
 
 
-@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("seed", range(12))
 def test_simulate_fuzz_tight_kv_preemption(seed):
-    # random small workloads with few KV blocks: preemption, token budget and slot limits
+    # random small workloads with few KV blocks: preemption, token budget and slot limits; block
+    # sizes cover the power-of-two and the general kernel instantiation
     rng = np.random.default_rng(100 + seed)
     n = int(rng.integers(5, 120))
     lin = rng.integers(1, 60, n)
     lout = rng.integers(0, 80, n)
     eng = F.engine(kv_cap=int(rng.integers(9, 40)) * 16, min_batched_tokens=int(rng.integers(144, 400)),
-                   max_num_seqs=int(rng.integers(1, 40)), block_size=int(rng.choice([4, 8, 16, 7])), n_gpus=4)
+                   max_num_seqs=int(rng.integers(1, 40)), block_size=[4, 8, 16, 7, 12, 1][seed % 6], n_gpus=4)
     cf = np.zeros((W.N_TP_SLOTS, 3, 2, F.NB))
     cf[:, :, :, :] = rng.uniform(1e-4, 1e-2, (W.N_TP_SLOTS, 3, 2, F.NB))
     cf[:, 0, 0, :] = 1e-12
     w = F.tiny(lin, lout, sp=F.spec(l_max=140, tp_values=(1, 2), L=2, h=16, c=1000), eng=eng, cf=cf, n_trials=2)
     _sim_parity(w, [(0, 1, 1), (0, 2, 1), (0, 1, 2), (0, 3, 1)], 2)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_simulate_fuzz_signed_costs_and_cuts(seed):
+    # long decode runs (32-iteration cost chunks) with signed cost terms (non-monotone clock)
+    # and time limits falling inside chunks: the chunk's stop test must match the sequential loop
+    rng = np.random.default_rng(300 + seed)
+    n = int(rng.integers(20, 200))
+    lin = rng.integers(1, 30, n)
+    lout = rng.integers(40, 400, n)
+    eng = F.engine(max_num_seqs=int(rng.integers(4, 64)), block_size=16, n_gpus=2)
+    cf = rng.uniform(1e-4, 1e-2, (W.N_TP_SLOTS, 3, 2, F.NB))
+    cf[:, 0, 0, :] = 1e-12
+    cf[:, 1, 1, :] = -rng.uniform(0, 4e-3, (W.N_TP_SLOTS, F.NB))   # negative prep constant
+    w = F.tiny(lin, lout, sp=F.spec(l_max=512, tp_values=(1, 2), L=2, h=16, c=1000), eng=eng, cf=cf, n_trials=3)
+    cands = [(0, 1, 1), (0, 2, 1), (0, 1, 2)]
+    _sim_parity(w, cands, 3)
+    tau = rng.uniform(0.05, 2.0, (len(cands), 3))
+    _sim_parity(w, cands, 3, tau=tau)
 
 
 def test_hand_traces_on_gpu():
