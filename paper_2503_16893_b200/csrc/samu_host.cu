@@ -8,6 +8,7 @@
 #include <mutex>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -204,6 +205,9 @@ static inline cudaError_t samu_count(samu_ctx* c, cudaError_t e) {
   return e;
 }
 
+// records and status go through the collectives (several ranks, or the one-rank NCCL test hook)
+static inline bool sharded(const samu_ctx* c) { return c->world > 1 || c->comm != nullptr; }
+
 template <class T>
 static cudaError_t upload(DevBuf& b, const std::vector<T>& v, cudaStream_t s) {
   cudaError_t e = b.ensure(sizeof(T) * v.size());
@@ -273,6 +277,14 @@ extern "C" samu_status samu_ctx_create(samu_ctx** out, int32_t cuda_device, void
     ncclUniqueId id;
     std::memcpy(id.internal, nccl_unique_id, 128);
     if (ncclCommInitRank(&c->comm, world, id, rank) != ncclSuccess) { delete c; return SAMU_E_NCCL; }
+  } else if (std::getenv("SAMU_FORCE_NCCL")) {
+    // test hook: a one-rank NCCL communicator, so the sharded code path and its NCCL calls run
+    // on a single GPU (NCCL refuses two ranks on one device)
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess || ncclCommInitRank(&c->comm, 1, id, 0) != ncclSuccess) {
+      delete c;
+      return SAMU_E_NCCL;
+    }
   }
   *out = c;
   return SAMU_OK;
@@ -746,7 +758,7 @@ static samu_status gather_records(samu_ctx* c, const samu_trial_rec* local, int 
                                   const std::vector<int>& slots) {
   cudaStream_t s = c->stream;
   if (n == 0) return SAMU_OK;
-  if (c->world == 1) {
+  if (!sharded(c)) {
     for (int x = 0; x < n; ++x)
       if (dst + (size_t)slots[x] * T != local + (size_t)x * T)
         CK(c, cudaMemcpyAsync(dst + (size_t)slots[x] * T, local + (size_t)x * T, sizeof(samu_trial_rec) * T,
@@ -840,7 +852,7 @@ extern "C" samu_status samu_simulate_batch(samu_ctx* c, const samu_candidate* ca
   if (out_summary && n_cands) {
     int T_total = n_trials;
     const samu_trial_rec* all = out_recs;
-    if (c->world > 1) {
+    if (sharded(c)) {
       // every rank holds n_trials local trials; the world total is their sum
       int32_t Tl = n_trials, Tsum = 0;
       DevBuf tmp;
@@ -1003,7 +1015,7 @@ struct Greedy {
     // the cache may have been reallocated after tau_rec pointers were taken: re-point them
     CK(c, local_rec.ensure(sizeof(samu_trial_rec) * pending.size() * std::max(Tl, 1)));
     for (size_t x = 0; x < pending.size(); ++x) {
-      pending[x].out_rec = (c->world == 1) ? rec(pending_slots[x]) : local_rec.as<samu_trial_rec>() + x * Tl;
+      pending[x].out_rec = !sharded(c) ? rec(pending_slots[x]) : local_rec.as<samu_trial_rec>() + x * Tl;
       pending[x].tau_rec = pending_tau[x] >= 0 ? rec(pending_tau[x]) + tb : nullptr;
       if (pending[x].fin_t_out) {
         std::vector<double> inf((size_t)Tl * n, std::numeric_limits<double>::infinity());
@@ -1012,7 +1024,7 @@ struct Greedy {
       }
     }
     RET(run_jobs(c, pending, lo.as<uint16_t>(), li.as<uint16_t>(), Tl, S));
-    if (c->world > 1) RET(gather_records(c, local_rec.as<samu_trial_rec>(), (int)pending.size(), T, cache.as<samu_trial_rec>(), pending_slots));
+    if (sharded(c)) RET(gather_records(c, local_rec.as<samu_trial_rec>(), (int)pending.size(), T, cache.as<samu_trial_rec>(), pending_slots));
     pending.clear();
     pending_slots.clear();
     pending_tau.clear();
@@ -1355,7 +1367,7 @@ struct Greedy {
       for (int v = 0; v < c->n_nodes; ++v)
         for (int k = 0; k < Tl; ++k) flag[v] |= h[(size_t)v * Tl + k];
     }
-    if (c->world > 1) {
+    if (sharded(c)) {
       CK(c, cudaMemcpyAsync(red, flag.data(), sizeof(int32_t) * c->n_nodes, cudaMemcpyHostToDevice, s));
       RET(comm_allreduce_i32(c, red, red + SAMU_MAX_NODES, c->n_nodes, 0));
       CK(c, cudaMemcpyAsync(flag.data(), red + SAMU_MAX_NODES, sizeof(int32_t) * c->n_nodes, cudaMemcpyDeviceToHost, s));

@@ -545,3 +545,48 @@ def test_local_ranks_sharded_summary_identical():
 
     for summ in _run_ranks(2, fn):
         assert summ == ref
+
+
+# ------------------------------------------------------------------------------------------
+# the NCCL code path on one GPU: a one-rank communicator (SAMU_FORCE_NCCL) routes records and
+# node status through ncclAllGather / ncclAllReduce exactly as a multi-GPU run does
+# ------------------------------------------------------------------------------------------
+_NCCL_CHILD = r"""
+import os, sys, json
+sys.path.insert(0, os.environ["SAMU_ROOT"])
+import numpy as np, torch
+import samu_workloads as W
+from paper_2503_16893_b200 import Samu
+w = W.make_workload("c2", n_prompts=120, n_trials=3)
+S = Samu(0); S.load_workload(w)
+plan = S.samu_plan_greedy(16893, 3)
+lo, li = S.samu_sample_lengths(16893, 0, 3)
+out = S.samu_simulate_batch([(0, 1, 1), (2, 2, 2)], lo, li, summary=True)
+print(json.dumps(dict(plan=[(s["entries"], s["fstar"], s["mean_tE"], s["T_E"]) for s in plan["stages"]],
+                      total=plan["total"], summary=[float(x["mean_t"]) for x in out["summary"]])))
+"""
+
+
+def test_nccl_path_one_rank_matches_oracle():
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SAMU_FORCE_NCCL="1", SAMU_ROOT=root)
+    r = subprocess.run([sys.executable, "-c", _NCCL_CHILD], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = json.loads(r.stdout.strip().splitlines()[-1])
+    w = W.make_workload("c2", n_prompts=120, n_trials=3)
+    P = O.Problem(w)
+    ref = P.plan_greedy(SEED, 3)
+    assert got["total"] == ref["total"]
+    assert [(tuple(map(tuple, e)), f, m, t) for e, f, m, t in got["plan"]] == \
+        [(tuple(s["entries"]), s["fstar"], s["mean_tE"], s["T_E"]) for s in ref["stages"]]
+    lo, li = P.sample(SEED, 0, 3)
+    for (node, dp, tp), mean in zip([(0, 1, 1), (2, 2, 2)], got["summary"]):
+        rec, _, _ = P.simulate(node, dp, tp, lo, li)
+        s = 0.0
+        for x in rec["t_end"]:
+            s += float(x)
+        assert mean == s / 3
