@@ -635,6 +635,41 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
                 const double xs = __ull2double_rn(S_j);
                 cj = __dadd_rn(__dadd_rn(__fma_rn(ac, xc, bc), __fma_rn(ap, xp, bp)), __fma_rn(as_, xs, bs_));
               }
+              // Exact parallel form of the sequential sum (same doubles as the one-by-one adds):
+              // while every partial sum stays in t's binade [2^e, 2^(e+1)) (ulp u), each add
+              // RN(acc + c) = acc + round_u(c), where round_u(c) = RN(t + c) - t (exact), unless c
+              // sits exactly half-way between multiples of u (a tie, whose even-rounding depends
+              // on acc): the partial sums are then t + prefix sums of the round_u(c), all
+              // multiples of u below 2^(e+1), hence exact in any order (a warp scan).  Chunks with
+              // a negative cost, a tie or a binade crossing take the sequential walk below.
+              {
+                const uint64_t eb = (uint64_t)__double_as_longlong(t) & 0x7FF0000000000000ull;
+                const bool tok = t > 0.0 && eb >= (64ull << 52) && eb < (0x7F0ull << 52);
+                if (tok) {
+                  const double s = __dadd_rn(t, cj);
+                  const double r = __dsub_rn(s, t);
+                  const double err = __dsub_rn(cj, r);   // exact (Fast2Sum, t >= c when in binade)
+                  const double halfu = __longlong_as_double((long long)(eb - (53ull << 52)));
+                  const double top = __longlong_as_double((long long)(eb + (1ull << 52)));   // 2^(e+1)
+                  double pre = r;
+#pragma unroll
+                  for (int o = 1; o < 32; o <<= 1) {
+                    const double nb2 = __shfl_up_sync(FULL, pre, o);
+                    if (lane >= o) pre = __dadd_rn(pre, nb2);
+                  }
+                  const double acc_j = __dadd_rn(t, pre);   // partial sum after iteration lane
+                  const bool in = (uint32_t)lane < cnt;
+                  const uint32_t bstop = __ballot_sync(FULL, in && !(acc_j < stop_t));
+                  const uint32_t upto = bstop ? (uint32_t)(__ffs(bstop) - 1) : cnt - 1;   // last lane used
+                  const bool bad = (uint32_t)lane <= upto && (cj < 0.0 || fabs(err) == halfu || !(acc_j < top));
+                  if (!__any_sync(FULL, bad)) {
+                    t = __shfl_sync(FULL, acc_j, upto);
+                    done_it += upto + 1;
+                    stopped = bstop != 0;
+                    continue;
+                  }
+                }
+              }
               W.cbuf[lane] = cj;
               const bool mono = __all_sync(FULL, !(cj < 0.0));
               __syncwarp();
