@@ -19,6 +19,8 @@
 
 #include <math_constants.h>
 
+#include <mutex>
+
 #ifdef SAMU_K2_STATS   // debug build only: event counters (scripts/k2_stats.py)
 __device__ unsigned long long g_k2_stats[16];
 #define K2STAT(i, v) do { if (lane == 0) atomicAdd(&g_k2_stats[i], (unsigned long long)(v)); } while (0)
@@ -108,7 +110,7 @@ __device__ __forceinline__ void set_error(int32_t* e, int32_t code, int32_t site
 
 struct Sim {
   // warp-uniform scalar state
-  double t, tau, next_ready;
+  double t, tau, next_ready, stop;   // stop = min(tau, next_ready)
   uint64_t fl_lo, fl_hi, reqit;
   uint32_t iter, d, needidx, B, S, next_fin, next_rank;
   int32_t F, maxO;
@@ -171,7 +173,13 @@ __device__ const uint64_t* warp_radix_sort(uint64_t* ka, uint32_t* ia, uint64_t*
 }  // namespace
 
 // ---------------------------------------------------------------------------------------------
-template <bool POW2>
+// Candidate descriptors of a launch with <= SAMU_K2_CONST_CANDS candidates live in the constant
+// bank: a field read is one register-indexed LDC (warp-uniform index) instead of an address
+// rebuild + L1 load each time register pressure forces the compiler to re-read it.
+#define SAMU_K2_CONST_CANDS 400
+__constant__ DevCand c_cands[SAMU_K2_CONST_CANDS];
+
+template <bool POW2, bool CONSTC>
 // Occupancy (profiles/r1_k2_v6_ncu.md): 5 blocks of 4 warps per SM caps registers at 96 (a
 // 28-byte spill) for 20 resident warps: 3-4 % faster than 2 x 8 warps at 122 registers; 24
 // warps (80 registers, 208-byte spill) and 8 warps are slower.  SAMU_DEFINES overrides both.
@@ -196,7 +204,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
     if (item >= (uint32_t)P.n_items) break;
     const uint2 it = P.items[item];
     const uint32_t ci = it.x, k = it.y >> 4, j = it.y & 15u;
-    const DevCand& C = P.cands[ci];
+    const DevCand& C = CONSTC ? c_cands[ci] : P.cands[ci];
     const size_t tb = (size_t)k * n;
     const uint16_t* __restrict__ lo = P.l_out + tb;
     const uint16_t* __restrict__ li = P.l_in + tb;
@@ -353,6 +361,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
       pi = si;
     }
     m.next_ready = m.n_pend ? kdouble(pk[0]) : CUDART_INF;
+    m.stop = fmin(m.tau, m.next_ready);
     const uint64_t K1 = 2ull * C.L * C.h_tp;
     const uint64_t LC = (uint64_t)C.L * C.c;
     const bool need_rel = fio || fto || commit || C.has_succ;
@@ -378,17 +387,20 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
     // ---- main loop (c25) ----
     while (!m.err) {
       K2STAT(1, 1);
-      if (m.t >= m.tau) { cut = true; break; }
-      // pending cross-node arrivals with ready <= t join the back of W
-      while (m.pend_ptr < m.n_pend && m.next_ready <= m.t) {
-        const uint32_t i = m.pend_ptr + lane;
-        const bool ok = i < m.n_pend && kdouble(pk[i]) <= m.t;
-        const uint32_t b = __ballot_sync(FULL, ok);
-        const uint32_t cnt = (b == FULL) ? 32u : (uint32_t)(__ffs(~b) - 1);
-        if ((uint32_t)lane < cnt) q[m.q_tail + lane] = pi[i];
-        m.q_tail += cnt;
-        m.pend_ptr += cnt;
-        m.next_ready = m.pend_ptr < m.n_pend ? kdouble(pk[m.pend_ptr]) : CUDART_INF;
+      if (m.t >= m.stop) {   // stop time or a pending arrival reached
+        if (m.t >= m.tau) { cut = true; break; }
+        // pending cross-node arrivals with ready <= t join the back of W
+        while (m.pend_ptr < m.n_pend && m.next_ready <= m.t) {
+          const uint32_t i = m.pend_ptr + lane;
+          const bool ok = i < m.n_pend && kdouble(pk[i]) <= m.t;
+          const uint32_t b = __ballot_sync(FULL, ok);
+          const uint32_t cnt = (b == FULL) ? 32u : (uint32_t)(__ffs(~b) - 1);
+          if ((uint32_t)lane < cnt) q[m.q_tail + lane] = pi[i];
+          m.q_tail += cnt;
+          m.pend_ptr += cnt;
+          m.next_ready = m.pend_ptr < m.n_pend ? kdouble(pk[m.pend_ptr]) : CUDART_INF;
+        }
+        m.stop = fmin(m.tau, m.next_ready);
       }
       const uint32_t wlen = m.stack_cnt + (m.q_tail - m.q_head);
       if (m.B == 0 && wlen == 0) {
@@ -428,9 +440,16 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           const uint32_t p = valid ? w_li + w_g : 0u;
           const uint32_t w_rem = max(w_lo, 1u) - w_g;   // tokens still to generate incl. the prefill's
           const uint32_t nb = valid ? bs.cdiv(p) : 0u;
-          uint32_t sp, sb, mm;
+          uint32_t sp, sb, mm;   // admitted totals: sp / sb at lane mm - 1
           K2STAT(4, 1);
-          if (min(wn, ms - m.B - k_adm) <= 1u) {
+          const uint32_t slots = min(wn, ms - m.B - k_adm);
+          const uint32_t tot_p = __reduce_add_sync(FULL, p), tot_b = __reduce_add_sync(FULL, nb);
+          if (tot_p + tok <= C.budget && (int32_t)(tot_b + blk) <= m.F) {
+            // the whole window fits the token and block budgets: only the slots bind, no scans
+            mm = slots;
+            sp = __reduce_add_sync(FULL, (uint32_t)lane < mm ? p : 0u);   // uniform totals
+            sb = __reduce_add_sync(FULL, (uint32_t)lane < mm ? nb : 0u);
+          } else if (slots <= 1u) {
             // at most the head can enter (one free slot or one waiting request): no scans
             sp = p;
             sb = nb;
@@ -555,7 +574,8 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
         K2STAT(3, k_adm);
         // Eq. prefill FLOPs: L (c B s + 2 B h s^2 / tp)
         const uint64_t Bp = k_adm, sp64 = smaxp;
-        const uint64_t fl = LC * Bp * sp64 + (uint64_t)C.L * 2ull * Bp * C.h_tp * sp64 * sp64;
+        // = B s (L c + 2 L (h/tp) s): the same integer, fewer 64-bit products
+        const uint64_t fl = (Bp * sp64) * (LC + K1 * sp64);
         const double lat = iter_cost(C.coef, ms, k_adm, fl, k_adm * smaxp, tok);
         m.t = __dadd_rn(m.t, lat);
         add_flops(m, fl);
@@ -591,7 +611,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
         } else {
         K2STAT(7, 1);
         const uint32_t B = m.B;
-        const double stop_t = fmin(m.tau, m.next_ready);
+        const double stop_t = m.stop;
         // KV need of the run's decodes: histogram rotated to start at needidx, prefix sums
         const uint32_t hv = (uint32_t)lane < bs.v ? W.hist[bs.mod(m.needidx + bs.v - (uint32_t)lane)] : 0u;
         const uint32_t pre = warp_incl_scan(hv, lane);
@@ -993,22 +1013,51 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
 
 int32_t simulate_smem_bytes() { return (int32_t)(sizeof(WarpSm) * SAMU_WARPS_PER_BLOCK); }
 
-cudaError_t simulate_prepare(int* blocks_per_sm) {
-  const int smem = simulate_smem_bytes();
-  cudaError_t e = cudaFuncSetAttribute(k_simulate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+template <bool POW2, bool CONSTC>
+static cudaError_t prepare_one(int smem, int* bpsm) {
+  cudaError_t e = cudaFuncSetAttribute(k_simulate<POW2, CONSTC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_simulate<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  int a = 0, b = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_simulate<true>, 32 * SAMU_WARPS_PER_BLOCK, smem);
-  if (e != cudaSuccess) return e;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_simulate<false>, 32 * SAMU_WARPS_PER_BLOCK, smem);
-  *blocks_per_sm = a < b ? a : b;
+  int a = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_simulate<POW2, CONSTC>, 32 * SAMU_WARPS_PER_BLOCK, smem);
+  *bpsm = *bpsm < a ? *bpsm : a;
   return e;
 }
 
-cudaError_t launch_simulate(const SimLaunch& L, int32_t n_blocks, bool pow2_block, cudaStream_t s) {
-  if (pow2_block) k_simulate<true><<<n_blocks, 32 * SAMU_WARPS_PER_BLOCK, simulate_smem_bytes(), s>>>(L);
-  else k_simulate<false><<<n_blocks, 32 * SAMU_WARPS_PER_BLOCK, simulate_smem_bytes(), s>>>(L);
+cudaError_t simulate_prepare(int* blocks_per_sm) {
+  const int smem = simulate_smem_bytes();
+  *blocks_per_sm = 1 << 30;
+  cudaError_t e;
+  if ((e = prepare_one<true, true>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<true, false>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<false, true>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  return prepare_one<false, false>(smem, blocks_per_sm);
+}
+
+cudaError_t launch_simulate(const SimLaunch& L, const DevCand* host_cands, int32_t n_blocks, bool pow2_block,
+                            cudaStream_t s) {
+  const int smem = simulate_smem_bytes();
+  const dim3 blk(32 * SAMU_WARPS_PER_BLOCK);
+  if (L.n_cands <= SAMU_K2_CONST_CANDS) {
+    // The table is one per device and process while contexts may launch on their own streams:
+    // the copy waits for the previous table user (any stream) and this launch becomes the next.
+    static std::mutex mu;
+    static cudaEvent_t last[64] = {};
+    std::lock_guard<std::mutex> lock(mu);
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!last[dev] && (e = cudaEventCreateWithFlags(&last[dev], cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(s, last[dev], 0)) != cudaSuccess) return e;
+    e = cudaMemcpyToSymbolAsync(c_cands, host_cands, sizeof(DevCand) * (size_t)L.n_cands, 0, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+    if (pow2_block) k_simulate<true, true><<<n_blocks, blk, smem, s>>>(L);
+    else k_simulate<false, true><<<n_blocks, blk, smem, s>>>(L);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    return cudaEventRecord(last[dev], s);
+  } else {
+    if (pow2_block) k_simulate<true, false><<<n_blocks, blk, smem, s>>>(L);
+    else k_simulate<false, false><<<n_blocks, blk, smem, s>>>(L);
+  }
   return cudaGetLastError();
 }

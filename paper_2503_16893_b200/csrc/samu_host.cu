@@ -722,7 +722,7 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
       L.scratch_idx = c->d_scratch_idx.as<uint32_t>();
       L.max_q = (int32_t)max_q;
       L.max_p = (int32_t)max_p;
-      CK(c, launch_simulate(L, n_blocks, pow2, s));
+      CK(c, launch_simulate(L, dc.data(), n_blocks, pow2, s));
     }
     CK(c, launch_combine(L.rep_rec, L.cands, (int32_t)idx.size(), T, S.over, c->n_nodes, s));
     c->launches += 2;

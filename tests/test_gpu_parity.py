@@ -157,6 +157,25 @@ def test_simulate_fuzz_signed_costs_and_cuts(seed):
     _sim_parity(w, cands, 3, tau=tau)
 
 
+def test_candidate_table_both_paths():
+    # launches with <= 400 candidates read them from the constant bank, larger ones from global
+    # memory (k_simulate<., CONSTC>): both must give the oracle's records
+    w = W.make_workload("c2", n_prompts=120, n_trials=2)
+    P = O.Problem(w)
+    S = gpu(w)
+    cands = [(v, dp, tp) for v in range(w.n_nodes) for (dp, tp) in P.plans(w.node_model[v])]
+    lo, li = P.sample(SEED, 0, 2)
+    glo, gli = S.samu_sample_lengths(SEED, 0, 2)
+    small = recs(S.samu_simulate_batch(cands, glo, gli))
+    big = recs(S.samu_simulate_batch(cands * 5, glo, gli))
+    assert len(cands) * 5 > 400
+    for ci, cd in enumerate(cands):
+        o = P.simulate(*cd, lo, li)[0]
+        assert_rec_equal(small[ci], o, f"const table {cd}")
+        for r in range(5):
+            assert_rec_equal(big[ci + r * len(cands)], o, f"global table {cd} copy {r}")
+
+
 def test_hand_traces_on_gpu():
     for kind, expect_t in (("const", 63.0), ("B", 80.0), ("S", 32 + 784 + 1012 + 33 + 979)):
         w = F.tiny([16, 16], [40, 40], sp=F.spec(l_max=64), cf=kind, eng=F.engine(kv_cap=64, min_batched_tokens=64))
