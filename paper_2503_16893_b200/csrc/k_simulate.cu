@@ -79,18 +79,21 @@ __device__ __forceinline__ double kdouble(uint64_t k) {
   return __longlong_as_double((long long)b);
 }
 
-// block-size arithmetic; the kernel is instantiated for power-of-two block sizes (bs = 16 by
-// default, reading c5) and for the general case
-template <bool POW2>
+// block-size arithmetic; the kernel is instantiated for the default block size 16 (reading c5)
+// as a compile-time constant, for other powers of two (BSK = 0) and for the general case (-1)
+template <int BSK>
 struct Bs {
-  uint32_t v, mask, shift;
-  __device__ __forceinline__ uint32_t mod(uint32_t x) const { return POW2 ? (x & mask) : x % v; }
-  __device__ __forceinline__ uint32_t div(uint32_t x) const { return POW2 ? (x >> shift) : x / v; }
-  __device__ __forceinline__ uint32_t cdiv(uint32_t x) const { return div(x + v - 1); }
+  uint32_t v_, mask_, shift_;
+  __device__ __forceinline__ uint32_t v() const { return BSK > 0 ? (uint32_t)BSK : v_; }
+  __device__ __forceinline__ uint32_t mask() const { return BSK > 0 ? (uint32_t)BSK - 1u : mask_; }
+  __device__ __forceinline__ uint32_t shift() const { return BSK > 0 ? (uint32_t)__builtin_ctz(BSK > 0 ? BSK : 1) : shift_; }
+  __device__ __forceinline__ uint32_t mod(uint32_t x) const { return BSK >= 0 ? (x & mask()) : x % v_; }
+  __device__ __forceinline__ uint32_t div(uint32_t x) const { return BSK >= 0 ? (x >> shift()) : x / v_; }
+  __device__ __forceinline__ uint32_t cdiv(uint32_t x) const { return div(x + v() - 1); }
   __device__ __forceinline__ uint32_t posmod(int32_t a) const {
-    if (POW2) return (uint32_t)a & mask;
-    const int32_t r = a % (int32_t)v;
-    return (uint32_t)(r < 0 ? r + (int32_t)v : r);
+    if (BSK >= 0) return (uint32_t)a & mask();
+    const int32_t r = a % (int32_t)v_;
+    return (uint32_t)(r < 0 ? r + (int32_t)v_ : r);
   }
 };
 
@@ -179,7 +182,7 @@ __device__ const uint64_t* warp_radix_sort(uint64_t* ka, uint32_t* ia, uint64_t*
 #define SAMU_K2_CONST_CANDS 400
 __constant__ DevCand c_cands[SAMU_K2_CONST_CANDS];
 
-template <bool POW2, bool CONSTC>
+template <int BSK, bool CONSTC>
 // Occupancy (profiles/r1_k2_v6_ncu.md): 5 blocks of 4 warps per SM caps registers at 96 (a
 // 28-byte spill) for 20 resident warps: 3-4 % faster than 2 x 8 warps at 122 registers; 24
 // warps (80 registers, 208-byte spill) and 8 warps are slower.  SAMU_DEFINES overrides both.
@@ -217,10 +220,10 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
     double* over = P.over ? P.over + ((size_t)k * A.n_nodes + C.node) * 16 : nullptr;
     const uint32_t r0 = C.rep_off[j], r1 = C.rep_off[j + 1];
     const uint32_t ms = C.max_seqs;
-    Bs<POW2> bs;
-    bs.v = C.bs;
-    bs.mask = C.bs - 1;
-    bs.shift = __ffs(C.bs) - 1;
+    Bs<BSK> bs;
+    bs.v_ = C.bs;
+    bs.mask_ = C.bs - 1;
+    bs.shift_ = __ffs(C.bs) - 1;
     const bool commit = C.commit && st;
 
     Sim m;
@@ -607,13 +610,13 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           m.F -= (int32_t)need1;
           m.S += B1;
           m.d += 1;
-          m.needidx = m.needidx == 0 ? bs.v - 1 : m.needidx - 1;
+          m.needidx = m.needidx == 0 ? bs.v() - 1 : m.needidx - 1;
         } else {
         K2STAT(7, 1);
         const uint32_t B = m.B;
         const double stop_t = m.stop;
         // KV need of the run's decodes: histogram rotated to start at needidx, prefix sums
-        const uint32_t hv = (uint32_t)lane < bs.v ? W.hist[bs.mod(m.needidx + bs.v - (uint32_t)lane)] : 0u;
+        const uint32_t hv = (uint32_t)lane < bs.v() ? W.hist[bs.mod(m.needidx + bs.v() - (uint32_t)lane)] : 0u;
         const uint32_t pre = warp_incl_scan(hv, lane);
         const uint32_t m_fin = m.next_fin - m.d;
         uint32_t i_pre = 0x7fffffffu;   // first run iteration that must preempt
@@ -622,8 +625,8 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           // each bs decodes need exactly B blocks: skip the search when the run cannot run out
           if ((uint64_t)F0 < (uint64_t)B * ((uint64_t)bs.div(m_fin) + 1)) {
             const uint32_t q0 = F0 / B, rem = F0 - q0 * B;
-            const uint32_t bad = __ballot_sync(FULL, (uint32_t)lane < bs.v && pre > rem);
-            const uint64_t ip = (uint64_t)q0 * bs.v + (uint32_t)(__ffs(bad) - 1);
+            const uint32_t bad = __ballot_sync(FULL, (uint32_t)lane < bs.v() && pre > rem);
+            const uint64_t ip = (uint64_t)q0 * bs.v() + (uint32_t)(__ffs(bad) - 1);
             i_pre = ip > 0x7fffffffull ? 0x7fffffffu : (uint32_t)ip;
           }
         }
@@ -766,7 +769,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           m.F -= (int32_t)need_sum;
           m.S += B * done_it;
           m.d += done_it;
-          m.needidx = bs.mod(m.needidx + bs.v - rr);
+          m.needidx = bs.mod(m.needidx + bs.v() - rr);
         }
         if (m.d != m.next_fin && done_it == i_pre && !(done_it > 0 && m.t >= stop_t)) {
           // ---- this decode must preempt (c7): recompute the last admitted requests ----
@@ -838,7 +841,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           m.iter += 1;
           m.S += B2;
           m.d += 1;
-          m.needidx = m.needidx == 0 ? bs.v - 1 : m.needidx - 1;
+          m.needidx = m.needidx == 0 ? bs.v() - 1 : m.needidx - 1;
         }
         }
         if (m.d == m.next_fin) {
@@ -1013,12 +1016,12 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
 
 int32_t simulate_smem_bytes() { return (int32_t)(sizeof(WarpSm) * SAMU_WARPS_PER_BLOCK); }
 
-template <bool POW2, bool CONSTC>
+template <int BSK, bool CONSTC>
 static cudaError_t prepare_one(int smem, int* bpsm) {
-  cudaError_t e = cudaFuncSetAttribute(k_simulate<POW2, CONSTC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = cudaFuncSetAttribute(k_simulate<BSK, CONSTC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   int a = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_simulate<POW2, CONSTC>, 32 * SAMU_WARPS_PER_BLOCK, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_simulate<BSK, CONSTC>, 32 * SAMU_WARPS_PER_BLOCK, smem);
   *bpsm = *bpsm < a ? *bpsm : a;
   return e;
 }
@@ -1027,16 +1030,25 @@ cudaError_t simulate_prepare(int* blocks_per_sm) {
   const int smem = simulate_smem_bytes();
   *blocks_per_sm = 1 << 30;
   cudaError_t e;
-  if ((e = prepare_one<true, true>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  if ((e = prepare_one<true, false>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  if ((e = prepare_one<false, true>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  return prepare_one<false, false>(smem, blocks_per_sm);
+  if ((e = prepare_one<16, true>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<16, false>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<0, true>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<0, false>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<-1, true>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  return prepare_one<-1, false>(smem, blocks_per_sm);
 }
 
-cudaError_t launch_simulate(const SimLaunch& L, const DevCand* host_cands, int32_t n_blocks, bool pow2_block,
+template <bool CONSTC>
+static void launch_variant(const SimLaunch& L, uint32_t block_size, int32_t n_blocks, int smem, cudaStream_t s) {
+  const dim3 blk(32 * SAMU_WARPS_PER_BLOCK);
+  if (block_size == 16) k_simulate<16, CONSTC><<<n_blocks, blk, smem, s>>>(L);
+  else if ((block_size & (block_size - 1)) == 0) k_simulate<0, CONSTC><<<n_blocks, blk, smem, s>>>(L);
+  else k_simulate<-1, CONSTC><<<n_blocks, blk, smem, s>>>(L);
+}
+
+cudaError_t launch_simulate(const SimLaunch& L, const DevCand* host_cands, int32_t n_blocks, uint32_t block_size,
                             cudaStream_t s) {
   const int smem = simulate_smem_bytes();
-  const dim3 blk(32 * SAMU_WARPS_PER_BLOCK);
   if (L.n_cands <= SAMU_K2_CONST_CANDS) {
     // The table is one per device and process while contexts may launch on their own streams:
     // the copy waits for the previous table user (any stream) and this launch becomes the next.
@@ -1051,13 +1063,10 @@ cudaError_t launch_simulate(const SimLaunch& L, const DevCand* host_cands, int32
     if ((e = cudaStreamWaitEvent(s, last[dev], 0)) != cudaSuccess) return e;
     e = cudaMemcpyToSymbolAsync(c_cands, host_cands, sizeof(DevCand) * (size_t)L.n_cands, 0, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return e;
-    if (pow2_block) k_simulate<true, true><<<n_blocks, blk, smem, s>>>(L);
-    else k_simulate<false, true><<<n_blocks, blk, smem, s>>>(L);
+    launch_variant<true>(L, block_size, n_blocks, smem, s);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     return cudaEventRecord(last[dev], s);
-  } else {
-    if (pow2_block) k_simulate<true, false><<<n_blocks, blk, smem, s>>>(L);
-    else k_simulate<false, false><<<n_blocks, blk, smem, s>>>(L);
   }
+  launch_variant<false>(L, block_size, n_blocks, smem, s);
   return cudaGetLastError();
 }

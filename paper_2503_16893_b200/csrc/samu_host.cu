@@ -698,7 +698,6 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
     L.fin_t = S.fin_t;
     L.over = S.over;
     L.error = c->d_error.as<int32_t>();
-    const bool pow2 = (c->eng.block_size & (c->eng.block_size - 1)) == 0;
     {
       const int bpsm = c->sim_blocks_per_sm;
       const int64_t warps_needed = (int64_t)items.size();
@@ -722,7 +721,7 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
       L.scratch_idx = c->d_scratch_idx.as<uint32_t>();
       L.max_q = (int32_t)max_q;
       L.max_p = (int32_t)max_p;
-      CK(c, launch_simulate(L, dc.data(), n_blocks, pow2, s));
+      CK(c, launch_simulate(L, dc.data(), n_blocks, (uint32_t)c->eng.block_size, s));
     }
     CK(c, launch_combine(L.rep_rec, L.cands, (int32_t)idx.size(), T, S.over, c->n_nodes, s));
     c->launches += 2;

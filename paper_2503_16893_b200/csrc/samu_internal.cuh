@@ -85,7 +85,7 @@ cudaError_t launch_ecdf_table(const uint32_t* values, const uint32_t* cum, int32
                               cudaStream_t s);
 cudaError_t launch_dense_coeff(const uint32_t* bucket_B, int32_t nb, const double* coeff_slot,
                                uint32_t max_seqs, double* out, cudaStream_t s);
-cudaError_t launch_simulate(const SimLaunch& L, const DevCand* host_cands, int32_t n_blocks, bool pow2_block,
+cudaError_t launch_simulate(const SimLaunch& L, const DevCand* host_cands, int32_t n_blocks, uint32_t block_size,
                             cudaStream_t s);
 cudaError_t simulate_prepare(int* blocks_per_sm);
 
