@@ -155,7 +155,7 @@ __global__ void k_dense_coeff(const uint32_t* __restrict__ bucket_B, int32_t nb,
     const double w = __ddiv_rn((double)(B - (int32_t)bucket_B[k]), (double)(bucket_B[k + 1] - bucket_B[k]));
     r = __dadd_rn(v[k], __dmul_rn(__dsub_rn(v[k + 1], v[k]), w));
   }
-  out[(size_t)pa * max_seqs + (B - 1)] = r;
+  out[(size_t)(B - 1) * 8 + pa] = r;   // [B][a_c b_c a_p b_p a_s b_s pad pad]: 3 x 16-byte loads per B
 }
 
 }  // namespace

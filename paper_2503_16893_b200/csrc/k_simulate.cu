@@ -98,12 +98,13 @@ struct Bs {
 };
 
 // Eq. per-iter cost, reading c24: ((fma_c + fma_p) + fma_s), exact integer -> RN
-__device__ __forceinline__ double iter_cost(const double* __restrict__ coef, uint32_t ms, uint32_t B, uint64_t F,
-                                            uint32_t Bs_, uint32_t S) {
-  const double* cb = coef + (B - 1);
-  const double tc = __fma_rn(__ldg(cb), __ull2double_rn(F), __ldg(cb + ms));
-  const double tp = __fma_rn(__ldg(cb + 2 * ms), __uint2double_rn(Bs_), __ldg(cb + 3 * ms));
-  const double ts = __fma_rn(__ldg(cb + 4 * ms), __uint2double_rn(S), __ldg(cb + 5 * ms));
+__device__ __forceinline__ double iter_cost(const double* __restrict__ coef, uint32_t B, uint64_t F, uint32_t Bs_,
+                                            uint32_t S) {
+  const double2* cb = reinterpret_cast<const double2*>(coef + (size_t)(B - 1) * 8);   // dense [B][8] (c11)
+  const double2 c = __ldg(cb), p = __ldg(cb + 1), q = __ldg(cb + 2);
+  const double tc = __fma_rn(c.x, __ull2double_rn(F), c.y);
+  const double tp = __fma_rn(p.x, __uint2double_rn(Bs_), p.y);
+  const double ts = __fma_rn(q.x, __uint2double_rn(S), q.y);
   return __dadd_rn(__dadd_rn(tc, tp), ts);
 }
 
@@ -114,18 +115,15 @@ __device__ __forceinline__ void set_error(int32_t* e, int32_t code, int32_t site
 struct Sim {
   // warp-uniform scalar state
   double t, tau, next_ready, stop;   // stop = min(tau, next_ready)
-  uint64_t fl_lo, fl_hi, reqit;
+  // FLOPs of the completed iterations = L c * a1 + 2 L (h/tp) * a2 (exact, folded into u128 at
+  // the end): a1 = sum of decode B + prefill B s, a2 = sum of decode S + prefill B s^2
+  uint64_t a1, a2, reqit;
   uint32_t iter, d, needidx, B, S, next_fin, next_rank;
   int32_t F, maxO;
   uint32_t stack_cnt, q_head, q_tail, n_heads, n_front, pend_ptr, n_pend;
   int32_t err, site;
 };
 
-__device__ __forceinline__ void add_flops(Sim& m, uint64_t f) {
-  const uint64_t lo = m.fl_lo + f;
-  m.fl_hi += (lo < m.fl_lo) ? 1ull : 0ull;
-  m.fl_lo = lo;
-}
 
 // Stable LSD radix sort of n (key, idx) pairs by the 64-bit key (8 passes of 8 bits, passes where
 // every key shares the digit are skipped), one warp, 256-bin histogram in shared memory.
@@ -180,6 +178,7 @@ __device__ const uint64_t* warp_radix_sort(uint64_t* ka, uint32_t* ia, uint64_t*
 // bank: a field read is one register-indexed LDC (warp-uniform index) instead of an address
 // rebuild + L1 load each time register pressure forces the compiler to re-read it.
 #define SAMU_K2_CONST_CANDS 400
+static_assert(sizeof(DevCand) * SAMU_K2_CONST_CANDS <= 64 * 1024, "candidate table exceeds the constant bank");
 __constant__ DevCand c_cands[SAMU_K2_CONST_CANDS];
 
 template <int BSK, bool CONSTC>
@@ -229,7 +228,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
     Sim m;
     m.t = C.resume ? (over ? over[j] : 0.0) : C.load_s;
     m.tau = C.tau ? C.tau[k] : (C.tau_rec ? C.tau_rec[k].t_end : CUDART_INF);
-    m.fl_lo = m.fl_hi = m.reqit = 0;
+    m.a1 = m.a2 = m.reqit = 0;
     m.iter = 0; m.d = 0; m.needidx = 0; m.B = 0; m.S = 0; m.next_rank = 0;
     m.F = C.blocks; m.maxO = INT_MIN; m.next_fin = FULL;
     m.stack_cnt = 0; m.q_head = 0; m.q_tail = 0; m.n_heads = 0; m.n_front = 0; m.pend_ptr = 0; m.n_pend = 0;
@@ -365,8 +364,8 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
     }
     m.next_ready = m.n_pend ? kdouble(pk[0]) : CUDART_INF;
     m.stop = fmin(m.tau, m.next_ready);
-    const uint64_t K1 = 2ull * C.L * C.h_tp;
-    const uint64_t LC = (uint64_t)C.L * C.c;
+    const uint64_t K1 = C.K1;   // 2 L (h/tp)
+    const uint64_t LC = C.LC;   // L c
     const bool need_rel = fio || fto || commit || C.has_succ;
     bool cut = false;
     // per-lane summaries of this lane's slots: min finish index, max (l - d)
@@ -578,10 +577,12 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
         // Eq. prefill FLOPs: L (c B s + 2 B h s^2 / tp)
         const uint64_t Bp = k_adm, sp64 = smaxp;
         // = B s (L c + 2 L (h/tp) s): the same integer, fewer 64-bit products
-        const uint64_t fl = (Bp * sp64) * (LC + K1 * sp64);
-        const double lat = iter_cost(C.coef, ms, k_adm, fl, k_adm * smaxp, tok);
+        const uint64_t Bs64 = Bp * sp64;
+        const uint64_t fl = Bs64 * (LC + K1 * sp64);
+        const double lat = iter_cost(C.coef, k_adm, fl, k_adm * smaxp, tok);
         m.t = __dadd_rn(m.t, lat);
-        add_flops(m, fl);
+        m.a1 += Bs64;
+        m.a2 += Bs64 * sp64;
         m.reqit += k_adm;
         m.iter += 1;
         m.F += freed;
@@ -603,8 +604,9 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           const uint32_t B1 = m.B;
           const uint32_t smax = (uint32_t)((int32_t)m.d + m.maxO);
           const uint64_t fl = LC * B1 + K1 * (uint64_t)m.S;
-          m.t = __dadd_rn(m.t, iter_cost(C.coef, ms, B1, fl, B1 * smax, m.S));
-          add_flops(m, fl);
+          m.t = __dadd_rn(m.t, iter_cost(C.coef, B1, fl, B1 * smax, m.S));
+          m.a1 += B1;
+          m.a2 += m.S;
           m.reqit += B1;
           m.iter += 1;
           m.F -= (int32_t)need1;
@@ -635,17 +637,15 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
         if (m_run > 0) {
           const uint64_t K0 = LC * B;
           const uint32_t smax0 = (uint32_t)((int32_t)m.d + m.maxO);
-          const double* cb = C.coef + (B - 1);
-          const double ac = __ldg(cb), bc = __ldg(cb + ms), ap = __ldg(cb + 2 * ms), bp = __ldg(cb + 3 * ms);
-          const double as_ = __ldg(cb + 4 * ms), bs_ = __ldg(cb + 5 * ms);
-          const uint64_t f_last = K0 + K1 * ((uint64_t)m.S + (uint64_t)B * (m_run - 1));
+          const double2* cb = reinterpret_cast<const double2*>(C.coef + (size_t)(B - 1) * 8);
+          const double2 cc = __ldg(cb), cp = __ldg(cb + 1), cs = __ldg(cb + 2);
+          const double ac = cc.x, bc = cc.y, ap = cp.x, bp = cp.y, as_ = cs.x, bs_ = cs.y;
           double t = m.t;
           if (m_run > 4) {
             // lane j evaluates iteration done_it + j of a 32-iteration chunk (the x of every
             // iteration are exact integers, so their conversions equal the sequential
             // increments), then the chunk's costs are added to t one by one in iteration order
             // (c23, c24: bit-identical to the sequential loop)
-            const bool exact = f_last < (1ull << 53);
             bool stopped = false;
             while (done_it < m_run && !stopped) {
               const uint32_t cnt = min(32u, m_run - done_it);
@@ -653,7 +653,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
               if ((uint32_t)lane < cnt) {
                 const uint64_t jj = done_it + (uint32_t)lane;
                 const uint64_t S_j = (uint64_t)m.S + (uint64_t)B * jj;
-                const double xc = exact ? (double)(K0 + K1 * S_j) : __ull2double_rn(K0 + K1 * S_j);
+                const double xc = __ull2double_rn(K0 + K1 * S_j);
                 const double xp = __ull2double_rn((uint64_t)B * (smax0 + jj));
                 const double xs = __ull2double_rn(S_j);
                 cj = __dadd_rn(__dadd_rn(__fma_rn(ac, xc, bc), __fma_rn(ap, xp, bp)), __fma_rn(as_, xs, bs_));
@@ -715,7 +715,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
               }
               __syncwarp();
             }
-          } else if (f_last < (1ull << 53)) {
+          } else if (K0 + K1 * ((uint64_t)m.S + (uint64_t)B * (m_run - 1)) < (1ull << 53)) {
             // every x of the run is an integer below 2^53: exact fp64 increments == RN conversions
             double xc = (double)(K0 + K1 * (uint64_t)m.S);
             const double dxc = (double)(K1 * B), dB = (double)B;
@@ -749,19 +749,9 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           if (m_run > 4) K2STAT(14, 1);
           // closed-form exact updates for the done_it iterations of the run
           const uint64_t mm = done_it;
-          // sum_j (K0 + K1 (S + B j)) = mm K0 + K1 (mm S + B mm (mm - 1) / 2)
-          const uint64_t inner = mm * (uint64_t)m.S + (uint64_t)B * (mm * (mm - 1) / 2);
-          if (f_last < (1ull << 53) && mm < 2048ull) {
-            add_flops(m, mm * K0 + K1 * inner);   // < 2^11 * 2^53: exact in u64
-          } else {
-            uint64_t lo64 = mm * K0, hi64 = __umul64hi(mm, K0);
-            const uint64_t plo = K1 * inner, phi = __umul64hi(K1, inner);
-            lo64 += plo;
-            hi64 += phi + (lo64 < plo ? 1ull : 0ull);
-            const uint64_t nlo = m.fl_lo + lo64;
-            m.fl_hi += hi64 + (nlo < lo64 ? 1ull : 0ull);
-            m.fl_lo = nlo;
-          }
+          // sum_j (K0 + K1 (S + B j)) = L c (B mm) + K1 (mm S + B mm (mm - 1) / 2)
+          m.a1 += (uint64_t)B * mm;
+          m.a2 += mm * (uint64_t)m.S + (uint64_t)B * (mm * (mm - 1) / 2);
           m.reqit += (uint64_t)B * mm;
           m.iter += done_it;
           const uint32_t rr = bs.mod(done_it);
@@ -834,9 +824,10 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           const uint32_t smax = (uint32_t)((int32_t)m.d + m.maxO);
           m.F -= (int32_t)need;
           const uint64_t fl = LC * B2 + K1 * (uint64_t)m.S;
-          const double lat = iter_cost(C.coef, ms, B2, fl, B2 * smax, m.S);
+          const double lat = iter_cost(C.coef, B2, fl, B2 * smax, m.S);
           m.t = __dadd_rn(m.t, lat);
-          add_flops(m, fl);
+          m.a1 += B2;
+          m.a2 += m.S;
           m.reqit += B2;
           m.iter += 1;
           m.S += B2;
@@ -1003,8 +994,14 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
     if (lane == 0) {
       samu_trial_rec rec;
       rec.t_end = m.t;
-      rec.flops_lo = m.fl_lo;
-      rec.flops_hi = m.fl_hi;
+      {   // FLOPs = LC a1 + K1 a2 in u128
+        uint64_t lo = LC * m.a1, hi = __umul64hi(LC, m.a1);
+        const uint64_t plo = K1 * m.a2, phi = __umul64hi(K1, m.a2);
+        lo += plo;
+        hi += phi + (lo < plo ? 1ull : 0ull);
+        rec.flops_lo = lo;
+        rec.flops_hi = hi;
+      }
       rec.req_iters = m.reqit;
       rec.iters = m.iter;
       rec.flags = (done ? 1u : 0u) | (cut ? 2u : 0u) | (all_done ? 4u : 0u);

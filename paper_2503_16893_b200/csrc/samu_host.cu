@@ -496,7 +496,7 @@ extern "C" samu_status samu_app_load(samu_ctx* c, const samu_engine_cfg* engine,
       std::vector<double> part(M.coeff.begin() + (size_t)slot * 6 * nb, M.coeff.begin() + (size_t)(slot + 1) * 6 * nb);
       CK(c, upload(cs, part, s));
       DevBuf& out = c->coef[{m, slot}];
-      CK(c, out.ensure(sizeof(double) * 6 * e.max_num_seqs));
+      CK(c, out.ensure(sizeof(double) * 8 * e.max_num_seqs));
       CK(c, samu_count(c, launch_dense_coeff(bb.as<uint32_t>(), nb, cs.as<double>(), e.max_num_seqs, out.as<double>(), s)));
       CK(c, cudaStreamSynchronize(s));
     }
@@ -661,6 +661,8 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
       D.L = M.spec.n_layers;
       D.h_tp = M.spec.hidden / (uint32_t)cd.tp;
       D.c = M.spec.c;
+      D.LC = (uint64_t)D.L * D.c;
+      D.K1 = 2ull * D.L * D.h_tp;
       const int slot = log2_exact((uint32_t)cd.tp);
       D.load_s = M.load[(size_t)slot * SAMU_MAX_DP + (cd.dp - 1)];
       D.coef = c->coef.at({model, slot}).as<double>();

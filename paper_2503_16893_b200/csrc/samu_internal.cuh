@@ -42,6 +42,7 @@ struct DevCand {
   int32_t blocks;              // KV blocks per replica (c5)
   uint32_t L, h_tp;            // layers, h / tp
   uint64_t c;                  // per-layer matmul weight elements
+  uint64_t LC, K1;             // L c and 2 L (h/tp): FLOPs = LC B + K1 S (decode), B s (LC + K1 s) (prefill)
   double load_s;               // loading time of (model, dp, tp)
   const double* coef;          // dense [3 phases][2 (a,b)][max_seqs]
   const uint32_t* rep_off;     // [dp + 1]

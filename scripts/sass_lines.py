@@ -31,9 +31,10 @@ for ln in sass.splitlines():
         continue
     if not inside:
         continue
-    m = re.search(r'//## File ".*", line (\d+)', ln)
+    m = re.search(r'//## File "(.*)", line (\d+)', ln)
     if m:
-        cur_line = int(m.group(1))
+        f = os.path.basename(m.group(1))
+        cur_line = int(m.group(2)) if f == "k_simulate.cu" else (f, int(m.group(2)))
         continue
     m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
     if m:
@@ -46,11 +47,13 @@ hdr = rows[1]
 ia, ie, iss = hdr.index("Address"), hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
 data = [r for r in rows[2:] if len(r) == len(hdr)]
 base = int(data[0][ia], 16)
-inst, samp = collections.Counter(), collections.Counter()
+inst, samp, hdr_i = collections.Counter(), collections.Counter(), collections.Counter()
 tot_i = tot_s = 0
 for r in data:
     off = int(r[ia], 16) - base
     line = line_of.get(off, -1)
+    if isinstance(line, tuple):
+        hdr_i[line[0]] += int(r[ie])
     i, s = int(r[ie]), int(r[iss])
     inst[line] += i
     samp[line] += s
@@ -60,11 +63,15 @@ src = open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper
                         "k_simulate.cu")).read().splitlines()
 print(f"total warp instructions {tot_i:.4e}, stall samples {tot_s}")
 for line, i in inst.most_common(top):
-    txt = src[line - 1].strip()[:90] if 0 < line <= len(src) else "?"
+    if isinstance(line, tuple):
+        txt, line = f"[{line[0]}:{line[1]}]", 0
+    else:
+        txt = src[line - 1].strip()[:90] if 0 < line <= len(src) else "?"
     print(f"{line:5d} {100 * i / tot_i:6.2f}% inst {100 * samp[line] / max(tot_s, 1):6.2f}% samp  {txt}")
+print("header intrinsics:", {k: f"{100 * v / tot_i:.2f}%" for k, v in hdr_i.most_common()})
 if len(sys.argv) > 5:
     ranges = [tuple(map(int, x.split("-"))) for x in sys.argv[5].split(",")]
     for a, b in ranges:
-        i = sum(v for k, v in inst.items() if a <= k <= b)
-        s = sum(v for k, v in samp.items() if a <= k <= b)
+        i = sum(v for k, v in inst.items() if isinstance(k, int) and a <= k <= b)
+        s = sum(v for k, v in samp.items() if isinstance(k, int) and a <= k <= b)
         print(f"lines {a}-{b}: {100 * i / tot_i:6.2f}% inst {100 * s / max(tot_s, 1):6.2f}% samp")
