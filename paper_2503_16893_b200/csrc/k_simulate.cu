@@ -619,13 +619,15 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
         const double stop_t = m.stop;
         // KV need of the run's decodes: histogram rotated to start at needidx, prefix sums
         const uint32_t hv = (uint32_t)lane < bs.v() ? W.hist[bs.mod(m.needidx + bs.v() - (uint32_t)lane)] : 0u;
-        const uint32_t pre = warp_incl_scan(hv, lane);
         const uint32_t m_fin = m.next_fin - m.d;
         uint32_t i_pre = 0x7fffffffu;   // first run iteration that must preempt
-        {
-          const uint32_t F0 = (uint32_t)m.F;
-          // each bs decodes need exactly B blocks: skip the search when the run cannot run out
-          if ((uint64_t)F0 < (uint64_t)B * ((uint64_t)bs.div(m_fin) + 1)) {
+        uint32_t pre = 0;
+        // each bs decodes need exactly B blocks: no search (and no scan) when the run cannot run out
+        const bool tight = (uint64_t)(uint32_t)m.F < (uint64_t)B * ((uint64_t)bs.div(m_fin) + 1);
+        if (tight) {
+          pre = warp_incl_scan(hv, lane);
+          {
+            const uint32_t F0 = (uint32_t)m.F;
             const uint32_t q0 = F0 / B, rem = F0 - q0 * B;
             const uint32_t bad = __ballot_sync(FULL, (uint32_t)lane < bs.v() && pre > rem);
             const uint64_t ip = (uint64_t)q0 * bs.v() + (uint32_t)(__ffs(bad) - 1);
@@ -674,13 +676,13 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
                   const double err = __dsub_rn(cj, r);   // exact (Fast2Sum, t >= c when in binade)
                   const double halfu = __longlong_as_double((long long)(eb - (53ull << 52)));
                   const double top = __longlong_as_double((long long)(eb + (1ull << 52)));   // 2^(e+1)
-                  double pre = r;
+                  double psum = r;
 #pragma unroll
                   for (int o = 1; o < 32; o <<= 1) {
-                    const double nb2 = __shfl_up_sync(FULL, pre, o);
-                    if (lane >= o) pre = __dadd_rn(pre, nb2);
+                    const double nb2 = __shfl_up_sync(FULL, psum, o);
+                    if (lane >= o) psum = __dadd_rn(psum, nb2);
                   }
-                  const double acc_j = __dadd_rn(t, pre);   // partial sum after iteration lane
+                  const double acc_j = __dadd_rn(t, psum);   // partial sum after iteration lane
                   const bool in = (uint32_t)lane < cnt;
                   const uint32_t bstop = __ballot_sync(FULL, in && !(acc_j < stop_t));
                   const uint32_t upto = bstop ? (uint32_t)(__ffs(bstop) - 1) : cnt - 1;   // last lane used
@@ -755,7 +757,10 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           m.reqit += (uint64_t)B * mm;
           m.iter += done_it;
           const uint32_t rr = bs.mod(done_it);
-          const uint32_t need_sum = bs.div(done_it) * B + (rr ? __shfl_sync(FULL, pre, rr - 1) : 0u);
+          const uint32_t need_rr = rr == 0 ? 0u
+                                   : tight ? __shfl_sync(FULL, pre, rr - 1)
+                                           : __reduce_add_sync(FULL, (uint32_t)lane < rr ? hv : 0u);
+          const uint32_t need_sum = bs.div(done_it) * B + need_rr;
           m.F -= (int32_t)need_sum;
           m.S += B * done_it;
           m.d += done_it;
