@@ -53,6 +53,13 @@ struct WarpSm {
   uint32_t adm_req[32], adm_meta[32];
   int2 adm_fo[32];
   double cbuf[32];           // per-iteration costs of a decode-run chunk (lane j = iteration j)
+  // warp-uniform state off the hot path (kept out of registers); every lane writes the same
+  // value and reads back its own write, so no synchronisation is needed
+  double tau, next_ready;    // time limit, ready time of the next pending cross-node arrival
+  const uint64_t* pk;        // pending arrivals sorted by (ready time, index): keys / requests
+  const uint32_t* pi;
+  uint32_t pend_ptr, n_pend, n_heads;
+  int32_t site;
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -114,14 +121,14 @@ __device__ __forceinline__ void set_error(int32_t* e, int32_t code, int32_t site
 
 struct Sim {
   // warp-uniform scalar state
-  double t, tau, next_ready, stop;   // stop = min(tau, next_ready)
+  double t, stop;   // stop = min(tau, next ready time of a pending arrival)
   // FLOPs of the completed iterations = L c * a1 + 2 L (h/tp) * a2 (exact, folded into u128 at
   // the end): a1 = sum of decode B + prefill B s, a2 = sum of decode S + prefill B s^2
   uint64_t a1, a2, reqit;
   uint32_t iter, d, needidx, B, S, next_fin, next_rank;
   int32_t F, maxO;
-  uint32_t stack_cnt, q_head, q_tail, n_heads, n_front, pend_ptr, n_pend;
-  int32_t err, site;
+  uint32_t stack_cnt, q_head, q_tail, n_front;
+  int32_t err;
 };
 
 
@@ -227,12 +234,14 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
 
     Sim m;
     m.t = C.resume ? (over ? over[j] : 0.0) : C.load_s;
-    m.tau = C.tau ? C.tau[k] : (C.tau_rec ? C.tau_rec[k].t_end : CUDART_INF);
+    double tau = C.tau ? C.tau[k] : (C.tau_rec ? C.tau_rec[k].t_end : CUDART_INF);
     m.a1 = m.a2 = m.reqit = 0;
     m.iter = 0; m.d = 0; m.needidx = 0; m.B = 0; m.S = 0; m.next_rank = 0;
     m.F = C.blocks; m.maxO = INT_MIN; m.next_fin = FULL;
-    m.stack_cnt = 0; m.q_head = 0; m.q_tail = 0; m.n_heads = 0; m.n_front = 0; m.pend_ptr = 0; m.n_pend = 0;
-    m.err = 0; m.site = 0;
+    m.stack_cnt = 0; m.q_head = 0; m.q_tail = 0; m.n_front = 0;
+    uint32_t n_heads = 0, n_pend = 0;
+    m.err = 0;
+    int32_t site = 0;
     uint32_t occ = 0;   // this lane's occupied slots (bit j = slot lane + 32 j)
 
     W.hist[lane] = 0;
@@ -257,11 +266,11 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
       const bool head = fresh && pr < 0;
       const bool pend = fresh && cross;
       const bool succ_wait = fresh && pr >= 0 && !cross;
-      if (succ_wait && st && (st[pr] >> 28) == SAMU_ST_DONE) { m.err = SAMU_E_STATE; m.site = 1; }
-      if (valid && s > SAMU_ST_DONE) { m.err = SAMU_E_STATE; m.site = 2; }
+      if (succ_wait && st && (st[pr] >> 28) == SAMU_ST_DONE) { m.err = SAMU_E_STATE; site = 1; }
+      if (valid && s > SAMU_ST_DONE) { m.err = SAMU_E_STATE; site = 2; }
       const uint32_t bh = __ballot_sync(FULL, head);
-      if (head && !st) q[m.n_heads + __popc(bh & lanemask_lt())] = r;   // fresh state: no front region
-      m.n_heads += __popc(bh);
+      if (head && !st) q[n_heads + __popc(bh & lanemask_lt())] = r;   // fresh state: no front region
+      n_heads += __popc(bh);
       // carried entries: class 0 running (reload) | 1 preempted | 3 queued | 4 running (resume)
       uint32_t cls = 7;
       if (valid && s == SAMU_ST_RUNNING) cls = C.resume ? 4u : 0u;
@@ -279,10 +288,10 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
         if (st && (st[pr] >> 28) == SAMU_ST_DONE && ft) ready = ft[pr];
         else if (sfin) ready = sfin[pr];
         else ready = CUDART_INF;
-        const uint32_t pos = m.n_pend + __popc(bp & lanemask_lt());
+        const uint32_t pos = n_pend + __popc(bp & lanemask_lt());
         if (pos < (uint32_t)P.max_p) { pkey[pos] = dkey(ready); pidx[pos] = r; }
       }
-      m.n_pend += __popc(bp);
+      n_pend += __popc(bp);
       if (bc) {
         n_run += __popc(__ballot_sync(FULL, valid && s == SAMU_ST_RUNNING));
         n_pre += __popc(__ballot_sync(FULL, valid && s == SAMU_ST_PREEMPTED));
@@ -290,13 +299,13 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
       }
       if (__ballot_sync(FULL, valid && s != SAMU_ST_DONE)) all_done = false;
     }
-    m.site = (int32_t)__reduce_max_sync(FULL, (uint32_t)m.site);
+    site = (int32_t)__reduce_max_sync(FULL, (uint32_t)site);
     m.err = __reduce_max_sync(FULL, (uint32_t)(-m.err)) ? SAMU_E_STATE : 0;
     m.n_front = C.resume ? n_pre : n_run + n_pre;
-    if (m.n_pend > (uint32_t)P.max_p || n_cls > (uint32_t)P.max_p ||
-        m.n_front + m.n_heads + n_q > (uint32_t)P.max_q) { m.err = SAMU_E_STATE; m.site = 3; }
-    if (C.resume && n_run > ms) { m.err = SAMU_E_STATE; m.site = 4; }
-    m.q_tail = m.n_front + m.n_heads + n_q;
+    if (n_pend > (uint32_t)P.max_p || n_cls > (uint32_t)P.max_p ||
+        m.n_front + n_heads + n_q > (uint32_t)P.max_q) { m.err = SAMU_E_STATE; site = 3; }
+    if (C.resume && n_run > ms) { m.err = SAMU_E_STATE; site = 4; }
+    m.q_tail = m.n_front + n_heads + n_q;
     if (!m.err && st) {
       // heads after the front region, in index order
       uint32_t nh = 0;
@@ -315,7 +324,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
         warp_radix_sort(skey, sidx, skey + P.max_p, sidx + P.max_p, n_cls, W.tmp, lane, &sorted_idx);
         int32_t used = 0;
         uint32_t S0 = 0;
-        const uint32_t q_base = m.n_front + m.n_heads;
+        const uint32_t q_base = m.n_front + n_heads;
         for (uint32_t i = lane; i < n_cls; i += 32) {
           const uint32_t r = sorted_idx[i];
           if (i < m.n_front) q[i] = r;
@@ -327,7 +336,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
             const uint32_t Lr = max((uint32_t)lo[r], 1u);
             const int32_t o = (int32_t)(lin + g);
             const uint32_t ph = bs.posmod(o - 1);
-            if (g >= Lr || g == 0) { m.err = SAMU_E_STATE; m.site = 5; }
+            if (g >= Lr || g == 0) { m.err = SAMU_E_STATE; site = 5; }
             W.s_req[jx] = r;
             W.s_fo[jx] = make_int2((int32_t)(Lr - g), o);
             W.s_meta[jx] = (jx << 5) | ph;
@@ -338,14 +347,14 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
         }
         used = (int32_t)__reduce_add_sync(FULL, (uint32_t)used);
         S0 = __reduce_add_sync(FULL, S0);
-        m.site = (int32_t)__reduce_max_sync(FULL, (uint32_t)m.site);
+        site = (int32_t)__reduce_max_sync(FULL, (uint32_t)site);
         m.err = __reduce_max_sync(FULL, (uint32_t)(-m.err)) ? SAMU_E_STATE : 0;
         if (C.resume) {
           m.B = n_run;
           m.S = S0;
           m.F -= used;
           m.next_rank = n_run;
-          if (m.F < 0) { m.err = SAMU_E_STATE; m.site = 8; }
+          if (m.F < 0) { m.err = SAMU_E_STATE; site = 8; }
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj)
             if ((uint32_t)(lane + 32 * jj) < n_run) occ |= 1u << jj;
@@ -357,13 +366,20 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
     // ---- pending cross-node arrivals in (ready, index) order: stable LSD radix sort ----
     const uint64_t* pk = pkey;
     const uint32_t* pi = pidx;
-    if (!m.err && m.n_pend > 1) {
+    if (!m.err && n_pend > 1) {
       uint32_t* si;
-      pk = warp_radix_sort(pkey, pidx, pkey + P.max_p, pidx + P.max_p, m.n_pend, W.tmp, lane, &si);
+      pk = warp_radix_sort(pkey, pidx, pkey + P.max_p, pidx + P.max_p, n_pend, W.tmp, lane, &si);
       pi = si;
     }
-    m.next_ready = m.n_pend ? kdouble(pk[0]) : CUDART_INF;
-    m.stop = fmin(m.tau, m.next_ready);
+    W.tau = tau;
+    W.next_ready = n_pend ? kdouble(pk[0]) : CUDART_INF;
+    W.pk = pk;
+    W.pi = pi;
+    W.pend_ptr = 0;
+    W.n_pend = n_pend;
+    W.n_heads = n_heads;
+    W.site = site;
+    m.stop = fmin(tau, W.next_ready);
     const uint64_t K1 = C.K1;   // 2 L (h/tp)
     const uint64_t LC = C.LC;   // L c
     const bool need_rel = fio || fto || commit || C.has_succ;
@@ -390,23 +406,23 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
     while (!m.err) {
       K2STAT(1, 1);
       if (m.t >= m.stop) {   // stop time or a pending arrival reached
-        if (m.t >= m.tau) { cut = true; break; }
+        if (m.t >= W.tau) { cut = true; break; }
         // pending cross-node arrivals with ready <= t join the back of W
-        while (m.pend_ptr < m.n_pend && m.next_ready <= m.t) {
-          const uint32_t i = m.pend_ptr + lane;
-          const bool ok = i < m.n_pend && kdouble(pk[i]) <= m.t;
+        while (W.pend_ptr < W.n_pend && W.next_ready <= m.t) {
+          const uint32_t i = W.pend_ptr + lane;
+          const bool ok = i < W.n_pend && kdouble(W.pk[i]) <= m.t;
           const uint32_t b = __ballot_sync(FULL, ok);
           const uint32_t cnt = (b == FULL) ? 32u : (uint32_t)(__ffs(~b) - 1);
-          if ((uint32_t)lane < cnt) q[m.q_tail + lane] = pi[i];
+          if ((uint32_t)lane < cnt) q[m.q_tail + lane] = W.pi[i];
           m.q_tail += cnt;
-          m.pend_ptr += cnt;
-          m.next_ready = m.pend_ptr < m.n_pend ? kdouble(pk[m.pend_ptr]) : CUDART_INF;
+          W.pend_ptr += cnt;
+          W.next_ready = W.pend_ptr < W.n_pend ? kdouble(W.pk[W.pend_ptr]) : CUDART_INF;
         }
-        m.stop = fmin(m.tau, m.next_ready);
+        m.stop = fmin(W.tau, W.next_ready);
       }
       const uint32_t wlen = m.stack_cnt + (m.q_tail - m.q_head);
       if (m.B == 0 && wlen == 0) {
-        if (m.pend_ptr < m.n_pend && m.next_ready != CUDART_INF) { m.t = m.next_ready; continue; }
+        if (W.pend_ptr < W.n_pend && W.next_ready != CUDART_INF) { m.t = W.next_ready; continue; }
         break;
       }
       // refill the window so it holds min(32, |W|) entries
@@ -594,7 +610,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           m.maxO = __reduce_max_sync(FULL, lmaxo);
         }
       } else {
-        if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; m.site = 9; break; }
+        if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; W.site = 9; break; }
         // ================= decode run (c9): uniform iterations until an event ===============
         const uint32_t need1 = W.hist[m.needidx];
         if (m.next_fin == m.d + 1 && (int32_t)need1 <= m.F) {
@@ -818,7 +834,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
             K2STAT(9, 1);
             m.B -= 1;
             m.S -= l;
-            if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; m.site = 10; break; }
+            if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; W.site = 10; break; }
           }
           if (m.err) break;
           m.next_fin = __reduce_min_sync(FULL, lminf);
@@ -960,8 +976,8 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
     }
 
     // ---- write back (commit) and the per-replica record ----
-    const bool done = !m.err && m.B == 0 && m.stack_cnt == 0 && m.q_head == m.q_tail && m.pend_ptr == m.n_pend;
-    if (m.err && lane == 0) set_error(P.error, m.err, m.site);
+    const bool done = !m.err && m.B == 0 && m.stack_cnt == 0 && m.q_head == m.q_tail && W.pend_ptr == W.n_pend;
+    if (m.err && lane == 0) set_error(P.error, m.err, W.site);
     if (commit && !m.err) {
       // running ranks renumbered 0..B-1 in admission order
       for (int s = lane; s < SLOTS; s += 32) W.tmp[s] = 0xFFFFFFFFu;
@@ -987,14 +1003,14 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
         st[rq] = (SAMU_ST_PREEMPTED << 28) | (m.stack_cnt - 1 - i);
         gst[rq] = (uint16_t)W.stk_g[i];
       }
-      const uint32_t qbase = max(m.q_head, m.n_front + m.n_heads);
+      const uint32_t qbase = max(m.q_head, m.n_front + W.n_heads);
       for (uint32_t pos = m.q_head + lane; pos < m.q_tail; pos += 32) {
         const uint32_t rq = q[pos];
         if (pos < m.n_front) st[rq] = (SAMU_ST_PREEMPTED << 28) | (m.stack_cnt + pos - m.q_head);
-        else if (pos < m.n_front + m.n_heads) gst[rq] = 0;
+        else if (pos < m.n_front + W.n_heads) gst[rq] = 0;
         else { st[rq] = (SAMU_ST_QUEUED << 28) | (pos - qbase); gst[rq] = 0; }
       }
-      if (over && lane == 0) over[j] = (done || !cut) ? 0.0 : __dsub_rn(m.t, m.tau);
+      if (over && lane == 0) over[j] = (done || !cut) ? 0.0 : __dsub_rn(m.t, W.tau);
     }
     if (lane == 0) {
       samu_trial_rec rec;
