@@ -189,11 +189,12 @@ static_assert(sizeof(DevCand) * SAMU_K2_CONST_CANDS <= 64 * 1024, "candidate tab
 __constant__ DevCand c_cands[SAMU_K2_CONST_CANDS];
 
 template <int BSK, bool CONSTC>
-// Occupancy (profiles/r1_k2_v6_ncu.md): 5 blocks of 4 warps per SM caps registers at 96 (a
-// 28-byte spill) for 20 resident warps: 3-4 % faster than 2 x 8 warps at 122 registers; 24
-// warps (80 registers, 208-byte spill) and 8 warps are slower.  SAMU_DEFINES overrides both.
+// Occupancy: 6 blocks of 4 warps per SM caps registers at 80 for 24 resident warps (C5 step
+// 436 -> 418 ms against 5 blocks at 96 registers, once the cold state moved to shared memory;
+// 7 blocks / 72 registers is slower, 16 warps at 128 registers slower still; see
+// scripts/variants.sh).  SAMU_DEFINES overrides both.
 #ifndef SAMU_K2_MINB
-#define SAMU_K2_MINB 5
+#define SAMU_K2_MINB 6
 #endif
 __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_simulate(SimLaunch P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];

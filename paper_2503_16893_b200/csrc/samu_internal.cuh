@@ -8,7 +8,7 @@
 
 #define SAMU_EMPTY 0xFFFFFFFFu
 #ifndef SAMU_WARPS_PER_BLOCK
-#define SAMU_WARPS_PER_BLOCK 4   // K2 block = 4 warps; 5 blocks / SM (96 registers): 20 warps per SM
+#define SAMU_WARPS_PER_BLOCK 4   // K2 block = 4 warps; 6 blocks / SM (80 registers): 24 warps per SM
 #endif
 
 // ------------------------------------------------------------------------------------------
