@@ -945,11 +945,10 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
       // ---- finish records + chain successor release (c19), for this iteration's finishers ----
       if (n_fin && need_rel) {
         const uint32_t itx = m.iter - 1;
-        uint32_t nrel = 0;
-        for (uint32_t base = 0; base < n_fin; base += 32) {
-          const uint32_t i = base + lane;
-          const bool v = i < n_fin;
-          const uint32_t r = v ? W.tmp[i] : 0u;
+        if (n_fin <= 32) {
+          // one finisher per lane; released successors ranked in registers (index order, c19)
+          const bool v = (uint32_t)lane < n_fin;
+          const uint32_t r = v ? W.tmp[lane] : 0u;
           int32_t sr = -1;
           if (v) {
             if (fio) fio[r] = itx;
@@ -958,20 +957,44 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
             if (C.has_succ) sr = __ldg(A.succ + r);
           }
           const uint32_t br = __ballot_sync(FULL, sr >= 0);
-          if (sr >= 0) W.tmp2[nrel + __popc(br & lanemask_lt())] = (uint32_t)sr;
-          nrel += __popc(br);
-        }
-        __syncwarp();
-        if (nrel) {
-          // append in index order: rank of each released id among the released set
-          for (uint32_t i = lane; i < nrel; i += 32) {
-            const uint32_t x = W.tmp2[i];
+          if (br) {
             uint32_t rank = 0;
-            for (uint32_t jj = 0; jj < nrel; ++jj) rank += W.tmp2[jj] < x ? 1u : 0u;
-            q[m.q_tail + rank] = x;
+            for (uint32_t bb = br; bb; bb &= bb - 1) {   // rank among the released ids
+              const int32_t x = __shfl_sync(FULL, sr, __ffs(bb) - 1);
+              rank += (x < sr) ? 1u : 0u;
+            }
+            if (sr >= 0) q[m.q_tail + rank] = (uint32_t)sr;
+            m.q_tail += __popc(br);
           }
-          m.q_tail += nrel;
+        } else {
+          uint32_t nrel = 0;
+          for (uint32_t base = 0; base < n_fin; base += 32) {
+            const uint32_t i = base + lane;
+            const bool v = i < n_fin;
+            const uint32_t r = v ? W.tmp[i] : 0u;
+            int32_t sr = -1;
+            if (v) {
+              if (fio) fio[r] = itx;
+              if (fto) fto[r] = m.t;
+              if (commit) { st[r] = SAMU_ST_DONE << 28; ft[r] = m.t; }
+              if (C.has_succ) sr = __ldg(A.succ + r);
+            }
+            const uint32_t br = __ballot_sync(FULL, sr >= 0);
+            if (sr >= 0) W.tmp2[nrel + __popc(br & lanemask_lt())] = (uint32_t)sr;
+            nrel += __popc(br);
+          }
           __syncwarp();
+          if (nrel) {
+            // append in index order: rank of each released id among the released set
+            for (uint32_t i = lane; i < nrel; i += 32) {
+              const uint32_t x = W.tmp2[i];
+              uint32_t rank = 0;
+              for (uint32_t jj = 0; jj < nrel; ++jj) rank += W.tmp2[jj] < x ? 1u : 0u;
+              q[m.q_tail + rank] = x;
+            }
+            m.q_tail += nrel;
+            __syncwarp();
+          }
         }
       }
     }
