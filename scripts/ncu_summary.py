@@ -22,7 +22,7 @@ def val(name, scale=1.0):
 
 rd, wr = val("dram__bytes_read.sum"), val("dram__bytes_write.sum")
 summary = {
-    "workload": workload, "kernel": "k_simulate<true> (K2)", "command": command,
+    "workload": workload, "kernel": "k_simulate<16, true> (K2)", "command": command,
     "gpu_time_ms": val("gpu__time_duration.sum"),
     "dram_bytes_read": int(rd), "dram_bytes_write": int(wr), "dram_bytes_per_launch": int(rd + wr),
     "smsp_inst_executed": int(val("smsp__inst_executed.sum")),
