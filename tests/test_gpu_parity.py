@@ -157,6 +157,22 @@ def test_simulate_fuzz_signed_costs_and_cuts(seed):
     _sim_parity(w, cands, 3, tau=tau)
 
 
+@pytest.mark.parametrize("load,cost", [(1.0, 3 * 2.0 ** -53), (1.0, 2.0 ** -53), (1.0, 5 * 2.0 ** -54),
+                                       (1.0, 0.3), (0.0, 3 * 2.0 ** -53), (1.0, 1e-17), (3.0, 2.0 ** -51 + 2.0 ** -52)])
+def test_chunk_sum_ties_and_binade_crossings(load, cost):
+    # Decode-run chunks sum their 32 costs in parallel (binade-local rounding + warp scan) and fall
+    # back to the sequential walk on ties / binade crossings.  Constant costs of exactly 1.5 or
+    # 0.5 ulp of the clock make every add a round-half-even tie whose result alternates with the
+    # clock's last bit; 0.3 s per iteration crosses binades every few iterations.  The clock must
+    # equal the oracle's one-by-one sum bit for bit.
+    ld = F.zero_load()
+    ld[0, 0] = load
+    w = F.tiny(np.array([5, 9, 17, 3]), np.array([200, 77, 140, 5]), load=ld, cf=F.coeff("const", cost),
+               sp=F.spec(l_max=512))
+    g = _sim_parity(w, [(0, 1, 1)], 1)
+    assert g["iters"][0, 0] == 200
+
+
 def test_candidate_table_both_paths():
     # launches with <= 400 candidates read them from the constant bank, larger ones from global
     # memory (k_simulate<., CONSTC>): both must give the oracle's records
