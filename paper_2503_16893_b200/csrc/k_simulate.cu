@@ -404,10 +404,12 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
       }
     m.next_fin = __reduce_min_sync(FULL, lminf);
     m.maxO = __reduce_max_sync(FULL, lmaxo);
-    // window: register cache of the first wn (<= 32) entries of W (lane i = position i):
+    // window: register cache of the first wn (<= 32) entries of W, circular over the lanes
+    // (position i in lane (wb + i) mod 32, so admitting a prefix just advances wb and the admitted
+    // requests enter the running set from their own lanes, spread round-robin over all lanes):
     // request, prompt tokens p = l_in + g, tokens still to generate incl. the prefill's (L - g)
     // (raw loads kept unconsumed until needed: the window refill does not wait on them)
-    uint32_t w_r = 0, w_li = 0, w_lo = 0, w_g = 0, wn = 0;
+    uint32_t w_r = 0, w_li = 0, w_lo = 0, w_g = 0, wn = 0, wb = 0;
 
     K2STAT(0, 1);
     // ---- main loop (c25) ----
@@ -437,11 +439,12 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
       {
         const uint32_t want = min(32u, wlen);
         if (wn < want) {
-          if ((uint32_t)lane >= wn && (uint32_t)lane < want) {
+          const uint32_t pos = ((uint32_t)lane - wb) & 31u;
+          if (pos >= wn && pos < want) {
             uint32_t r, g;
-            if ((uint32_t)lane < m.stack_cnt) { r = W.stk_req[m.stack_cnt - 1 - lane]; g = W.stk_g[m.stack_cnt - 1 - lane]; }
+            if (pos < m.stack_cnt) { r = W.stk_req[m.stack_cnt - 1 - pos]; g = W.stk_g[m.stack_cnt - 1 - pos]; }
             else {
-              const uint32_t qp = m.q_head + lane - m.stack_cnt;
+              const uint32_t qp = m.q_head + pos - m.stack_cnt;
               r = q[qp];
               g = qp < m.n_front ? (uint32_t)gst[r] : 0u;   // recompute front keeps its tokens
             }
@@ -454,7 +457,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
         }
       }
       // does the head of W fit? (slots, token budget, blocks)
-      const uint32_t hp = __shfl_sync(FULL, w_li + w_g, 0);
+      const uint32_t hp = __shfl_sync(FULL, w_li + w_g, wb);
       const bool fits = wlen > 0 && m.B < ms && hp <= C.budget && (int32_t)bs.cdiv(hp) <= m.F;
       uint32_t n_fin = 0;
       if (fits) {
@@ -462,36 +465,41 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
         uint32_t k_adm = 0, tok = 0, smaxp = 0, S_add = 0, n_stay = 0;
         int32_t blk = 0, freed = 0;
         for (;;) {
-          const bool valid = (uint32_t)lane < wn;
+          const uint32_t pos = ((uint32_t)lane - wb) & 31u;   // window position of this lane
+          const bool valid = pos < wn;
           const uint32_t p = valid ? w_li + w_g : 0u;
           const uint32_t w_rem = max(w_lo, 1u) - w_g;   // tokens still to generate incl. the prefill's
           const uint32_t nb = valid ? bs.cdiv(p) : 0u;
-          uint32_t sp, sb, mm;   // admitted totals: sp / sb at lane mm - 1
+          uint32_t mm, add_tok, add_blk;   // admitted count, tokens, blocks
           K2STAT(4, 1);
           const uint32_t slots = min(wn, ms - m.B - k_adm);
           const uint32_t tot_p = __reduce_add_sync(FULL, p), tot_b = __reduce_add_sync(FULL, nb);
           if (tot_p + tok <= C.budget && (int32_t)(tot_b + blk) <= m.F) {
             // the whole window fits the token and block budgets: only the slots bind, no scans
             mm = slots;
-            sp = __reduce_add_sync(FULL, (uint32_t)lane < mm ? p : 0u);   // uniform totals
-            sb = __reduce_add_sync(FULL, (uint32_t)lane < mm ? nb : 0u);
+            add_tok = __reduce_add_sync(FULL, pos < mm ? p : 0u);
+            add_blk = __reduce_add_sync(FULL, pos < mm ? nb : 0u);
           } else if (slots <= 1u) {
             // at most the head can enter (one free slot or one waiting request): no scans
-            sp = p;
-            sb = nb;
-            const uint32_t p0 = __shfl_sync(FULL, p, 0);
-            mm = (wn > 0 && m.B + k_adm < ms && tok + p0 <= C.budget && (int32_t)(blk + bs.cdiv(p0)) <= m.F) ? 1u : 0u;
+            const uint32_t p0 = __shfl_sync(FULL, p, wb);
+            add_tok = p0;
+            add_blk = bs.cdiv(p0);
+            mm = (wn > 0 && m.B + k_adm < ms && tok + p0 <= C.budget && (int32_t)(blk + add_blk) <= m.F) ? 1u : 0u;
           } else {
             K2STAT(5, 1);
-            sp = warp_incl_scan(p, lane);
-            sb = warp_incl_scan(nb, lane);
-            const bool ok = valid && (m.B + k_adm + lane + 1 <= ms) && (tok + sp <= C.budget) &&
+            // scans in window order: lane i takes position i
+            const uint32_t src = ((uint32_t)lane + wb) & 31u;
+            const uint32_t sp = warp_incl_scan(__shfl_sync(FULL, p, src), lane);
+            const uint32_t sb = warp_incl_scan(__shfl_sync(FULL, nb, src), lane);
+            const bool ok = (uint32_t)lane < wn && (m.B + k_adm + lane + 1 <= ms) && (tok + sp <= C.budget) &&
                             ((int32_t)(blk + sb) <= m.F);
             const uint32_t bal = __ballot_sync(FULL, ok);
             mm = (bal == FULL) ? 32u : (uint32_t)(__ffs(~bal) - 1);
+            add_tok = __shfl_sync(FULL, sp, mm == 0 ? 0 : mm - 1);
+            add_blk = __shfl_sync(FULL, sb, mm == 0 ? 0 : mm - 1);
           }
           if (mm == 0) break;
-          const bool adm = (uint32_t)lane < mm;
+          const bool adm = pos < mm;
           const bool finish_now = adm && w_rem <= 1u;
           const bool stay = adm && !finish_now;
           const uint32_t bst = __ballot_sync(FULL, stay);
@@ -502,7 +510,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           if (stay) {
             s_o = (int32_t)(p + 1) - (int32_t)m.d;
             s_fin = (int32_t)(m.d + w_rem - 1);
-            s_meta = ((m.next_rank + k_adm + lane) << 5) | bs.posmod((int32_t)p - (int32_t)m.d);
+            s_meta = ((m.next_rank + k_adm + pos) << 5) | bs.posmod((int32_t)p - (int32_t)m.d);
             atomicAdd(&W.hist[s_meta & 31u], 1u);
           }
           if (finish_now && need_rel) W.tmp[n_fin + __popc(bfn & lanemask_lt())] = w_r;
@@ -514,7 +522,19 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           if (ns) {
             const bool has_free = occ != 0xFFu;
             const uint32_t fl = __ballot_sync(FULL, has_free);
-            if ((uint32_t)__popc(fl) >= ns) {
+            if ((bst & ~fl) == 0) {
+              // every staying lane has a free slot of its own: no exchange
+              if (stay) {
+                const int jb = __ffs(~occ & 0xFFu) - 1;
+                const int s = lane + 32 * jb;
+                W.s_req[s] = w_r;
+                W.s_fo[s] = make_int2(s_fin, s_o);
+                W.s_meta[s] = s_meta;
+                occ |= 1u << jb;
+                lminf = min(lminf, (uint32_t)s_fin);
+                lmaxo = max(lmaxo, s_o);
+              }
+            } else if ((uint32_t)__popc(fl) >= ns) {
               // a-th stay lane -> a-th lane with a free slot, through a lane table in smem
               if (stay) W.adm_meta[__popc(bst & lanemask_lt())] = (uint32_t)lane;
               __syncwarp();
@@ -563,26 +583,24 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
             __syncwarp();
           }
           n_stay += ns;
-          tok += __shfl_sync(FULL, sp, mm - 1);
-          blk += (int32_t)__shfl_sync(FULL, sb, mm - 1);
+          tok += add_tok;
+          blk += (int32_t)add_blk;
           k_adm += mm;
           const uint32_t take = min(mm, m.stack_cnt);
           m.stack_cnt -= take;
           m.q_head += mm - take;
-          // shift the window by mm and refill it
-          w_r = __shfl_down_sync(FULL, w_r, mm == 32 ? 0 : mm);
-          w_li = __shfl_down_sync(FULL, w_li, mm == 32 ? 0 : mm);
-          w_lo = __shfl_down_sync(FULL, w_lo, mm == 32 ? 0 : mm);
-          w_g = __shfl_down_sync(FULL, w_g, mm == 32 ? 0 : mm);
+          // advance the window by mm and refill it
+          wb = (wb + mm) & 31u;
           wn -= mm;
           const uint32_t wl2 = m.stack_cnt + (m.q_tail - m.q_head);
           const uint32_t want = min(32u, wl2);
           if (wn < want) {
-            if ((uint32_t)lane >= wn && (uint32_t)lane < want) {
+            const uint32_t pos = ((uint32_t)lane - wb) & 31u;
+            if (pos >= wn && pos < want) {
               uint32_t r, g;
-              if ((uint32_t)lane < m.stack_cnt) { r = W.stk_req[m.stack_cnt - 1 - lane]; g = W.stk_g[m.stack_cnt - 1 - lane]; }
+              if (pos < m.stack_cnt) { r = W.stk_req[m.stack_cnt - 1 - pos]; g = W.stk_g[m.stack_cnt - 1 - pos]; }
               else {
-                const uint32_t qp = m.q_head + lane - m.stack_cnt;
+                const uint32_t qp = m.q_head + pos - m.stack_cnt;
                 r = q[qp];
                 g = qp < m.n_front ? (uint32_t)gst[r] : 0u;
               }
@@ -832,10 +850,8 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
             // the victim is the new front of W: shift the window up by one
             {
               const uint32_t Lv = max((uint32_t)lo[vr], 1u);
-              const uint32_t pr = __shfl_up_sync(FULL, w_r, 1), pa = __shfl_up_sync(FULL, w_li, 1),
-                             pl = __shfl_up_sync(FULL, w_lo, 1), pg = __shfl_up_sync(FULL, w_g, 1);
-              if (lane == 0) { w_r = vr; w_li = l - vg; w_lo = Lv; w_g = vg; }
-              else { w_r = pr; w_li = pa; w_lo = pl; w_g = pg; }
+              wb = (wb - 1u) & 31u;   // a full window drops its last entry, the lane now at wb
+              if ((uint32_t)lane == wb) { w_r = vr; w_li = l - vg; w_lo = Lv; w_g = vg; }
               wn = min(wn + 1, 32u);
             }
             m.stack_cnt += 1;
