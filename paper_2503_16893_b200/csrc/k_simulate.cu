@@ -670,7 +670,13 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           pre = warp_incl_scan(hv, lane);
           {
             const uint32_t F0 = (uint32_t)m.F;
-            const uint32_t q0 = F0 / B, rem = F0 - q0 * B;
+            // q0 = F0 / B from an fp32 estimate corrected by the remainder (F0 < B (l_max / bs + 1)
+            // here, so the estimate is within one of the quotient)
+            uint32_t q0 = __float2uint_rz(__fdividef((float)F0, (float)B));
+            int32_t rs = (int32_t)(F0 - q0 * B);
+            while (rs < 0) { --q0; rs += (int32_t)B; }
+            while (rs >= (int32_t)B) { ++q0; rs -= (int32_t)B; }
+            const uint32_t rem = (uint32_t)rs;
             const uint32_t bad = __ballot_sync(FULL, (uint32_t)lane < bs.v() && pre > rem);
             const uint64_t ip = (uint64_t)q0 * bs.v() + (uint32_t)(__ffs(bad) - 1);
             i_pre = ip > 0x7fffffffull ? 0x7fffffffu : (uint32_t)ip;
@@ -812,17 +818,33 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           // ---- this decode must preempt (c7): recompute the last admitted requests ----
           uint32_t need = W.hist[m.needidx];
           while ((int32_t)need > m.F) {
-            uint32_t best = 0;
-            int bslot = -1;
+            uint32_t vmeta;
+            int ol, vs;
+            if (m.next_rank < (1u << 23)) {
+              // ranks are unique: key = (meta << 3 | j) + 1 names the slot of the lane's maximum
+              uint32_t key = 0;
 #pragma unroll
-            for (int jj = 0; jj < 8; ++jj) {
-              const int s = lane + 32 * jj;
-              if (((occ >> jj) & 1u) && (bslot < 0 || W.s_meta[s] > best)) { best = W.s_meta[s]; bslot = s; }
+              for (int jj = 0; jj < 8; ++jj) {
+                const uint32_t kj = ((occ >> jj) & 1u) ? ((W.s_meta[lane + 32 * jj] << 3) | (uint32_t)jj) + 1u : 0u;
+                key = max(key, kj);
+              }
+              const uint32_t vkey = __reduce_max_sync(FULL, key);
+              ol = __ffs(__ballot_sync(FULL, key == vkey)) - 1;
+              vs = ol + 32 * (int)((vkey - 1u) & 7u);
+              vmeta = (vkey - 1u) >> 3;
+            } else {
+              uint32_t best = 0;
+              int bslot = -1;
+#pragma unroll
+              for (int jj = 0; jj < 8; ++jj) {
+                const int s = lane + 32 * jj;
+                if (((occ >> jj) & 1u) && (bslot < 0 || W.s_meta[s] > best)) { best = W.s_meta[s]; bslot = s; }
+              }
+              vmeta = __reduce_max_sync(FULL, bslot >= 0 ? best : 0u);
+              const uint32_t own = __ballot_sync(FULL, bslot >= 0 && best == vmeta);
+              ol = __ffs(own) - 1;
+              vs = __shfl_sync(FULL, bslot, ol);
             }
-            const uint32_t vmeta = __reduce_max_sync(FULL, bslot >= 0 ? best : 0u);
-            const uint32_t own = __ballot_sync(FULL, bslot >= 0 && best == vmeta);
-            const int ol = __ffs(own) - 1;
-            const int vs = __shfl_sync(FULL, bslot, ol);
             const uint32_t vr = W.s_req[vs];
             const int32_t vo = W.s_fo[vs].y;
             const uint32_t vph = vmeta & 31u;
