@@ -223,8 +223,11 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
     const uint32_t ci = it.x, k = it.y >> 4, j = it.y & 15u;
     const DevCand& C = CONSTC ? c_cands[ci] : P.cands[ci];
     const size_t tb = (size_t)k * n;
-    const uint16_t* __restrict__ lo = P.l_out + tb;
-    const uint16_t* __restrict__ li = P.l_in + tb;
+    // sampled lengths of this trial, indexed with 32-bit offsets from the kernel parameters (the
+    // host guarantees local trials x requests < 2^32): one add + one wide multiply per load
+    const uint32_t tb32 = (uint32_t)k * (uint32_t)n;
+#define LO_(r) P.l_out[tb32 + (uint32_t)(r)]
+#define LI_(r) P.l_in[tb32 + (uint32_t)(r)]
     uint32_t* st = P.st ? P.st + tb : nullptr;
     uint16_t* gst = P.g ? P.g + tb : nullptr;
     double* ft = P.fin_t ? P.fin_t + tb : nullptr;
@@ -340,8 +343,8 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           else {   // resume: running requests keep their admission order in slots 0..B-1
             const uint32_t jx = i - m.n_front - n_q;
             const uint32_t g = gst[r];
-            const uint32_t lin = li[r];
-            const uint32_t Lr = max((uint32_t)lo[r], 1u);
+            const uint32_t lin = LI_(r);
+            const uint32_t Lr = max((uint32_t)LO_(r), 1u);
             const int32_t o = (int32_t)(lin + g);
             const uint32_t ph = bs.posmod(o - 1);
             if (g >= Lr || g == 0) { m.err = SAMU_E_STATE; site = 5; }
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
     W.n_heads = n_heads;
     W.site = site;
     m.stop = fmin(tau, W.next_ready);
-    const uint64_t K1 = C.K1;   // 2 L (h/tp)
+    const uint32_t K1 = (uint32_t)C.K1;   // 2 L (h/tp) (< 2^32, checked by the host)
     const uint64_t LC = C.LC;   // L c
     const bool need_rel = fio || fto || commit || C.has_succ;
     bool cut = false;
@@ -449,8 +452,8 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
               g = qp < m.n_front ? (uint32_t)gst[r] : 0u;   // recompute front keeps its tokens
             }
             w_r = r;
-            w_li = li[r];
-            w_lo = lo[r];
+            w_li = LI_(r);
+            w_lo = LO_(r);
             w_g = g;
           }
           wn = want;
@@ -605,8 +608,8 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
                 g = qp < m.n_front ? (uint32_t)gst[r] : 0u;
               }
               w_r = r;
-              w_li = li[r];
-              w_lo = lo[r];
+              w_li = LI_(r);
+              w_lo = LO_(r);
               w_g = g;
             }
             wn = want;
@@ -617,14 +620,13 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
         K2STAT(2, 1);
         K2STAT(3, k_adm);
         // Eq. prefill FLOPs: L (c B s + 2 B h s^2 / tp)
-        const uint64_t Bp = k_adm, sp64 = smaxp;
-        // = B s (L c + 2 L (h/tp) s): the same integer, fewer 64-bit products
-        const uint64_t Bs64 = Bp * sp64;
-        const uint64_t fl = Bs64 * (LC + K1 * sp64);
-        const double lat = iter_cost(C.coef, k_adm, fl, k_adm * smaxp, tok);
+        // = B s (L c + 2 L (h/tp) s): the same integer, fewer 64-bit products (B s < 2^24)
+        const uint32_t Bs32 = k_adm * smaxp;
+        const uint64_t fl = (LC + (uint64_t)K1 * smaxp) * Bs32;
+        const double lat = iter_cost(C.coef, k_adm, fl, Bs32, tok);
         m.t = __dadd_rn(m.t, lat);
-        m.a1 += Bs64;
-        m.a2 += Bs64 * sp64;
+        m.a1 += Bs32;
+        m.a2 += (uint64_t)Bs32 * smaxp;
         m.reqit += k_adm;
         m.iter += 1;
         m.F += freed;
@@ -645,7 +647,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           // m_run = 1, without its search and closed forms (same arithmetic)
           const uint32_t B1 = m.B;
           const uint32_t smax = (uint32_t)((int32_t)m.d + m.maxO);
-          const uint64_t fl = LC * B1 + K1 * (uint64_t)m.S;
+          const uint64_t fl = LC * B1 + (uint64_t)K1 * m.S;
           m.t = __dadd_rn(m.t, iter_cost(C.coef, B1, fl, B1 * smax, m.S));
           m.a1 += B1;
           m.a2 += m.S;
@@ -701,11 +703,12 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
               const uint32_t cnt = min(32u, m_run - done_it);
               double cj = 0.0;
               if ((uint32_t)lane < cnt) {
-                const uint64_t jj = done_it + (uint32_t)lane;
-                const uint64_t S_j = (uint64_t)m.S + (uint64_t)B * jj;
-                const double xc = __ull2double_rn(K0 + K1 * S_j);
-                const double xp = __ull2double_rn((uint64_t)B * (smax0 + jj));
-                const double xs = __ull2double_rn(S_j);
+                // S_j and B (s + j) stay below 256 * l_max < 2^24 (kernel limits)
+                const uint32_t jj = done_it + (uint32_t)lane;
+                const uint32_t S_j = m.S + B * jj;
+                const double xc = __ull2double_rn(K0 + (uint64_t)K1 * S_j);
+                const double xp = __uint2double_rn(B * (smax0 + jj));
+                const double xs = __uint2double_rn(S_j);
                 cj = __dadd_rn(__dadd_rn(__fma_rn(ac, xc, bc), __fma_rn(ap, xp, bp)), __fma_rn(as_, xs, bs_));
               }
               // Exact parallel form of the sequential sum (same doubles as the one-by-one adds):
@@ -765,11 +768,11 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
               }
               __syncwarp();
             }
-          } else if (K0 + K1 * ((uint64_t)m.S + (uint64_t)B * (m_run - 1)) < (1ull << 53)) {
+          } else if (K0 + (uint64_t)K1 * (m.S + B * (m_run - 1)) < (1ull << 53)) {
             // every x of the run is an integer below 2^53: exact fp64 increments == RN conversions
-            double xc = (double)(K0 + K1 * (uint64_t)m.S);
-            const double dxc = (double)(K1 * B), dB = (double)B;
-            double xp = (double)((uint64_t)B * smax0), xs = (double)m.S;
+            double xc = (double)(K0 + (uint64_t)K1 * m.S);
+            const double dxc = (double)((uint64_t)K1 * B), dB = (double)B;
+            double xp = (double)(B * smax0), xs = (double)m.S;
             uint32_t jj = 0;
             do {
               const double tc = __fma_rn(ac, xc, bc);
@@ -785,10 +788,10 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           } else {
             uint32_t jj = 0;
             do {
-              const uint64_t S_j = (uint64_t)m.S + (uint64_t)B * jj;
-              const double tc = __fma_rn(ac, __ull2double_rn(K0 + K1 * S_j), bc);
-              const double tp = __fma_rn(ap, __ull2double_rn((uint64_t)B * (smax0 + jj)), bp);
-              const double ts = __fma_rn(as_, __ull2double_rn(S_j), bs_);
+              const uint32_t S_j = m.S + B * jj;
+              const double tc = __fma_rn(ac, __ull2double_rn(K0 + (uint64_t)K1 * S_j), bc);
+              const double tp = __fma_rn(ap, __uint2double_rn(B * (smax0 + jj)), bp);
+              const double ts = __fma_rn(as_, __uint2double_rn(S_j), bs_);
               t = __dadd_rn(t, __dadd_rn(__dadd_rn(tc, tp), ts));
               ++jj;
             } while (jj < m_run && t < stop_t);
@@ -849,7 +852,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
             const int32_t vo = W.s_fo[vs].y;
             const uint32_t vph = vmeta & 31u;
             const uint32_t l = (uint32_t)(vo + (int32_t)m.d);
-            const uint32_t vg = l - (uint32_t)li[vr];
+            const uint32_t vg = l - (uint32_t)LI_(vr);
             m.F += (int32_t)bs.cdiv(l - 1);
             if (vph == m.needidx) --need;
             __syncwarp();
@@ -871,7 +874,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
             __syncwarp();
             // the victim is the new front of W: shift the window up by one
             {
-              const uint32_t Lv = max((uint32_t)lo[vr], 1u);
+              const uint32_t Lv = max((uint32_t)LO_(vr), 1u);
               wb = (wb - 1u) & 31u;   // a full window drops its last entry, the lane now at wb
               if ((uint32_t)lane == wb) { w_r = vr; w_li = l - vg; w_lo = Lv; w_g = vg; }
               wn = min(wn + 1, 32u);
@@ -890,7 +893,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           const uint32_t B2 = m.B;
           const uint32_t smax = (uint32_t)((int32_t)m.d + m.maxO);
           m.F -= (int32_t)need;
-          const uint64_t fl = LC * B2 + K1 * (uint64_t)m.S;
+          const uint64_t fl = LC * B2 + (uint64_t)K1 * m.S;
           const double lat = iter_cost(C.coef, B2, fl, B2 * smax, m.S);
           m.t = __dadd_rn(m.t, lat);
           m.a1 += B2;
@@ -1064,7 +1067,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           uint32_t rank = 0;
           for (int s2 = 0; s2 < SLOTS; ++s2) rank += W.tmp[s2] < me ? 1u : 0u;
           st[rq] = (SAMU_ST_RUNNING << 28) | rank;
-          gst[rq] = (uint16_t)((uint32_t)(W.s_fo[s].y + (int32_t)m.d) - (uint32_t)li[rq]);
+          gst[rq] = (uint16_t)((uint32_t)(W.s_fo[s].y + (int32_t)m.d) - (uint32_t)LI_(rq));
         }
       }
       for (uint32_t i = lane; i < m.stack_cnt; i += 32) {
@@ -1086,7 +1089,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
       rec.t_end = m.t;
       {   // FLOPs = LC a1 + K1 a2 in u128
         uint64_t lo = LC * m.a1, hi = __umul64hi(LC, m.a1);
-        const uint64_t plo = K1 * m.a2, phi = __umul64hi(K1, m.a2);
+        const uint64_t plo = (uint64_t)K1 * m.a2, phi = __umul64hi((uint64_t)K1, m.a2);
         lo += plo;
         hi += phi + (lo < plo ? 1ull : 0ull);
         rec.flops_lo = lo;

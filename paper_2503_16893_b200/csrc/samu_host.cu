@@ -338,6 +338,8 @@ extern "C" samu_status samu_model_register(samu_ctx* c, int32_t model_id, const 
   if (s.n_layers < 1 || s.hidden < 1 || s.c < 1 || s.l_max < 1 || s.l_max > 65535 || s.tp_mask == 0 ||
       (s.tp_mask >> SAMU_N_TP_SLOTS) || s.kv_bytes_per_token < 1)
     FAIL(c, SAMU_E_INVALID, "model_register: invalid spec");
+  if (2ull * s.n_layers * s.hidden >= (1ull << 32))   // 2 L (h/tp) is a u32 factor in K2
+    FAIL(c, SAMU_E_INVALID, "model_register: 2 L h must stay below 2^32");
   for (int k = 0; k < n_buckets; ++k)
     if (bucket_B[k] < 1 || (k && bucket_B[k] <= bucket_B[k - 1]))
       FAIL(c, SAMU_E_INVALID, "model_register: buckets not strictly increasing");
@@ -626,6 +628,8 @@ struct StatePtrs {
 static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16_t* l_out, const uint16_t* l_in,
                             int32_t T, const StatePtrs& S) {
   if (jobs.empty() || T == 0) return SAMU_OK;
+  if ((uint64_t)T * (uint64_t)c->n_req >= (1ull << 32))   // K2 indexes [trial][request] with u32
+    FAIL(c, SAMU_E_INVALID, "simulate: trials x requests must stay below 2^32 per launch");
   cudaStream_t s = c->stream;
   int max_phase = 0;
   for (auto& j : jobs) max_phase = std::max(max_phase, j.phase);
