@@ -518,8 +518,12 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           }
           if (finish_now && need_rel) W.tmp[n_fin + __popc(bfn & lanemask_lt())] = w_r;
           n_fin += __popc(bfn);
-          if (bfn) freed += (int32_t)__reduce_add_sync(FULL, finish_now ? nb : 0u);
-          if (bst) S_add += __reduce_add_sync(FULL, stay ? p + 1 : 0u);
+          if (bfn) {
+            freed += (int32_t)__reduce_add_sync(FULL, finish_now ? nb : 0u);
+            S_add += __reduce_add_sync(FULL, stay ? p + 1 : 0u);
+          } else {
+            S_add += add_tok + ns;   // every admitted request stays: sum of (p + 1)
+          }
           smaxp = max(smaxp, __reduce_max_sync(FULL, adm ? p : 0u));
           // insert the stays into free slots: the a-th lane with a free slot takes the a-th stay
           if (ns) {
@@ -980,9 +984,16 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
               for (uint32_t c2 = 0; c2 < cnt; ++c2) W.tmp[ex + c2] = W.tmp2[c2 * 32 + lane];
             }
           }
-          n_fin = __reduce_add_sync(FULL, cnt_l);
+          if (BSK >= 16) {
+            // freed blocks (<= 256 * ceil(65535 / 16) = 2^20) and the count (<= 256) in one word
+            const uint32_t pk = __reduce_add_sync(FULL, ((uint32_t)fr_l << 9) | cnt_l);
+            n_fin = pk & 0x1FFu;
+            m.F += (int32_t)(pk >> 9);
+          } else {
+            n_fin = __reduce_add_sync(FULL, cnt_l);
+            m.F += (int32_t)__reduce_add_sync(FULL, (uint32_t)fr_l);
+          }
           K2STAT(12, n_fin);
-          m.F += (int32_t)__reduce_add_sync(FULL, (uint32_t)fr_l);
           m.S -= __reduce_add_sync(FULL, sfin_l);
           m.B -= n_fin;
           m.next_fin = __reduce_min_sync(FULL, lminf);
