@@ -476,18 +476,18 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
           uint32_t mm, add_tok, add_blk;   // admitted count, tokens, blocks
           K2STAT(4, 1);
           const uint32_t slots = min(wn, ms - m.B - k_adm);
-          const uint32_t tot_p = __reduce_add_sync(FULL, p), tot_b = __reduce_add_sync(FULL, nb);
-          if (tot_p + tok <= C.budget && (int32_t)(tot_b + blk) <= m.F) {
-            // the whole window fits the token and block budgets: only the slots bind, no scans
-            mm = slots;
-            add_tok = __reduce_add_sync(FULL, pos < mm ? p : 0u);
-            add_blk = __reduce_add_sync(FULL, pos < mm ? nb : 0u);
-          } else if (slots <= 1u) {
+          if (slots <= 1u) {
             // at most the head can enter (one free slot or one waiting request): no scans
             const uint32_t p0 = __shfl_sync(FULL, p, wb);
             add_tok = p0;
             add_blk = bs.cdiv(p0);
             mm = (wn > 0 && m.B + k_adm < ms && tok + p0 <= C.budget && (int32_t)(blk + add_blk) <= m.F) ? 1u : 0u;
+          } else if (__reduce_add_sync(FULL, p) + tok <= C.budget &&
+                     (int32_t)(__reduce_add_sync(FULL, nb) + blk) <= m.F) {
+            // the whole window fits the token and block budgets: only the slots bind, no scans
+            mm = slots;
+            add_tok = __reduce_add_sync(FULL, pos < mm ? p : 0u);
+            add_blk = __reduce_add_sync(FULL, pos < mm ? nb : 0u);
           } else {
             K2STAT(5, 1);
             // scans in window order: lane i takes position i
