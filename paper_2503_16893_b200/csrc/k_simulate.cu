@@ -488,6 +488,15 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
             mm = slots;
             add_tok = __reduce_add_sync(FULL, pos < mm ? p : 0u);
             add_blk = __reduce_add_sync(FULL, pos < mm ? nb : 0u);
+          } else if (const uint32_t p01 = __shfl_sync(FULL, p, wb) + __shfl_sync(FULL, p, (wb + 1u) & 31u),
+                                    b01 = __shfl_sync(FULL, nb, wb) + __shfl_sync(FULL, nb, (wb + 1u) & 31u);
+                     tok + p01 > C.budget || (int32_t)(blk + b01) > m.F) {
+            // the first two do not fit together (block-bound prefills, e.g. 2k-token chunks): at
+            // most the head enters, no scans
+            const uint32_t p0 = __shfl_sync(FULL, p, wb);
+            add_tok = p0;
+            add_blk = bs.cdiv(p0);
+            mm = (tok + p0 <= C.budget && (int32_t)(blk + add_blk) <= m.F) ? 1u : 0u;
           } else {
             K2STAT(5, 1);
             // scans in window order: lane i takes position i
