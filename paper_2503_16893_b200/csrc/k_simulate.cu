@@ -188,37 +188,17 @@ __device__ const uint64_t* warp_radix_sort(uint64_t* ka, uint32_t* ia, uint64_t*
 static_assert(sizeof(DevCand) * SAMU_K2_CONST_CANDS <= 64 * 1024, "candidate table exceeds the constant bank");
 __constant__ DevCand c_cands[SAMU_K2_CONST_CANDS];
 
-template <int BSK, bool CONSTC>
-// Occupancy: 6 blocks of 4 warps per SM caps registers at 80 for 24 resident warps (C5 step
-// 436 -> 418 ms against 5 blocks at 96 registers, once the cold state moved to shared memory;
-// 7 blocks / 72 registers is slower, 16 warps at 128 registers slower still; see
-// scripts/variants.sh).  SAMU_DEFINES overrides both.
-#ifndef SAMU_K2_MINB
-#define SAMU_K2_MINB 6
-#endif
-__global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_simulate(SimLaunch P) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  // lane id kept in a register: an opaque copy cannot be rematerialised from SR_TID (an S2R
-  // with ~20 cycles of latency) under register pressure (-1.3 % step time);
-  int lane_v = threadIdx.x & 31;
-  asm volatile("" : "+r"(lane_v));
-  const int lane = lane_v;
-  int warp_v = threadIdx.x >> 5;   // the same for the warp index, i.e. the warp's shared block (-3.3 %)
-  asm volatile("" : "+r"(warp_v));
-  const int warp = warp_v;
-  WarpSm& W = reinterpret_cast<WarpSm*>(smem_raw)[warp];
-  const int gw = blockIdx.x * SAMU_WARPS_PER_BLOCK + warp;
-  uint32_t* q = P.scratch_q + (size_t)gw * P.max_q;
-  uint64_t* pkey = P.scratch_key + (size_t)gw * 4 * P.max_p;
-  uint32_t* pidx = P.scratch_idx + (size_t)gw * 4 * P.max_p;
+// One work item (candidate, trial, replica): the whole simulation of one replica-sim.
+// LEAN: the candidate starts from fresh state with independent requests (no carried
+// WorkloadState, no chain successors or cross-node arrivals, no time limit, no per-request
+// outputs) — e.g. the first greedy step of ensembling / routing nodes.  The queue is then the
+// replica's request list itself and the event loop carries none of the dependency / commit /
+// cut machinery (fewer live registers: ~10 % faster on those items).
+template <int BSK, bool CONSTC, bool LEAN>
+__device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSm& W, const int lane, uint32_t* q, uint64_t* pkey,
+                                         uint32_t* pidx, const uint32_t item) {
   const DevApp& A = P.app;
   const int n = A.n_req;
-
-  for (;;) {
-    uint32_t item = 0;
-    if (lane == 0) item = atomicAdd(P.next_item, 1u);
-    item = __shfl_sync(FULL, item, 0);
-    if (item >= (uint32_t)P.n_items) break;
     const uint2 it = P.items[item];
     const uint32_t ci = it.x, k = it.y >> 4, j = it.y & 15u;
     const DevCand& C = CONSTC ? c_cands[ci] : P.cands[ci];
@@ -241,7 +221,9 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
     bs.v_ = C.bs;
     bs.mask_ = C.bs - 1;
     bs.shift_ = __ffs(C.bs) - 1;
-    const bool commit = C.commit && st;
+    const bool commit = !LEAN && C.commit && st;
+    // waiting-queue reads: the replica's request list (LEAN: never appended to) or the scratch ring
+    const uint32_t* qr = LEAN ? C.rep_req + r0 : q;
 
     Sim m;
     m.t = C.resume ? (over ? over[j] : 0.0) : C.load_s;
@@ -265,6 +247,10 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
     uint32_t* sidx = pidx + 2 * (size_t)P.max_p;
     uint32_t n_run = 0, n_pre = 0, n_q = 0, n_cls = 0;
     bool all_done = true;
+    if (LEAN) {
+      n_heads = r1 - r0;
+      all_done = r1 == r0;
+    } else {
     for (uint32_t base = r0; base < r1; base += 32) {
       const uint32_t idx = base + lane;
       const bool valid = idx < r1;
@@ -310,14 +296,15 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
       }
       if (__ballot_sync(FULL, valid && s != SAMU_ST_DONE)) all_done = false;
     }
+    }
     site = (int32_t)__reduce_max_sync(FULL, (uint32_t)site);
     m.err = __reduce_max_sync(FULL, (uint32_t)(-m.err)) ? SAMU_E_STATE : 0;
     m.n_front = C.resume ? n_pre : n_run + n_pre;
-    if (n_pend > (uint32_t)P.max_p || n_cls > (uint32_t)P.max_p ||
-        m.n_front + n_heads + n_q > (uint32_t)P.max_q) { m.err = SAMU_E_STATE; site = 3; }
+    if (!LEAN && (n_pend > (uint32_t)P.max_p || n_cls > (uint32_t)P.max_p ||
+                  m.n_front + n_heads + n_q > (uint32_t)P.max_q)) { m.err = SAMU_E_STATE; site = 3; }
     if (C.resume && n_run > ms) { m.err = SAMU_E_STATE; site = 4; }
     m.q_tail = m.n_front + n_heads + n_q;
-    if (!m.err && st) {
+    if (!LEAN && !m.err && st) {
       // heads after the front region, in index order
       uint32_t nh = 0;
       for (uint32_t base = r0; base < r1; base += 32) {
@@ -377,7 +364,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
     // ---- pending cross-node arrivals in (ready, index) order: stable LSD radix sort ----
     const uint64_t* pk = pkey;
     const uint32_t* pi = pidx;
-    if (!m.err && n_pend > 1) {
+    if (!LEAN && !m.err && n_pend > 1) {
       uint32_t* si;
       pk = warp_radix_sort(pkey, pidx, pkey + P.max_p, pidx + P.max_p, n_pend, W.tmp, lane, &si);
       pi = si;
@@ -393,7 +380,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
     m.stop = fmin(tau, W.next_ready);
     const uint32_t K1 = (uint32_t)C.K1;   // 2 L (h/tp) (< 2^32, checked by the host)
     const uint64_t LC = C.LC;   // L c
-    const bool need_rel = fio || fto || commit || C.has_succ;
+    const bool need_rel = !LEAN && (fio || fto || commit || C.has_succ);
     bool cut = false;
     // per-lane summaries of this lane's slots: min finish index, max (l - d)
     uint32_t lminf = FULL;
@@ -418,7 +405,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
     // ---- main loop (c25) ----
     while (!m.err) {
       K2STAT(1, 1);
-      if (m.t >= m.stop) {   // stop time or a pending arrival reached
+      if (!LEAN && m.t >= m.stop) {   // stop time or a pending arrival reached
         if (m.t >= W.tau) { cut = true; break; }
         // pending cross-node arrivals with ready <= t join the back of W
         while (W.pend_ptr < W.n_pend && W.next_ready <= m.t) {
@@ -435,7 +422,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
       }
       const uint32_t wlen = m.stack_cnt + (m.q_tail - m.q_head);
       if (m.B == 0 && wlen == 0) {
-        if (W.pend_ptr < W.n_pend && W.next_ready != CUDART_INF) { m.t = W.next_ready; continue; }
+        if (!LEAN && W.pend_ptr < W.n_pend && W.next_ready != CUDART_INF) { m.t = W.next_ready; continue; }
         break;
       }
       // refill the window so it holds min(32, |W|) entries
@@ -448,8 +435,8 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
             if (pos < m.stack_cnt) { r = W.stk_req[m.stack_cnt - 1 - pos]; g = W.stk_g[m.stack_cnt - 1 - pos]; }
             else {
               const uint32_t qp = m.q_head + pos - m.stack_cnt;
-              r = q[qp];
-              g = qp < m.n_front ? (uint32_t)gst[r] : 0u;   // recompute front keeps its tokens
+              r = qr[qp];
+              g = (!LEAN && qp < m.n_front) ? (uint32_t)gst[r] : 0u;   // recompute front keeps its tokens
             }
             w_r = r;
             w_li = LI_(r);
@@ -617,8 +604,8 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
               if (pos < m.stack_cnt) { r = W.stk_req[m.stack_cnt - 1 - pos]; g = W.stk_g[m.stack_cnt - 1 - pos]; }
               else {
                 const uint32_t qp = m.q_head + pos - m.stack_cnt;
-                r = q[qp];
-                g = qp < m.n_front ? (uint32_t)gst[r] : 0u;
+                r = qr[qp];
+                g = (!LEAN && qp < m.n_front) ? (uint32_t)gst[r] : 0u;
               }
               w_r = r;
               w_li = LI_(r);
@@ -1011,7 +998,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
         }
       }
       // ---- finish records + chain successor release (c19), for this iteration's finishers ----
-      if (n_fin && need_rel) {
+      if (!LEAN && n_fin && need_rel) {
         const uint32_t itx = m.iter - 1;
         if (n_fin <= 32) {
           // one finisher per lane; released successors ranked in registers (index order, c19)
@@ -1121,17 +1108,52 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
       P.rep_rec[((size_t)ci * P.n_trials + k) * 16 + j] = rec;
     }
     __syncwarp();
+}
+#undef LO_
+#undef LI_
+
+// Occupancy: 6 blocks of 4 warps per SM caps registers at 80 for 24 resident warps (C5 step
+// 436 -> 418 ms against 5 blocks at 96 registers, once the cold state moved to shared memory;
+// 7 blocks / 72 registers is slower, 16 warps at 128 registers slower still; see
+// scripts/variants.sh).  SAMU_DEFINES overrides both.
+#ifndef SAMU_K2_MINB
+#define SAMU_K2_MINB 6
+#endif
+// A LEAN launch holds only items of LEAN candidates (DevCand::lean); the host issues LEAN and
+// general items as two launches (one kernel holding both paths is slower: twice the code).
+template <int BSK, bool CONSTC, bool LEAN>
+__global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_simulate(SimLaunch P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // lane id kept in a register: an opaque copy cannot be rematerialised from SR_TID (an S2R
+  // with ~20 cycles of latency) under register pressure (-1.3 % step time);
+  int lane_v = threadIdx.x & 31;
+  asm volatile("" : "+r"(lane_v));
+  const int lane = lane_v;
+  int warp_v = threadIdx.x >> 5;   // the same for the warp index, i.e. the warp's shared block (-3.3 %)
+  asm volatile("" : "+r"(warp_v));
+  const int warp = warp_v;
+  WarpSm& W = reinterpret_cast<WarpSm*>(smem_raw)[warp];
+  const int gw = blockIdx.x * SAMU_WARPS_PER_BLOCK + warp;
+  uint32_t* q = P.scratch_q + (size_t)gw * P.max_q;
+  uint64_t* pkey = P.scratch_key + (size_t)gw * 4 * P.max_p;
+  uint32_t* pidx = P.scratch_idx + (size_t)gw * 4 * P.max_p;
+  for (;;) {
+    uint32_t item = 0;
+    if (lane == 0) item = atomicAdd(P.next_item, 1u);
+    item = __shfl_sync(FULL, item, 0);
+    if (item >= (uint32_t)P.n_items) break;
+    sim_item<BSK, CONSTC, LEAN>(P, W, lane, q, pkey, pidx, item);
   }
 }
 
 int32_t simulate_smem_bytes() { return (int32_t)(sizeof(WarpSm) * SAMU_WARPS_PER_BLOCK); }
 
-template <int BSK, bool CONSTC>
+template <int BSK, bool CONSTC, bool LEAN>
 static cudaError_t prepare_one(int smem, int* bpsm) {
-  cudaError_t e = cudaFuncSetAttribute(k_simulate<BSK, CONSTC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = cudaFuncSetAttribute(k_simulate<BSK, CONSTC, LEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   int a = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_simulate<BSK, CONSTC>, 32 * SAMU_WARPS_PER_BLOCK, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_simulate<BSK, CONSTC, LEAN>, 32 * SAMU_WARPS_PER_BLOCK, smem);
   *bpsm = *bpsm < a ? *bpsm : a;
   return e;
 }
@@ -1140,24 +1162,28 @@ cudaError_t simulate_prepare(int* blocks_per_sm) {
   const int smem = simulate_smem_bytes();
   *blocks_per_sm = 1 << 30;
   cudaError_t e;
-  if ((e = prepare_one<16, true>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  if ((e = prepare_one<16, false>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  if ((e = prepare_one<0, true>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  if ((e = prepare_one<0, false>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  if ((e = prepare_one<-1, true>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  return prepare_one<-1, false>(smem, blocks_per_sm);
+  if ((e = prepare_one<16, true, false>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<16, true, true>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<16, false, false>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<16, false, true>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<0, true, false>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<0, false, false>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<-1, true, false>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  return prepare_one<-1, false, false>(smem, blocks_per_sm);
 }
 
 template <bool CONSTC>
-static void launch_variant(const SimLaunch& L, uint32_t block_size, int32_t n_blocks, int smem, cudaStream_t s) {
+static void launch_variant(const SimLaunch& L, uint32_t block_size, bool lean, int32_t n_blocks, int smem,
+                           cudaStream_t s) {
   const dim3 blk(32 * SAMU_WARPS_PER_BLOCK);
-  if (block_size == 16) k_simulate<16, CONSTC><<<n_blocks, blk, smem, s>>>(L);
-  else if ((block_size & (block_size - 1)) == 0) k_simulate<0, CONSTC><<<n_blocks, blk, smem, s>>>(L);
-  else k_simulate<-1, CONSTC><<<n_blocks, blk, smem, s>>>(L);
+  if (block_size == 16 && lean) k_simulate<16, CONSTC, true><<<n_blocks, blk, smem, s>>>(L);
+  else if (block_size == 16) k_simulate<16, CONSTC, false><<<n_blocks, blk, smem, s>>>(L);
+  else if ((block_size & (block_size - 1)) == 0) k_simulate<0, CONSTC, false><<<n_blocks, blk, smem, s>>>(L);
+  else k_simulate<-1, CONSTC, false><<<n_blocks, blk, smem, s>>>(L);
 }
 
 cudaError_t launch_simulate(const SimLaunch& L, const DevCand* host_cands, int32_t n_blocks, uint32_t block_size,
-                            cudaStream_t s) {
+                            bool lean, cudaStream_t s) {
   const int smem = simulate_smem_bytes();
   if (L.n_cands <= SAMU_K2_CONST_CANDS) {
     // The table is one per device and process while contexts may launch on their own streams:
@@ -1173,10 +1199,10 @@ cudaError_t launch_simulate(const SimLaunch& L, const DevCand* host_cands, int32
     if ((e = cudaStreamWaitEvent(s, last[dev], 0)) != cudaSuccess) return e;
     e = cudaMemcpyToSymbolAsync(c_cands, host_cands, sizeof(DevCand) * (size_t)L.n_cands, 0, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return e;
-    launch_variant<true>(L, block_size, n_blocks, smem, s);
+    launch_variant<true>(L, block_size, lean, n_blocks, smem, s);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     return cudaEventRecord(last[dev], s);
   }
-  launch_variant<false>(L, block_size, n_blocks, smem, s);
+  launch_variant<false>(L, block_size, lean, n_blocks, smem, s);
   return cudaGetLastError();
 }

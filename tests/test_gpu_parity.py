@@ -88,10 +88,14 @@ def _sim_parity(w, cands, T, tb=0, tau=None):
     g = recs(out)
     fi = out["fin_iter"].cpu().numpy().view(np.uint32)
     ft = out["fin_t"].cpu().numpy()
+    # the same batch without per-request outputs: independent nodes without a time limit run on
+    # K2's LEAN path (k_simulate<16, ., true>), the rest on the general one
+    g_lean = recs(S.samu_simulate_batch(cands, glo, gli, time_limit=tau))
     for ci, cd in enumerate(cands):
         node, dp, tp = cd[:3]
         o, ofi, oft = P.simulate(node, dp, tp, lo, li, tau=None if tau is None else tau[ci], want_fin=True)
         assert_rec_equal(g[ci], o, f"cand {cd}")
+        assert_rec_equal(g_lean[ci], o, f"cand {cd} without per-request outputs")
         a, b = w.node_range(node)
         assert np.array_equal(fi[ci][:, a:b], ofi[:, a:b]), f"finish iterations differ for {cd}"
         assert np.array_equal(ft[ci][:, a:b], oft[:, a:b]), f"finish times differ for {cd}"
