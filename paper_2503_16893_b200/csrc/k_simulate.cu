@@ -189,14 +189,15 @@ static_assert(sizeof(DevCand) * SAMU_K2_CONST_CANDS <= 64 * 1024, "candidate tab
 __constant__ DevCand c_cands[SAMU_K2_CONST_CANDS];
 
 // One work item (candidate, trial, replica): the whole simulation of one replica-sim.
-// LEAN: the candidate starts from fresh state with independent requests (no carried
-// WorkloadState, no chain successors or cross-node arrivals, no time limit, no per-request
-// outputs) — e.g. the first greedy step of ensembling / routing nodes.  The queue is then the
-// replica's request list itself and the event loop carries none of the dependency / commit /
-// cut machinery (fewer live registers: ~10 % faster on those items).
-template <int BSK, bool CONSTC, bool LEAN>
+// MODE (DevCand::mode): 0 general; 2 FRESH: fresh state, no cross-node arrivals, no time limit,
+// no per-request outputs (chain successors allowed) — the event loop carries no commit / cut /
+// arrival machinery; 1 LEAN: FRESH without chain successors (e.g. the first greedy step of
+// ensembling / routing nodes) — the queue is then the replica's request list itself.  Fewer live
+// registers: ~10 % faster on those items.
+template <int BSK, bool CONSTC, int MODE>
 __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSm& W, const int lane, uint32_t* q, uint64_t* pkey,
                                          uint32_t* pidx, const uint32_t item) {
+  constexpr bool LEAN = MODE == 1, FRESH = MODE != 0;
   const DevApp& A = P.app;
   const int n = A.n_req;
     const uint2 it = P.items[item];
@@ -221,13 +222,13 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSm& W, const in
     bs.v_ = C.bs;
     bs.mask_ = C.bs - 1;
     bs.shift_ = __ffs(C.bs) - 1;
-    const bool commit = !LEAN && C.commit && st;
+    const bool commit = !FRESH && C.commit && st;
     // waiting-queue reads: the replica's request list (LEAN: never appended to) or the scratch ring
     const uint32_t* qr = LEAN ? C.rep_req + r0 : q;
 
     Sim m;
     m.t = C.resume ? (over ? over[j] : 0.0) : C.load_s;
-    double tau = C.tau ? C.tau[k] : (C.tau_rec ? C.tau_rec[k].t_end : CUDART_INF);
+    double tau = FRESH ? CUDART_INF : C.tau ? C.tau[k] : (C.tau_rec ? C.tau_rec[k].t_end : CUDART_INF);
     m.a1 = m.a2 = m.reqit = 0;
     m.iter = 0; m.d = 0; m.needidx = 0; m.B = 0; m.S = 0; m.next_rank = 0;
     m.F = C.blocks; m.maxO = INT_MIN; m.next_fin = FULL;
@@ -304,7 +305,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSm& W, const in
                   m.n_front + n_heads + n_q > (uint32_t)P.max_q)) { m.err = SAMU_E_STATE; site = 3; }
     if (C.resume && n_run > ms) { m.err = SAMU_E_STATE; site = 4; }
     m.q_tail = m.n_front + n_heads + n_q;
-    if (!LEAN && !m.err && st) {
+    if (!FRESH && !m.err && st) {
       // heads after the front region, in index order
       uint32_t nh = 0;
       for (uint32_t base = r0; base < r1; base += 32) {
@@ -364,7 +365,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSm& W, const in
     // ---- pending cross-node arrivals in (ready, index) order: stable LSD radix sort ----
     const uint64_t* pk = pkey;
     const uint32_t* pi = pidx;
-    if (!LEAN && !m.err && n_pend > 1) {
+    if (!FRESH && !m.err && n_pend > 1) {
       uint32_t* si;
       pk = warp_radix_sort(pkey, pidx, pkey + P.max_p, pidx + P.max_p, n_pend, W.tmp, lane, &si);
       pi = si;
@@ -380,7 +381,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSm& W, const in
     m.stop = fmin(tau, W.next_ready);
     const uint32_t K1 = (uint32_t)C.K1;   // 2 L (h/tp) (< 2^32, checked by the host)
     const uint64_t LC = C.LC;   // L c
-    const bool need_rel = !LEAN && (fio || fto || commit || C.has_succ);
+    const bool need_rel = LEAN ? false : FRESH ? (bool)C.has_succ : (fio || fto || commit || C.has_succ);
     bool cut = false;
     // per-lane summaries of this lane's slots: min finish index, max (l - d)
     uint32_t lminf = FULL;
@@ -405,7 +406,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSm& W, const in
     // ---- main loop (c25) ----
     while (!m.err) {
       K2STAT(1, 1);
-      if (!LEAN && m.t >= m.stop) {   // stop time or a pending arrival reached
+      if (!FRESH && m.t >= m.stop) {   // stop time or a pending arrival reached
         if (m.t >= W.tau) { cut = true; break; }
         // pending cross-node arrivals with ready <= t join the back of W
         while (W.pend_ptr < W.n_pend && W.next_ready <= m.t) {
@@ -422,7 +423,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSm& W, const in
       }
       const uint32_t wlen = m.stack_cnt + (m.q_tail - m.q_head);
       if (m.B == 0 && wlen == 0) {
-        if (!LEAN && W.pend_ptr < W.n_pend && W.next_ready != CUDART_INF) { m.t = W.next_ready; continue; }
+        if (!FRESH && W.pend_ptr < W.n_pend && W.next_ready != CUDART_INF) { m.t = W.next_ready; continue; }
         break;
       }
       // refill the window so it holds min(32, |W|) entries
@@ -436,7 +437,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSm& W, const in
             else {
               const uint32_t qp = m.q_head + pos - m.stack_cnt;
               r = qr[qp];
-              g = (!LEAN && qp < m.n_front) ? (uint32_t)gst[r] : 0u;   // recompute front keeps its tokens
+              g = (!FRESH && qp < m.n_front) ? (uint32_t)gst[r] : 0u;   // recompute front keeps its tokens
             }
             w_r = r;
             w_li = LI_(r);
@@ -605,7 +606,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSm& W, const in
               else {
                 const uint32_t qp = m.q_head + pos - m.stack_cnt;
                 r = qr[qp];
-                g = (!LEAN && qp < m.n_front) ? (uint32_t)gst[r] : 0u;
+                g = (!FRESH && qp < m.n_front) ? (uint32_t)gst[r] : 0u;
               }
               w_r = r;
               w_li = LI_(r);
@@ -1006,9 +1007,13 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSm& W, const in
           const uint32_t r = v ? W.tmp[lane] : 0u;
           int32_t sr = -1;
           if (v) {
-            if (fio) fio[r] = itx;
-            if (fto) fto[r] = m.t;
-            if (commit) { st[r] = SAMU_ST_DONE << 28; ft[r] = m.t; }
+            if (!FRESH) {
+              if (!FRESH) {
+                if (fio) fio[r] = itx;
+                if (fto) fto[r] = m.t;
+                if (commit) { st[r] = SAMU_ST_DONE << 28; ft[r] = m.t; }
+              }
+            }
             if (C.has_succ) sr = __ldg(A.succ + r);
           }
           const uint32_t br = __ballot_sync(FULL, sr >= 0);
@@ -1029,9 +1034,11 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSm& W, const in
             const uint32_t r = v ? W.tmp[i] : 0u;
             int32_t sr = -1;
             if (v) {
-              if (fio) fio[r] = itx;
-              if (fto) fto[r] = m.t;
-              if (commit) { st[r] = SAMU_ST_DONE << 28; ft[r] = m.t; }
+              if (!FRESH) {
+                if (fio) fio[r] = itx;
+                if (fto) fto[r] = m.t;
+                if (commit) { st[r] = SAMU_ST_DONE << 28; ft[r] = m.t; }
+              }
               if (C.has_succ) sr = __ldg(A.succ + r);
             }
             const uint32_t br = __ballot_sync(FULL, sr >= 0);
@@ -1119,9 +1126,9 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSm& W, const in
 #ifndef SAMU_K2_MINB
 #define SAMU_K2_MINB 6
 #endif
-// A LEAN launch holds only items of LEAN candidates (DevCand::lean); the host issues LEAN and
-// general items as two launches (one kernel holding both paths is slower: twice the code).
-template <int BSK, bool CONSTC, bool LEAN>
+// A launch holds only items of one MODE (DevCand::mode); the host issues one launch per mode
+// present (one kernel holding several paths is slower: a multiple of the code footprint).
+template <int BSK, bool CONSTC, int MODE>
 __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_simulate(SimLaunch P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // lane id kept in a register: an opaque copy cannot be rematerialised from SR_TID (an S2R
@@ -1142,18 +1149,18 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
     if (lane == 0) item = atomicAdd(P.next_item, 1u);
     item = __shfl_sync(FULL, item, 0);
     if (item >= (uint32_t)P.n_items) break;
-    sim_item<BSK, CONSTC, LEAN>(P, W, lane, q, pkey, pidx, item);
+    sim_item<BSK, CONSTC, MODE>(P, W, lane, q, pkey, pidx, item);
   }
 }
 
 int32_t simulate_smem_bytes() { return (int32_t)(sizeof(WarpSm) * SAMU_WARPS_PER_BLOCK); }
 
-template <int BSK, bool CONSTC, bool LEAN>
+template <int BSK, bool CONSTC, int MODE>
 static cudaError_t prepare_one(int smem, int* bpsm) {
-  cudaError_t e = cudaFuncSetAttribute(k_simulate<BSK, CONSTC, LEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = cudaFuncSetAttribute(k_simulate<BSK, CONSTC, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   int a = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_simulate<BSK, CONSTC, LEAN>, 32 * SAMU_WARPS_PER_BLOCK, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_simulate<BSK, CONSTC, MODE>, 32 * SAMU_WARPS_PER_BLOCK, smem);
   *bpsm = *bpsm < a ? *bpsm : a;
   return e;
 }
@@ -1162,28 +1169,31 @@ cudaError_t simulate_prepare(int* blocks_per_sm) {
   const int smem = simulate_smem_bytes();
   *blocks_per_sm = 1 << 30;
   cudaError_t e;
-  if ((e = prepare_one<16, true, false>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  if ((e = prepare_one<16, true, true>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  if ((e = prepare_one<16, false, false>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  if ((e = prepare_one<16, false, true>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  if ((e = prepare_one<0, true, false>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  if ((e = prepare_one<0, false, false>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  if ((e = prepare_one<-1, true, false>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  return prepare_one<-1, false, false>(smem, blocks_per_sm);
+  if ((e = prepare_one<16, true, 0>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<16, true, 1>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<16, true, 2>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<16, false, 0>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<16, false, 1>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<16, false, 2>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<0, true, 0>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<0, false, 0>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<-1, true, 0>(smem, blocks_per_sm)) != cudaSuccess) return e;
+  return prepare_one<-1, false, 0>(smem, blocks_per_sm);
 }
 
 template <bool CONSTC>
-static void launch_variant(const SimLaunch& L, uint32_t block_size, bool lean, int32_t n_blocks, int smem,
+static void launch_variant(const SimLaunch& L, uint32_t block_size, int mode, int32_t n_blocks, int smem,
                            cudaStream_t s) {
   const dim3 blk(32 * SAMU_WARPS_PER_BLOCK);
-  if (block_size == 16 && lean) k_simulate<16, CONSTC, true><<<n_blocks, blk, smem, s>>>(L);
-  else if (block_size == 16) k_simulate<16, CONSTC, false><<<n_blocks, blk, smem, s>>>(L);
-  else if ((block_size & (block_size - 1)) == 0) k_simulate<0, CONSTC, false><<<n_blocks, blk, smem, s>>>(L);
-  else k_simulate<-1, CONSTC, false><<<n_blocks, blk, smem, s>>>(L);
+  if (block_size == 16 && mode == 1) k_simulate<16, CONSTC, 1><<<n_blocks, blk, smem, s>>>(L);
+  else if (block_size == 16 && mode == 2) k_simulate<16, CONSTC, 2><<<n_blocks, blk, smem, s>>>(L);
+  else if (block_size == 16) k_simulate<16, CONSTC, 0><<<n_blocks, blk, smem, s>>>(L);
+  else if ((block_size & (block_size - 1)) == 0) k_simulate<0, CONSTC, 0><<<n_blocks, blk, smem, s>>>(L);
+  else k_simulate<-1, CONSTC, 0><<<n_blocks, blk, smem, s>>>(L);
 }
 
 cudaError_t launch_simulate(const SimLaunch& L, const DevCand* host_cands, int32_t n_blocks, uint32_t block_size,
-                            bool lean, cudaStream_t s) {
+                            int mode, cudaStream_t s) {
   const int smem = simulate_smem_bytes();
   if (L.n_cands <= SAMU_K2_CONST_CANDS) {
     // The table is one per device and process while contexts may launch on their own streams:
@@ -1199,10 +1209,10 @@ cudaError_t launch_simulate(const SimLaunch& L, const DevCand* host_cands, int32
     if ((e = cudaStreamWaitEvent(s, last[dev], 0)) != cudaSuccess) return e;
     e = cudaMemcpyToSymbolAsync(c_cands, host_cands, sizeof(DevCand) * (size_t)L.n_cands, 0, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return e;
-    launch_variant<true>(L, block_size, lean, n_blocks, smem, s);
+    launch_variant<true>(L, block_size, mode, n_blocks, smem, s);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     return cudaEventRecord(last[dev], s);
   }
-  launch_variant<false>(L, block_size, lean, n_blocks, smem, s);
+  launch_variant<false>(L, block_size, mode, n_blocks, smem, s);
   return cudaGetLastError();
 }

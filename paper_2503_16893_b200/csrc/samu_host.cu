@@ -116,7 +116,7 @@ struct samu_ctx {
   std::map<std::pair<int, int>, std::vector<uint32_t>> rep_off_host;
 
   // launch scratch
-  DevBuf d_cands, d_items, d_items_lean, d_counter, d_rep_rec, d_scratch_q, d_scratch_key, d_scratch_idx, d_error;
+  DevBuf d_cands, d_items[3], d_counter, d_rep_rec, d_scratch_q, d_scratch_key, d_scratch_idx, d_error;
   DevBuf d_sum, d_gather_send, d_gather_recv;
   int sim_blocks_per_sm = 0;
 
@@ -677,9 +677,11 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
       D.fin_t_out = J.fin_t_out;
       D.fin_iter_out = J.fin_iter_out;
       D.out_rec = J.out_rec;
-      // K2 LEAN path: fresh state, independent requests, no cut, no per-request outputs
-      D.lean = (S.st == nullptr && !D.resume && !D.commit && !D.has_succ && !D.src_fin && !D.tau && !D.tau_rec &&
-                !D.fin_t_out && !D.fin_iter_out && c->node_input[node] < 0 && c->eng.block_size == 16) ? 1 : 0;
+      // K2 path (DevCand::mode): FRESH = fresh state, no cross-node arrivals, no cut, no per-request
+      // outputs; LEAN = FRESH without chain successors
+      const bool fresh = S.st == nullptr && !D.resume && !D.commit && !D.src_fin && !D.tau && !D.tau_rec &&
+                         !D.fin_t_out && !D.fin_iter_out && c->node_input[node] < 0 && c->eng.block_size == 16;
+      D.mode = !fresh ? 0 : D.has_succ ? 2 : 1;
       const std::vector<uint32_t>& ho = c->rep_off_host.at({node, cd.dp});
       uint32_t mx = 0;
       for (int j = 0; j < cd.dp; ++j) mx = std::max(mx, ho[j + 1] - ho[j]);
@@ -691,18 +693,18 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
     std::vector<int> order(idx.size());
     for (size_t x = 0; x < idx.size(); ++x) order[x] = (int)x;
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
-    // two launches: candidates with dependency / state / cut machinery, then the LEAN ones (a
-    // single kernel holding both code paths runs ~10 % slower: twice the instruction footprint)
-    std::vector<uint2> items, items_lean;
+    // one launch per K2 mode present (a single kernel holding several code paths runs ~10 %
+    // slower: a multiple of the instruction footprint)
+    std::vector<uint2> items[3];
     for (int x : order)
       for (int k = 0; k < T; ++k)
         for (int j = 0; j < dc[x].dp; ++j)
-          (dc[x].lean ? items_lean : items).push_back(make_uint2((uint32_t)x, ((uint32_t)k << 4) | (uint32_t)j));
+          items[dc[x].mode].push_back(make_uint2((uint32_t)x, ((uint32_t)k << 4) | (uint32_t)j));
     SimLaunch L;
     L.app = dev_app(c);
     L.n_cands = (int32_t)idx.size();
     L.n_trials = T;
-    L.n_items = (int32_t)items.size();
+    L.n_items = 0;   // set per launch (one launch per K2 mode)
     L.l_out = l_out;
     L.l_in = l_in;
     L.st = S.st;
@@ -712,7 +714,7 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
     L.error = c->d_error.as<int32_t>();
     {
       const int bpsm = c->sim_blocks_per_sm;
-      const int64_t warps_needed = (int64_t)std::max(items.size(), items_lean.size());
+      const int64_t warps_needed = (int64_t)std::max({items[0].size(), items[1].size(), items[2].size()});
       int n_blocks = (int)std::min<int64_t>((int64_t)c->n_sm * bpsm, (warps_needed + SAMU_WARPS_PER_BLOCK - 1) / SAMU_WARPS_PER_BLOCK);
       n_blocks = std::max(n_blocks, 1);
       const size_t n_warps = (size_t)n_blocks * SAMU_WARPS_PER_BLOCK;
@@ -720,13 +722,12 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
       CK(c, c->d_scratch_key.ensure(sizeof(uint64_t) * n_warps * 4 * max_p));
       CK(c, c->d_scratch_idx.ensure(sizeof(uint32_t) * n_warps * 4 * max_p));
       CK(c, upload(c->d_cands, dc, s));
-      CK(c, upload(c->d_items, items, s));
-      CK(c, upload(c->d_items_lean, items_lean, s));
-      CK(c, c->d_counter.ensure(2 * sizeof(uint32_t)));
-      CK(c, cudaMemsetAsync(c->d_counter.p, 0, 2 * sizeof(uint32_t), s));
+      for (int md = 0; md < 3; ++md) CK(c, upload(c->d_items[md], items[md], s));
+      CK(c, c->d_counter.ensure(3 * sizeof(uint32_t)));
+      CK(c, cudaMemsetAsync(c->d_counter.p, 0, 3 * sizeof(uint32_t), s));
       CK(c, c->d_rep_rec.ensure(sizeof(samu_trial_rec) * 16 * idx.size() * T));
       L.cands = c->d_cands.as<DevCand>();
-      L.items = c->d_items.as<uint2>();
+      L.items = c->d_items[0].as<uint2>();
       L.next_item = c->d_counter.as<uint32_t>();
       L.rep_rec = c->d_rep_rec.as<samu_trial_rec>();
       L.scratch_q = c->d_scratch_q.as<uint32_t>();
@@ -734,14 +735,15 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
       L.scratch_idx = c->d_scratch_idx.as<uint32_t>();
       L.max_q = (int32_t)max_q;
       L.max_p = (int32_t)max_p;
-      if (!items.empty()) CK(c, launch_simulate(L, dc.data(), n_blocks, (uint32_t)c->eng.block_size, false, s));
-      if (!items_lean.empty()) {
-        SimLaunch LL = L;
-        LL.items = c->d_items_lean.as<uint2>();
-        LL.n_items = (int32_t)items_lean.size();
-        LL.next_item = c->d_counter.as<uint32_t>() + 1;
-        CK(c, launch_simulate(LL, dc.data(), n_blocks, (uint32_t)c->eng.block_size, true, s));
-        c->launches += 1;
+      int n_launched = 0;
+      for (int md : {0, 2, 1}) {
+        if (items[md].empty()) continue;
+        SimLaunch LM = L;
+        LM.items = c->d_items[md].as<uint2>();
+        LM.n_items = (int32_t)items[md].size();
+        LM.next_item = c->d_counter.as<uint32_t>() + md;
+        CK(c, launch_simulate(LM, dc.data(), n_blocks, (uint32_t)c->eng.block_size, md, s));
+        c->launches += n_launched++ ? 1 : 0;
       }
     }
     CK(c, launch_combine(L.rep_rec, L.cands, (int32_t)idx.size(), T, S.over, c->n_nodes, s));

@@ -38,7 +38,7 @@ struct DevEcdf {
 // One candidate (node, plan) as the simulation kernel sees it.
 struct DevCand {
   int32_t node, dp, tp, resume, commit, has_succ;
-  int32_t lean;                // fresh state, independent requests, no cut, no per-request outputs (K2 LEAN path)
+  int32_t mode;                // K2 path: 0 general, 2 FRESH (fresh state, no arrivals / cut / outputs), 1 LEAN (FRESH, no successors)
   uint32_t max_seqs, bs, budget;
   int32_t blocks;              // KV blocks per replica (c5)
   uint32_t L, h_tp;            // layers, h / tp
@@ -88,7 +88,7 @@ cudaError_t launch_ecdf_table(const uint32_t* values, const uint32_t* cum, int32
 cudaError_t launch_dense_coeff(const uint32_t* bucket_B, int32_t nb, const double* coeff_slot,
                                uint32_t max_seqs, double* out, cudaStream_t s);
 cudaError_t launch_simulate(const SimLaunch& L, const DevCand* host_cands, int32_t n_blocks, uint32_t block_size,
-                            bool lean, cudaStream_t s);
+                            int mode, cudaStream_t s);
 cudaError_t simulate_prepare(int* blocks_per_sm);
 
 int32_t simulate_smem_bytes();

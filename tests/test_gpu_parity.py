@@ -231,6 +231,9 @@ def test_dependency_parity_c4():
         oe, ofe, fte = P.simulate(1, dpe, tpe, lo, li, src_fin=fts, want_fin=True)
         assert_rec_equal(g[0], os_, "summariser")
         assert_rec_equal(g[1], oe, "evaluator")
+        # the summariser alone without per-request outputs runs on K2's FRESH path (chains, no
+        # state / cut / outputs)
+        assert_rec_equal(recs(S.samu_simulate_batch([(0, dps, tps)], glo, gli))[0], os_, "summariser, FRESH path")
         fi = out["fin_iter"].cpu().numpy().view(np.uint32)
         a, b = w.node_range(0)
         assert np.array_equal(fi[0][:, a:b], ofs[:, a:b])
