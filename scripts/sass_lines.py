@@ -17,7 +17,7 @@ import tempfile
 
 rep, so = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
-fn = sys.argv[4] if len(sys.argv) > 4 else "_Z10k_simulateILb1EEv9SimLaunch"
+fn = sys.argv[4] if len(sys.argv) > 4 else "_Z10k_simulateILi16ELb1ELi1EEv9SimLaunch"
 
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=tmp, capture_output=True)
