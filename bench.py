@@ -295,7 +295,8 @@ def main():
                        "parallelism": f"trials sharded dp{world}",
                        "l2": f"inputs larger than L2: lengths {2 * 2 * T * w.n_req / 1e6:.0f} MB re-sampled every step"},
             "req_iters_per_s": reqit / (ms / 1e3), "sim_iters_per_s": iters / (ms / 1e3),
-            "roofline": {"bound": "alu", "kernel": "k_simulate", "achieved": achieved / 1e12, "peak": peak / 1e12,
+            "roofline": {"bound": "alu", "kernel": "k_simulate (K2: one launch per mode, FRESH + LEAN at C5)",
+                         "achieved": achieved / 1e12, "peak": peak / 1e12,
                          "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": ncu_traffic(w.name),
                          "peak_source": "fp64: 148 SM x 64 FMA lanes x 2 x sm clock (derived, DESIGN.md section 6)",
