@@ -41,14 +41,16 @@ namespace {
 constexpr uint32_t FULL = 0xFFFFFFFFu;
 constexpr int SLOTS = 256;
 
-struct WarpSm {
+// SMALL (LEAN launches): no finish / release lists, 2 KB less, so 28 warps fit an SM
+template <bool SMALL>
+struct WarpSmT {
   uint32_t s_req[SLOTS];     // request id of an occupied slot
   int2 s_fo[SLOTS];          // (decode index at which it finishes, l - d)
   uint32_t s_meta[SLOTS];    // admission rank << 5 | phase  (phase = (o - 1) mod bs)
   uint32_t stk_req[SLOTS];   // preempted stack, top = front of W
   uint32_t stk_g[SLOTS];
-  uint32_t tmp[SLOTS];       // finished requests of the current iteration / radix histogram
-  uint32_t tmp2[SLOTS];      // staging / released successors
+  uint32_t tmp[SMALL ? 1 : SLOTS];    // finished requests of the current iteration / radix histogram
+  uint32_t tmp2[SMALL ? 1 : SLOTS];   // staging / released successors
   uint32_t hist[32];         // running requests per phase
   uint32_t adm_req[32], adm_meta[32];
   int2 adm_fo[32];
@@ -61,6 +63,7 @@ struct WarpSm {
   uint32_t pend_ptr, n_pend, n_heads;
   int32_t site;
 };
+using WarpSm = WarpSmT<false>;
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
@@ -195,7 +198,7 @@ __constant__ DevCand c_cands[SAMU_K2_CONST_CANDS];
 // ensembling / routing nodes) — the queue is then the replica's request list itself.  Fewer live
 // registers: ~10 % faster on those items.
 template <int BSK, bool CONSTC, int MODE>
-__device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSm& W, const int lane, uint32_t* q, uint64_t* pkey,
+__device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1>& W, const int lane, uint32_t* q, uint64_t* pkey,
                                          uint32_t* pidx, const uint32_t item) {
   constexpr bool LEAN = MODE == 1, FRESH = MODE != 0;
   const DevApp& A = P.app;
@@ -965,7 +968,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSm& W, const in
                   sfin_l += l_now;
                   atomicSub(&W.hist[W.s_meta[s] & 31u], 1u);
                   occ &= ~(1u << jj);
-                  W.tmp2[cnt * 32 + lane] = W.s_req[s];   // staged per lane (<= 8 each)
+                  if (need_rel) W.tmp2[cnt * 32 + lane] = W.s_req[s];   // staged per lane (<= 8 each)
                   ++cnt;
                 } else {
                   mn = min(mn, (uint32_t)fo.x);
@@ -1126,10 +1129,15 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSm& W, const in
 #ifndef SAMU_K2_MINB
 #define SAMU_K2_MINB 6
 #endif
+// LEAN launches: 7 blocks (28 warps, 72 registers; the smaller shared block fits)
+#ifndef SAMU_K2_MINB_LEAN
+#define SAMU_K2_MINB_LEAN 7
+#endif
 // A launch holds only items of one MODE (DevCand::mode); the host issues one launch per mode
 // present (one kernel holding several paths is slower: a multiple of the code footprint).
 template <int BSK, bool CONSTC, int MODE>
-__global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_simulate(SimLaunch P) {
+__global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, MODE == 1 ? SAMU_K2_MINB_LEAN : SAMU_K2_MINB)
+    k_simulate(SimLaunch P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // lane id kept in a register: an opaque copy cannot be rematerialised from SR_TID (an S2R
   // with ~20 cycles of latency) under register pressure (-1.3 % step time);
@@ -1139,7 +1147,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
   int warp_v = threadIdx.x >> 5;   // the same for the warp index, i.e. the warp's shared block (-3.3 %)
   asm volatile("" : "+r"(warp_v));
   const int warp = warp_v;
-  WarpSm& W = reinterpret_cast<WarpSm*>(smem_raw)[warp];
+  WarpSmT<MODE == 1>& W = reinterpret_cast<WarpSmT<MODE == 1>*>(smem_raw)[warp];
   const int gw = blockIdx.x * SAMU_WARPS_PER_BLOCK + warp;
   uint32_t* q = P.scratch_q + (size_t)gw * P.max_q;
   uint64_t* pkey = P.scratch_key + (size_t)gw * 4 * P.max_p;
@@ -1153,10 +1161,14 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, SAMU_K2_MINB) k_sim
   }
 }
 
-int32_t simulate_smem_bytes() { return (int32_t)(sizeof(WarpSm) * SAMU_WARPS_PER_BLOCK); }
+int32_t simulate_smem_bytes(int mode) {
+  return (int32_t)((mode == 1 ? sizeof(WarpSmT<true>) : sizeof(WarpSmT<false>)) * SAMU_WARPS_PER_BLOCK);
+}
 
 template <int BSK, bool CONSTC, int MODE>
-static cudaError_t prepare_one(int smem, int* bpsm) {
+static cudaError_t prepare_one(int* bpsm_modes) {
+  const int smem = simulate_smem_bytes(MODE);
+  int* bpsm = bpsm_modes + MODE;
   cudaError_t e = cudaFuncSetAttribute(k_simulate<BSK, CONSTC, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   int a = 0;
@@ -1165,20 +1177,20 @@ static cudaError_t prepare_one(int smem, int* bpsm) {
   return e;
 }
 
-cudaError_t simulate_prepare(int* blocks_per_sm) {
-  const int smem = simulate_smem_bytes();
-  *blocks_per_sm = 1 << 30;
+// resident blocks per SM for each K2 mode (the minimum over that mode's instantiations)
+cudaError_t simulate_prepare(int blocks_per_sm[3]) {
+  blocks_per_sm[0] = blocks_per_sm[1] = blocks_per_sm[2] = 1 << 30;
   cudaError_t e;
-  if ((e = prepare_one<16, true, 0>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  if ((e = prepare_one<16, true, 1>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  if ((e = prepare_one<16, true, 2>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  if ((e = prepare_one<16, false, 0>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  if ((e = prepare_one<16, false, 1>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  if ((e = prepare_one<16, false, 2>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  if ((e = prepare_one<0, true, 0>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  if ((e = prepare_one<0, false, 0>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  if ((e = prepare_one<-1, true, 0>(smem, blocks_per_sm)) != cudaSuccess) return e;
-  return prepare_one<-1, false, 0>(smem, blocks_per_sm);
+  if ((e = prepare_one<16, true, 0>(blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<16, true, 1>(blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<16, true, 2>(blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<16, false, 0>(blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<16, false, 1>(blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<16, false, 2>(blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<0, true, 0>(blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<0, false, 0>(blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<-1, true, 0>(blocks_per_sm)) != cudaSuccess) return e;
+  return prepare_one<-1, false, 0>(blocks_per_sm);
 }
 
 template <bool CONSTC>
@@ -1194,7 +1206,7 @@ static void launch_variant(const SimLaunch& L, uint32_t block_size, int mode, in
 
 cudaError_t launch_simulate(const SimLaunch& L, const DevCand* host_cands, int32_t n_blocks, uint32_t block_size,
                             int mode, cudaStream_t s) {
-  const int smem = simulate_smem_bytes();
+  const int smem = simulate_smem_bytes(mode);
   if (L.n_cands <= SAMU_K2_CONST_CANDS) {
     // The table is one per device and process while contexts may launch on their own streams:
     // the copy waits for the previous table user (any stream) and this launch becomes the next.

@@ -118,7 +118,7 @@ struct samu_ctx {
   // launch scratch
   DevBuf d_cands, d_items[3], d_counter, d_rep_rec, d_scratch_q, d_scratch_key, d_scratch_idx, d_error;
   DevBuf d_sum, d_gather_send, d_gather_recv;
-  int sim_blocks_per_sm = 0;
+  int sim_blocks_per_sm[3] = {0, 0, 0};   // resident K2 blocks per SM, per K2 mode
 
   // stats
   int64_t n_sims = 0;
@@ -633,11 +633,11 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
   cudaStream_t s = c->stream;
   int max_phase = 0;
   for (auto& j : jobs) max_phase = std::max(max_phase, j.phase);
-  if (!c->sim_blocks_per_sm) {
-    int bpsm = 0;
-    CK(c, simulate_prepare(&bpsm));
-    if (bpsm < 1) FAIL(c, SAMU_E_CUDA, "simulate: kernel does not fit on an SM");
-    c->sim_blocks_per_sm = bpsm;
+  if (!c->sim_blocks_per_sm[0]) {
+    int bpsm[3] = {0, 0, 0};
+    CK(c, simulate_prepare(bpsm));
+    if (bpsm[0] < 1 || bpsm[1] < 1 || bpsm[2] < 1) FAIL(c, SAMU_E_CUDA, "simulate: kernel does not fit on an SM");
+    for (int md = 0; md < 3; ++md) c->sim_blocks_per_sm[md] = bpsm[md];
   }
   CK(c, c->d_error.ensure(2 * sizeof(int32_t)));
   CK(c, cudaMemsetAsync(c->d_error.p, 0, 2 * sizeof(int32_t), s));
@@ -713,11 +713,14 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
     L.over = S.over;
     L.error = c->d_error.as<int32_t>();
     {
-      const int bpsm = c->sim_blocks_per_sm;
-      const int64_t warps_needed = (int64_t)std::max({items[0].size(), items[1].size(), items[2].size()});
-      int n_blocks = (int)std::min<int64_t>((int64_t)c->n_sm * bpsm, (warps_needed + SAMU_WARPS_PER_BLOCK - 1) / SAMU_WARPS_PER_BLOCK);
-      n_blocks = std::max(n_blocks, 1);
-      const size_t n_warps = (size_t)n_blocks * SAMU_WARPS_PER_BLOCK;
+      // persistent grid per mode: resident blocks x SMs, no more warps than items
+      int n_blocks[3];
+      size_t n_warps = SAMU_WARPS_PER_BLOCK;   // scratch rings: modes 0 and 2 (LEAN uses none)
+      for (int md = 0; md < 3; ++md) {
+        const int64_t want = ((int64_t)items[md].size() + SAMU_WARPS_PER_BLOCK - 1) / SAMU_WARPS_PER_BLOCK;
+        n_blocks[md] = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->n_sm * c->sim_blocks_per_sm[md], want));
+        if (md != 1) n_warps = std::max(n_warps, (size_t)n_blocks[md] * SAMU_WARPS_PER_BLOCK);
+      }
       CK(c, c->d_scratch_q.ensure(sizeof(uint32_t) * n_warps * max_q));
       CK(c, c->d_scratch_key.ensure(sizeof(uint64_t) * n_warps * 4 * max_p));
       CK(c, c->d_scratch_idx.ensure(sizeof(uint32_t) * n_warps * 4 * max_p));
@@ -742,7 +745,7 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
         LM.items = c->d_items[md].as<uint2>();
         LM.n_items = (int32_t)items[md].size();
         LM.next_item = c->d_counter.as<uint32_t>() + md;
-        CK(c, launch_simulate(LM, dc.data(), n_blocks, (uint32_t)c->eng.block_size, md, s));
+        CK(c, launch_simulate(LM, dc.data(), n_blocks[md], (uint32_t)c->eng.block_size, md, s));
         c->launches += n_launched++ ? 1 : 0;
       }
     }

@@ -89,9 +89,9 @@ cudaError_t launch_dense_coeff(const uint32_t* bucket_B, int32_t nb, const doubl
                                uint32_t max_seqs, double* out, cudaStream_t s);
 cudaError_t launch_simulate(const SimLaunch& L, const DevCand* host_cands, int32_t n_blocks, uint32_t block_size,
                             int mode, cudaStream_t s);
-cudaError_t simulate_prepare(int* blocks_per_sm);
+cudaError_t simulate_prepare(int blocks_per_sm[3]);   // per K2 mode
 
-int32_t simulate_smem_bytes();
+int32_t simulate_smem_bytes(int mode);
 cudaError_t launch_combine(const samu_trial_rec* rep_rec, const DevCand* cands, int32_t n_cands, int32_t n_trials,
                            double* over, int32_t n_nodes, cudaStream_t s);
 cudaError_t launch_summary(const samu_trial_rec* recs, int32_t n_cands, int32_t n_trials,
