@@ -182,6 +182,8 @@ def main():
     ap.add_argument("--trials", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--planner-trials", type=int, default=128,
+                    help="also time one full Algorithm 1 run (samu_plan_greedy, rows a1-a12) at this trial count; 0 = off")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -278,6 +280,26 @@ def main():
                                              w.ecdf_values[m].nbytes + w.ecdf_cum[m].nbytes for m in range(len(w.models)))
     d2h = nc * 48
 
+    # the whole planner (Algorithm 1: every greedy inner step incl. truncated sims, stage scoring
+    # and argmax, row a12) once, wall time around the call (synchronising), max over ranks
+    planner = None
+    if args.planner_trials > 0:
+        Tp = min(args.planner_trials, T)
+        S.samu_plan_greedy(w.seed, 1)            # warm-up: allocations for the planner's buffers
+        barrier()
+        t0 = time.perf_counter()
+        plan = S.samu_plan_greedy(w.seed, Tp)
+        torch.cuda.synchronize()
+        plan_s = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([plan_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            plan_s = t.item()
+        planner = {"algorithm": "greedy (Algorithm 1, P:542-574)", "workload": w.name, "trials": Tp,
+                   "seconds": plan_s, "stages": len(plan["stages"]), "candidate_evaluations": plan["n_cand_evals"],
+                   "candidate_trial_sims": plan["n_sims"], "candidate_trial_sims_per_s": plan["n_sims"] / plan_s,
+                   "planned_total_s": plan["total"]}
+
     if rank == 0:
         pk = peaks()
         clock = clk.summary()
@@ -306,6 +328,8 @@ def main():
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches), "clocks": clock,
         }
+        if planner:
+            line["planner"] = planner
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = {k: v for k, v in time_oracle(w, cands, args.cpu_seconds).items()
                                     if k in ("value", "unit", "cores", "kind", "sample", "req_iters_per_s")}
