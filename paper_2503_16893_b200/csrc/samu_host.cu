@@ -116,7 +116,7 @@ struct samu_ctx {
   std::map<std::pair<int, int>, std::vector<uint32_t>> rep_off_host;
 
   // launch scratch
-  DevBuf d_cands, d_items[3], d_counter, d_rep_rec, d_scratch_q, d_scratch_key, d_scratch_idx, d_error;
+  DevBuf d_cands, d_items, d_counter, d_rep_rec, d_scratch_q, d_scratch_key, d_scratch_idx, d_error;
   DevBuf d_sum, d_gather_send, d_gather_recv;
   int sim_blocks_per_sm[3] = {0, 0, 0};   // resident K2 blocks per SM, per K2 mode
 
@@ -616,6 +616,7 @@ struct SimJob {
   double* fin_t_out = nullptr;         // [T][n]
   uint32_t* fin_iter_out = nullptr;    // [T][n]
   samu_trial_rec* out_rec = nullptr;   // [T]
+  bool fresh_node = false;             // the node's WorkloadState is FRESH in every trial (never committed)
 };
 
 struct StatePtrs {
@@ -679,7 +680,7 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
       D.out_rec = J.out_rec;
       // K2 path (DevCand::mode): FRESH = fresh state, no cross-node arrivals, no cut, no per-request
       // outputs; LEAN = FRESH without chain successors
-      const bool fresh = S.st == nullptr && !D.resume && !D.commit && !D.src_fin && !D.tau && !D.tau_rec &&
+      const bool fresh = (S.st == nullptr || J.fresh_node) && !D.resume && !D.commit && !D.src_fin && !D.tau && !D.tau_rec &&
                          !D.fin_t_out && !D.fin_iter_out && c->node_input[node] < 0 && c->eng.block_size == 16;
       D.mode = !fresh ? 0 : D.has_succ ? 2 : 1;
       const std::vector<uint32_t>& ho = c->rep_off_host.at({node, cd.dp});
@@ -695,6 +696,16 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
     // one launch per K2 mode present (a single kernel holding several code paths runs ~10 %
     // slower: a multiple of the instruction footprint)
+    {
+      // small batches (e.g. the planner's later inner steps) run as one general launch: a launch per
+      // mode only pays off when each covers several waves of the persistent grid
+      int64_t cnt[3] = {0, 0, 0};
+      for (size_t x = 0; x < dc.size(); ++x) cnt[dc[x].mode] += (int64_t)T * dc[x].dp;
+      const int64_t wave = (int64_t)c->n_sm * 24;
+      const bool split = cnt[0] + cnt[1] + cnt[2] >= 4 * wave;
+      for (DevCand& D : dc)
+        if (!split || cnt[D.mode] < wave) D.mode = 0;
+    }
     std::vector<uint2> items[3];
     for (int x : order)
       for (int k = 0; k < T; ++k)
@@ -725,12 +736,18 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
       CK(c, c->d_scratch_key.ensure(sizeof(uint64_t) * n_warps * 4 * max_p));
       CK(c, c->d_scratch_idx.ensure(sizeof(uint32_t) * n_warps * 4 * max_p));
       CK(c, upload(c->d_cands, dc, s));
-      for (int md = 0; md < 3; ++md) CK(c, upload(c->d_items[md], items[md], s));
+      std::vector<uint2> all_items;   // one upload: [mode 0 | mode 1 | mode 2]
+      size_t item_off[3];
+      for (int md = 0; md < 3; ++md) {
+        item_off[md] = all_items.size();
+        all_items.insert(all_items.end(), items[md].begin(), items[md].end());
+      }
+      CK(c, upload(c->d_items, all_items, s));
       CK(c, c->d_counter.ensure(3 * sizeof(uint32_t)));
       CK(c, cudaMemsetAsync(c->d_counter.p, 0, 3 * sizeof(uint32_t), s));
       CK(c, c->d_rep_rec.ensure(sizeof(samu_trial_rec) * 16 * idx.size() * T));
       L.cands = c->d_cands.as<DevCand>();
-      L.items = c->d_items[0].as<uint2>();
+      L.items = c->d_items.as<uint2>();
       L.next_item = c->d_counter.as<uint32_t>();
       L.rep_rec = c->d_rep_rec.as<samu_trial_rec>();
       L.scratch_q = c->d_scratch_q.as<uint32_t>();
@@ -742,7 +759,7 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
       for (int md : {0, 2, 1}) {
         if (items[md].empty()) continue;
         SimLaunch LM = L;
-        LM.items = c->d_items[md].as<uint2>();
+        LM.items = c->d_items.as<uint2>() + item_off[md];
         LM.n_items = (int32_t)items[md].size();
         LM.next_item = c->d_counter.as<uint32_t>() + md;
         CK(c, launch_simulate(LM, dc.data(), n_blocks[md], (uint32_t)c->eng.block_size, md, s));
@@ -933,6 +950,7 @@ struct Greedy {
   std::vector<int> pending_tau;            // f* full slot whose records give tau, or -1
   int64_t evals = 0;
   std::vector<bool> is_input;
+  std::vector<bool> touched;               // node committed in some stage (its state is no longer FRESH)
   bool preempt = true;                  // false: no-preemption ablation (reading c29)
   const uint32_t* known = nullptr;      // device known output lengths (reading c30)
   std::vector<int> undone_now;          // per node: unfinished in some trial (current stage)
@@ -995,6 +1013,7 @@ struct Greedy {
     full_slot[key] = slot;
     SimJob J;
     J.cand = samu_candidate{e.node, e.dp, e.tp, resumes(e) ? 1 : 0, -1, 0};
+    J.fresh_node = !touched[e.node];
     J.phase = phase;
     J.src_fin = sf;
     if (is_input[e.node]) {
@@ -1026,6 +1045,7 @@ struct Greedy {
     cut_slot[key] = slot;
     SimJob J;
     J.cand = samu_candidate{e.node, e.dp, e.tp, resumes(e) ? 1 : 0, -1, 0};
+    J.fresh_node = !touched[e.node];
     J.phase = 0;
     J.src_fin = sf;
     pending.push_back(J);             // tau_k = T_f*^(k) (this rank's trials), resolved at flush
@@ -1281,6 +1301,7 @@ struct Greedy {
     trial_share(T, c->world, c->rank, &tb, &Tl);
     cudaStream_t s = c->stream;
     is_input.assign(c->n_nodes, false);
+    touched.assign(c->n_nodes, false);
     for (int v = 0; v < c->n_nodes; ++v) if (c->node_input[v] >= 0) is_input[c->node_input[v]] = true;
     const size_t tn = (size_t)std::max(Tl, 1) * n;
     CK(c, lo.ensure(sizeof(uint16_t) * tn));
@@ -1341,6 +1362,7 @@ struct Greedy {
     }
     RET(run_jobs(c, jobs, lo.as<uint16_t>(), li.as<uint16_t>(), Tl, S));
     CK(c, samu_count(c, launch_rebase(st.as<uint32_t>(), fin_t.as<double>(), (int64_t)Tl * n, rec(fslot) + tb, (int32_t)n, s)));
+    for (const Ent& e : Es) touched[e.node] = true;
     prev = Es;
     return SAMU_OK;
   }
