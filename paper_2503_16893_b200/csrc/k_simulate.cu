@@ -203,9 +203,16 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1>&
   constexpr bool LEAN = MODE == 1, FRESH = MODE != 0;
   const DevApp& A = P.app;
   const int n = A.n_req;
-    const uint2 it = P.items[item];
-    const uint32_t ci = it.x, k = it.y >> 4, j = it.y & 15u;
+    // decode the item: candidate by binary search over the launch's offsets, then (trial, replica)
+    uint32_t lo_x = 0, hi_x = (uint32_t)P.n_ord;   // off[lo_x] <= item < off[hi_x]
+    while (hi_x - lo_x > 1) {
+      const uint32_t mid = (lo_x + hi_x) >> 1;
+      if (__ldg(P.off + mid) <= item) lo_x = mid; else hi_x = mid;
+    }
+    const uint32_t ci = __ldg(P.ord + lo_x);
     const DevCand& C = CONSTC ? c_cands[ci] : P.cands[ci];
+    const uint32_t rel = item - __ldg(P.off + lo_x), dpc = (uint32_t)C.dp;
+    const uint32_t k = rel / dpc, j = rel - k * dpc;
     const size_t tb = (size_t)k * n;
     // sampled lengths of this trial, indexed with 32-bit offsets from the kernel parameters (the
     // host guarantees local trials x requests < 2^32): one add + one wide multiply per load

@@ -706,11 +706,31 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
       for (DevCand& D : dc)
         if (!split || cnt[D.mode] < wave) D.mode = 0;
     }
-    std::vector<uint2> items[3];
-    for (int x : order)
-      for (int k = 0; k < T; ++k)
-        for (int j = 0; j < dc[x].dp; ++j)
-          items[dc[x].mode].push_back(make_uint2((uint32_t)x, ((uint32_t)k << 4) | (uint32_t)j));
+    {
+      int64_t total = 0;
+      for (const DevCand& D : dc) total += (int64_t)T * D.dp;
+      if (total >= ((int64_t)1 << 31)) FAIL(c, SAMU_E_INVALID, "simulate: too many work items (trials x replicas)");
+    }
+    // per mode: candidate order and item offsets (the device decodes item -> (candidate, trial, replica))
+    std::vector<uint32_t> ord_off;   // [mode 0 ord | off][mode 1 ...][mode 2 ...]
+    size_t ord_at[3], off_at[3];
+    int64_t n_items[3];
+    int n_ord[3];
+    for (int md = 0; md < 3; ++md) {
+      std::vector<uint32_t> ordm, offm{0};
+      for (int x : order)
+        if (dc[x].mode == md) {
+          ordm.push_back((uint32_t)x);
+          offm.push_back(offm.back() + (uint32_t)(T * dc[x].dp));
+        }
+      n_items[md] = offm.back();
+      n_ord[md] = (int)ordm.size();
+      ord_at[md] = ord_off.size();
+      ord_off.insert(ord_off.end(), ordm.begin(), ordm.end());
+      off_at[md] = ord_off.size();
+      ord_off.insert(ord_off.end(), offm.begin(), offm.end());
+    }
+
     SimLaunch L;
     L.app = dev_app(c);
     L.n_cands = (int32_t)idx.size();
@@ -728,7 +748,7 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
       int n_blocks[3];
       size_t n_warps = SAMU_WARPS_PER_BLOCK;   // scratch rings: modes 0 and 2 (LEAN uses none)
       for (int md = 0; md < 3; ++md) {
-        const int64_t want = ((int64_t)items[md].size() + SAMU_WARPS_PER_BLOCK - 1) / SAMU_WARPS_PER_BLOCK;
+        const int64_t want = (n_items[md] + SAMU_WARPS_PER_BLOCK - 1) / SAMU_WARPS_PER_BLOCK;
         n_blocks[md] = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->n_sm * c->sim_blocks_per_sm[md], want));
         if (md != 1) n_warps = std::max(n_warps, (size_t)n_blocks[md] * SAMU_WARPS_PER_BLOCK);
       }
@@ -736,18 +756,14 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
       CK(c, c->d_scratch_key.ensure(sizeof(uint64_t) * n_warps * 4 * max_p));
       CK(c, c->d_scratch_idx.ensure(sizeof(uint32_t) * n_warps * 4 * max_p));
       CK(c, upload(c->d_cands, dc, s));
-      std::vector<uint2> all_items;   // one upload: [mode 0 | mode 1 | mode 2]
-      size_t item_off[3];
-      for (int md = 0; md < 3; ++md) {
-        item_off[md] = all_items.size();
-        all_items.insert(all_items.end(), items[md].begin(), items[md].end());
-      }
-      CK(c, upload(c->d_items, all_items, s));
+      CK(c, upload(c->d_items, ord_off, s));
       CK(c, c->d_counter.ensure(3 * sizeof(uint32_t)));
       CK(c, cudaMemsetAsync(c->d_counter.p, 0, 3 * sizeof(uint32_t), s));
       CK(c, c->d_rep_rec.ensure(sizeof(samu_trial_rec) * 16 * idx.size() * T));
       L.cands = c->d_cands.as<DevCand>();
-      L.items = c->d_items.as<uint2>();
+      L.ord = nullptr;
+      L.off = nullptr;
+      L.n_ord = 0;
       L.next_item = c->d_counter.as<uint32_t>();
       L.rep_rec = c->d_rep_rec.as<samu_trial_rec>();
       L.scratch_q = c->d_scratch_q.as<uint32_t>();
@@ -757,10 +773,12 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
       L.max_p = (int32_t)max_p;
       int n_launched = 0;
       for (int md : {0, 2, 1}) {
-        if (items[md].empty()) continue;
+        if (n_items[md] == 0) continue;
         SimLaunch LM = L;
-        LM.items = c->d_items.as<uint2>() + item_off[md];
-        LM.n_items = (int32_t)items[md].size();
+        LM.ord = c->d_items.as<uint32_t>() + ord_at[md];
+        LM.off = c->d_items.as<uint32_t>() + off_at[md];
+        LM.n_ord = n_ord[md];
+        LM.n_items = (int32_t)n_items[md];
         LM.next_item = c->d_counter.as<uint32_t>() + md;
         CK(c, launch_simulate(LM, dc.data(), n_blocks[md], (uint32_t)c->eng.block_size, md, s));
         c->launches += n_launched++ ? 1 : 0;

@@ -62,7 +62,11 @@ struct SimLaunch {
   const DevCand* cands;
   int32_t n_cands;
   int32_t n_trials;
-  const uint2* items;          // (cand, trial*16 + replica), longest first
+  // work items (candidate, trial, replica), longest candidates first: item i belongs to candidate
+  // ord[x] for off[x] <= i < off[x + 1] (off[x + 1] - off[x] = trials x dp), then trial-major
+  const uint32_t* ord;         // [n_ord] candidate indices
+  const uint32_t* off;         // [n_ord + 1] item offsets
+  int32_t n_ord;
   int32_t n_items;
   uint32_t* next_item;         // work counter
   const uint16_t* l_out;       // [T][n]
