@@ -380,15 +380,20 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1>&
       pk = warp_radix_sort(pkey, pidx, pkey + P.max_p, pidx + P.max_p, n_pend, W.tmp, lane, &si);
       pi = si;
     }
-    W.tau = tau;
-    W.next_ready = n_pend ? kdouble(pk[0]) : CUDART_INF;
-    W.pk = pk;
-    W.pi = pi;
-    W.pend_ptr = 0;
-    W.n_pend = n_pend;
-    W.n_heads = n_heads;
-    W.site = site;
-    m.stop = fmin(tau, W.next_ready);
+    const double next_ready0 = n_pend ? kdouble(pk[0]) : CUDART_INF;
+    __syncwarp();   // lane 0 writes the warp's cold state; every later reader is behind a __syncwarp
+    if (lane == 0) {
+      W.tau = tau;
+      W.next_ready = next_ready0;
+      W.pk = pk;
+      W.pi = pi;
+      W.pend_ptr = 0;
+      W.n_pend = n_pend;
+      W.n_heads = n_heads;
+      W.site = site;
+    }
+    __syncwarp();
+    m.stop = fmin(tau, next_ready0);
     const uint32_t K1 = (uint32_t)C.K1;   // 2 L (h/tp) (< 2^32, checked by the host)
     const uint64_t LC = C.LC;   // L c
     const bool need_rel = LEAN ? false : FRESH ? (bool)C.has_succ : (fio || fto || commit || C.has_succ);
@@ -417,19 +422,27 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1>&
     while (!m.err) {
       K2STAT(1, 1);
       if (!FRESH && m.t >= m.stop) {   // stop time or a pending arrival reached
-        if (m.t >= W.tau) { cut = true; break; }
+        const double tau_w = W.tau;
+        if (m.t >= tau_w) { cut = true; break; }
         // pending cross-node arrivals with ready <= t join the back of W
-        while (W.pend_ptr < W.n_pend && W.next_ready <= m.t) {
-          const uint32_t i = W.pend_ptr + lane;
-          const bool ok = i < W.n_pend && kdouble(W.pk[i]) <= m.t;
+        const uint32_t n_pend_w = W.n_pend;
+        const uint64_t* pk_w = W.pk;
+        uint32_t pend_ptr = W.pend_ptr;
+        double next_ready = W.next_ready;
+        while (pend_ptr < n_pend_w && next_ready <= m.t) {
+          const uint32_t i = pend_ptr + lane;
+          const bool ok = i < n_pend_w && kdouble(pk_w[i]) <= m.t;
           const uint32_t b = __ballot_sync(FULL, ok);
           const uint32_t cnt = (b == FULL) ? 32u : (uint32_t)(__ffs(~b) - 1);
           if ((uint32_t)lane < cnt) q[m.q_tail + lane] = W.pi[i];
           m.q_tail += cnt;
-          W.pend_ptr += cnt;
-          W.next_ready = W.pend_ptr < W.n_pend ? kdouble(W.pk[W.pend_ptr]) : CUDART_INF;
+          pend_ptr += cnt;
+          next_ready = pend_ptr < n_pend_w ? kdouble(pk_w[pend_ptr]) : CUDART_INF;
         }
-        m.stop = fmin(W.tau, W.next_ready);
+        __syncwarp();
+        if (lane == 0) { W.pend_ptr = pend_ptr; W.next_ready = next_ready; }
+        __syncwarp();
+        m.stop = fmin(tau_w, next_ready);
       }
       const uint32_t wlen = m.stack_cnt + (m.q_tail - m.q_head);
       if (m.B == 0 && wlen == 0) {
@@ -649,7 +662,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1>&
           m.maxO = __reduce_max_sync(FULL, lmaxo);
         }
       } else {
-        if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; W.site = 9; break; }
+        if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; if (lane == 0) W.site = 9; break; }
         // ================= decode run (c9): uniform iterations until an event ===============
         const uint32_t need1 = W.hist[m.needidx];
         if (m.next_fin == m.d + 1 && (int32_t)need1 <= m.F) {
@@ -894,7 +907,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1>&
             K2STAT(9, 1);
             m.B -= 1;
             m.S -= l;
-            if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; W.site = 10; break; }
+            if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; if (lane == 0) W.site = 10; break; }
           }
           if (m.err) break;
           m.next_fin = __reduce_min_sync(FULL, lminf);

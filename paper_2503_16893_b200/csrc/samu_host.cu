@@ -702,9 +702,13 @@ static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16
       int64_t cnt[3] = {0, 0, 0};
       for (size_t x = 0; x < dc.size(); ++x) cnt[dc[x].mode] += (int64_t)T * dc[x].dp;
       const int64_t wave = (int64_t)c->n_sm * 24;
-      const bool split = cnt[0] + cnt[1] + cnt[2] >= 4 * wave;
+      // SAMU_K2_MODES=always|never overrides the size rule (tests run the LEAN / FRESH paths on
+      // small batches; "never" runs everything on the general path)
+      const char* pol = std::getenv("SAMU_K2_MODES");
+      const bool always = pol && std::strcmp(pol, "always") == 0, never = pol && std::strcmp(pol, "never") == 0;
+      const bool split = !never && (always || cnt[0] + cnt[1] + cnt[2] >= 4 * wave);
       for (DevCand& D : dc)
-        if (!split || cnt[D.mode] < wave) D.mode = 0;
+        if (!split || (!always && cnt[D.mode] < wave)) D.mode = 0;
     }
     {
       int64_t total = 0;

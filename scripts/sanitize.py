@@ -13,6 +13,9 @@ for name, kw in [("c2", dict(n_prompts=60)), ("c4", dict(n_docs=20)), ("c5", dic
              for (dp, tp) in S.samu_enumerate_plans(v)[:3] if not (w.pred[w.node == v] >= 0).any() or
              (w.node[np.maximum(w.pred[w.node == v], 0)] == v).all()]
     S.samu_simulate_batch(cands, lo, li, summary=True, want_fin_iter=True, want_fin_t=True)
+    os.environ["SAMU_K2_MODES"] = "always"   # the LEAN / FRESH paths on this small batch too
+    S.samu_simulate_batch(cands, lo, li, summary=True)
+    del os.environ["SAMU_K2_MODES"]
     st = S.fresh_state(2)
     S.samu_simulate_batch([cands[0][:3] + (0, -1, 1)], lo, li, state=st, time_limit=np.array([[5.0, 7.0]]))
     S.samu_simulate_batch([cands[0][:3] + (1, -1, 0), (cands[0][0], 1, 1, 0, -1, 0)], lo, li, state=st)

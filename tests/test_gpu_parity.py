@@ -4,6 +4,9 @@ Bar (BASELINE.json north_star): sampled lengths, per-request finish iterations, 
 greedy plan bit-exact; fp64 totals within 1e-9 rel — asserted here as exact equality, since
 both sides evaluate the same operations in the same order (readings c17, c22, c24).
 """
+import contextlib
+import os
+
 import numpy as np
 import pytest
 
@@ -26,6 +29,20 @@ def gpu(w):
     S = Samu(0)
     S.load_workload(w)
     return S
+
+
+@contextlib.contextmanager
+def k2_modes(policy):
+    """SAMU_K2_MODES: "always" runs K2's LEAN / FRESH paths even on batches below the size rule."""
+    old = os.environ.get("SAMU_K2_MODES")
+    os.environ["SAMU_K2_MODES"] = policy
+    try:
+        yield
+    finally:
+        if old is None:
+            del os.environ["SAMU_K2_MODES"]
+        else:
+            os.environ["SAMU_K2_MODES"] = old
 
 
 def u16(t):
@@ -89,8 +106,9 @@ def _sim_parity(w, cands, T, tb=0, tau=None):
     fi = out["fin_iter"].cpu().numpy().view(np.uint32)
     ft = out["fin_t"].cpu().numpy()
     # the same batch without per-request outputs: independent nodes without a time limit run on
-    # K2's LEAN path (k_simulate<16, ., true>), the rest on the general one
-    g_lean = recs(S.samu_simulate_batch(cands, glo, gli, time_limit=tau))
+    # K2's LEAN path (k_simulate<16, ., 1>), the rest on the general one
+    with k2_modes("always"):
+        g_lean = recs(S.samu_simulate_batch(cands, glo, gli, time_limit=tau))
     for ci, cd in enumerate(cands):
         node, dp, tp = cd[:3]
         o, ofi, oft = P.simulate(node, dp, tp, lo, li, tau=None if tau is None else tau[ci], want_fin=True)
@@ -233,7 +251,9 @@ def test_dependency_parity_c4():
         assert_rec_equal(g[1], oe, "evaluator")
         # the summariser alone without per-request outputs runs on K2's FRESH path (chains, no
         # state / cut / outputs)
-        assert_rec_equal(recs(S.samu_simulate_batch([(0, dps, tps)], glo, gli))[0], os_, "summariser, FRESH path")
+        with k2_modes("always"):
+            g0 = recs(S.samu_simulate_batch([(0, dps, tps)], glo, gli))[0]
+        assert_rec_equal(g0, os_, "summariser, FRESH path")
         fi = out["fin_iter"].cpu().numpy().view(np.uint32)
         a, b = w.node_range(0)
         assert np.array_equal(fi[0][:, a:b], ofs[:, a:b])
