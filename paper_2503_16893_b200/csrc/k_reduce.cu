@@ -5,6 +5,8 @@
 // how trials were sharded across GPUs.
 #include "samu_internal.cuh"
 
+#include <algorithm>
+
 #include <math_constants.h>
 
 namespace {
@@ -94,6 +96,11 @@ __global__ void k_summary(const samu_trial_rec* __restrict__ recs, int32_t T, sa
     o.mean_req_iters = __ddiv_rn(__ull2double_rn(ri), (double)T);
     out[c] = o;
   }
+}
+
+// fill n doubles with v (finish-time buffers start at +inf: never finished)
+__global__ void k_fill_f64(double* __restrict__ p, int64_t n, double v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
 }
 
 // carried finish times re-based to the next stage's clock: fin_t -= t_E^(k) for done requests
@@ -204,6 +211,13 @@ cudaError_t launch_summary(const samu_trial_rec* recs, int32_t n_cands, int32_t 
     if (e != cudaSuccess) return e;
   }
   k_summary<<<n_cands, 256, smem, s>>>(recs, n_trials, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_f64(double* p, int64_t n, double v, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
+  k_fill_f64<<<(unsigned)blocks, 256, 0, s>>>(p, n, v);
   return cudaGetLastError();
 }
 

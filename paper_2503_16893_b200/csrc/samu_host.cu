@@ -15,6 +15,7 @@
 #include <string>
 #include <tuple>
 #include <vector>
+#include <chrono>
 
 #include "samu_internal.cuh"
 
@@ -86,6 +87,14 @@ struct samu_local_group {
   }
 };
 
+// Device buffers of the planner (Greedy / Replay), kept by the context between calls: allocating
+// and freeing ~100 MB-1 GB per call (cudaMalloc / cudaFree synchronise and page-map) made the
+// planner's wall time vary by seconds.
+struct PlanBufs {
+  DevBuf lo, li, st, g, fin_t, over, cache, local_rec, d_sc, d_out, d_best, d_any;
+  std::vector<DevBuf> fin_pool;
+};
+
 struct samu_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -116,6 +125,8 @@ struct samu_ctx {
   std::map<std::pair<int, int>, std::vector<uint32_t>> rep_off_host;
 
   // launch scratch
+  DevBuf d_cand_sum;   // per-candidate summaries of samu_simulate_batch
+  PlanBufs pb;         // planner buffers (borrowed by Greedy / Replay for the duration of a call)
   DevBuf d_cands, d_items, d_counter, d_rep_rec, d_scratch_q, d_scratch_key, d_scratch_idx, d_error;
   DevBuf d_sum, d_gather_send, d_gather_recv;
   int sim_blocks_per_sm[3] = {0, 0, 0};   // resident K2 blocks per SM, per K2 mode
@@ -626,8 +637,31 @@ struct StatePtrs {
   double* over = nullptr;
 };
 
+// SAMU_TRACE=1: per-stage planner timing on stderr (host wall clock; run_jobs is synchronous)
+static bool trace_on() {
+  static const bool on = [] { const char* e = std::getenv("SAMU_TRACE"); return e && *e == '1'; }();
+  return on;
+}
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+static double g_trace_jobs_s = 0.0;   // time inside run_jobs since the last reset (trace only)
+static int64_t g_trace_jobs_n = 0;
+
+static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const uint16_t* l_out, const uint16_t* l_in,
+                                 int32_t T, const StatePtrs& S);
 static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16_t* l_out, const uint16_t* l_in,
                             int32_t T, const StatePtrs& S) {
+  if (!trace_on()) return run_jobs_impl(c, jobs, l_out, l_in, T, S);
+  const double t0 = now_s();
+  const samu_status r = run_jobs_impl(c, jobs, l_out, l_in, T, S);
+  g_trace_jobs_s += now_s() - t0;
+  g_trace_jobs_n += 1;
+  return r;
+}
+
+static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const uint16_t* l_out, const uint16_t* l_in,
+                                 int32_t T, const StatePtrs& S) {
   if (jobs.empty() || T == 0) return SAMU_OK;
   if ((uint64_t)T * (uint64_t)c->n_req >= (1ull << 32))   // K2 indexes [trial][request] with u32
     FAIL(c, SAMU_E_INVALID, "simulate: trials x requests must stay below 2^32 per launch");
@@ -903,11 +937,8 @@ extern "C" samu_status samu_simulate_batch(samu_ctx* c, const samu_candidate* ca
       J.fin_t_out = own_fin.back().as<double>();
     }
     if (out_fin_iter) CK(c, cudaMemsetAsync(J.fin_iter_out, 0xFF, sizeof(uint32_t) * n_trials * n, c->stream));
-    if (J.fin_t_out) {
-      std::vector<double> inf((size_t)n_trials * n, std::numeric_limits<double>::infinity());
-      CK(c, cudaMemcpyAsync(J.fin_t_out, inf.data(), sizeof(double) * inf.size(), cudaMemcpyHostToDevice, c->stream));
-      CK(c, cudaStreamSynchronize(c->stream));
-    }
+    if (J.fin_t_out)
+      CK(c, samu_count(c, launch_fill_f64(J.fin_t_out, (int64_t)n_trials * n, std::numeric_limits<double>::infinity(), c->stream)));
   }
   for (int i = 0; i < n_cands; ++i)
     if (cands[i].dep_src >= 0) jobs[i].src_fin = jobs[cands[i].dep_src].fin_t_out;
@@ -935,10 +966,10 @@ extern "C" samu_status samu_simulate_batch(samu_ctx* c, const samu_candidate* ca
       RET(gather_records(c, out_recs, n_cands, T_total, c->d_sum.as<samu_trial_rec>(), slots));
       all = c->d_sum.as<samu_trial_rec>();
     }
-    DevBuf dsum;
-    CK(c, dsum.ensure(sizeof(samu_cand_summary) * n_cands));
-    CK(c, samu_count(c, launch_summary(all, n_cands, T_total, dsum.as<samu_cand_summary>(), c->stream)));
-    CK(c, cudaMemcpyAsync(out_summary, dsum.p, sizeof(samu_cand_summary) * n_cands, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, c->d_cand_sum.ensure(sizeof(samu_cand_summary) * n_cands));
+    CK(c, samu_count(c, launch_summary(all, n_cands, T_total, c->d_cand_sum.as<samu_cand_summary>(), c->stream)));
+    CK(c, cudaMemcpyAsync(out_summary, c->d_cand_sum.p, sizeof(samu_cand_summary) * n_cands, cudaMemcpyDeviceToHost,
+                          c->stream));
     CK(c, cudaStreamSynchronize(c->stream));
   }
   return SAMU_OK;
@@ -966,6 +997,7 @@ struct Greedy {
   int cap_slots = 0, n_slots = 0;
   std::map<std::vector<int>, int> full_slot, cut_slot;
   std::map<int, DevBuf> fin_buf;           // full slot -> [Tl][n] finish times (dependency sources)
+  std::vector<DevBuf> fin_pool;            // finish-time buffers of earlier stages, reused (no cudaMalloc / cudaFree per stage)
   std::map<int, int> pending_phase;        // slot -> phase within the pending batch
   std::vector<SimJob> pending;
   std::vector<int> pending_slots;
@@ -1040,6 +1072,7 @@ struct Greedy {
     J.src_fin = sf;
     if (is_input[e.node]) {
       DevBuf& fb = fin_buf[slot];
+      if (!fin_pool.empty()) { fb = std::move(fin_pool.back()); fin_pool.pop_back(); }
       CK(c, fb.ensure(sizeof(double) * (size_t)Tl * n));
       J.fin_t_out = fb.as<double>();
     }
@@ -1084,11 +1117,9 @@ struct Greedy {
     for (size_t x = 0; x < pending.size(); ++x) {
       pending[x].out_rec = !sharded(c) ? rec(pending_slots[x]) : local_rec.as<samu_trial_rec>() + x * Tl;
       pending[x].tau_rec = pending_tau[x] >= 0 ? rec(pending_tau[x]) + tb : nullptr;
-      if (pending[x].fin_t_out) {
-        std::vector<double> inf((size_t)Tl * n, std::numeric_limits<double>::infinity());
-        CK(c, cudaMemcpyAsync(pending[x].fin_t_out, inf.data(), sizeof(double) * inf.size(), cudaMemcpyHostToDevice, c->stream));
-        CK(c, cudaStreamSynchronize(c->stream));
-      }
+      if (pending[x].fin_t_out)
+        CK(c, samu_count(c, launch_fill_f64(pending[x].fin_t_out, (int64_t)Tl * n, std::numeric_limits<double>::infinity(),
+                                            c->stream)));
     }
     RET(run_jobs(c, pending, lo.as<uint16_t>(), li.as<uint16_t>(), Tl, S));
     if (sharded(c)) RET(gather_records(c, local_rec.as<samu_trial_rec>(), (int)pending.size(), T, cache.as<samu_trial_rec>(), pending_slots));
@@ -1317,8 +1348,30 @@ struct Greedy {
     return SAMU_OK;
   }
 
+  // take the context's planner buffers for this call (returned by the destructor)
+  bool borrowed = false;
+  void borrow() {
+    PlanBufs& b = c->pb;
+    lo = std::move(b.lo); li = std::move(b.li); st = std::move(b.st); g = std::move(b.g);
+    fin_t = std::move(b.fin_t); over = std::move(b.over); cache = std::move(b.cache);
+    local_rec = std::move(b.local_rec); d_sc = std::move(b.d_sc); d_out = std::move(b.d_out);
+    d_best = std::move(b.d_best); d_any = std::move(b.d_any); fin_pool = std::move(b.fin_pool);
+    cap_slots = T > 0 ? (int)(cache.n / (sizeof(samu_trial_rec) * (size_t)T)) : 0;
+    borrowed = true;
+  }
+  ~Greedy() {
+    if (!borrowed) return;
+    PlanBufs& b = c->pb;
+    for (auto& kv : fin_buf) fin_pool.push_back(std::move(kv.second));
+    b.lo = std::move(lo); b.li = std::move(li); b.st = std::move(st); b.g = std::move(g);
+    b.fin_t = std::move(fin_t); b.over = std::move(over); b.cache = std::move(cache);
+    b.local_rec = std::move(local_rec); b.d_sc = std::move(d_sc); b.d_out = std::move(d_out);
+    b.d_best = std::move(d_best); b.d_any = std::move(d_any); b.fin_pool = std::move(fin_pool);
+  }
+
   samu_status setup(uint64_t seed, int T_total) {
     T = T_total;
+    if (!borrowed) borrow();
     n = (size_t)c->n_req;
     trial_share(T, c->world, c->rank, &tb, &Tl);
     cudaStream_t s = c->stream;
@@ -1335,11 +1388,7 @@ struct Greedy {
     CK(c, cudaMemsetAsync(st.p, 0, sizeof(uint32_t) * tn, s));
     CK(c, cudaMemsetAsync(g.p, 0, sizeof(uint16_t) * tn, s));
     CK(c, cudaMemsetAsync(over.p, 0, sizeof(double) * (size_t)std::max(Tl, 1) * c->n_nodes * 16, s));
-    {
-      std::vector<double> inf(tn, std::numeric_limits<double>::infinity());
-      CK(c, cudaMemcpyAsync(fin_t.p, inf.data(), sizeof(double) * tn, cudaMemcpyHostToDevice, s));
-      CK(c, cudaStreamSynchronize(s));
-    }
+    CK(c, samu_count(c, launch_fill_f64(fin_t.as<double>(), (int64_t)tn, std::numeric_limits<double>::infinity(), s)));
     if (Tl) RET(sample_or_known(c, seed, tb, Tl, known, lo.as<uint16_t>(), li.as<uint16_t>()));
     S = StatePtrs{st.as<uint32_t>(), g.as<uint16_t>(), fin_t.as<double>(), over.as<double>()};
     CK(c, d_best.ensure(sizeof(int32_t) + sizeof(double)));
@@ -1389,12 +1438,23 @@ struct Greedy {
     return SAMU_OK;
   }
 
-  void new_stage_caches() { full_slot.clear(); cut_slot.clear(); fin_buf.clear(); n_slots = 0; }
+  void new_stage_caches() {
+    full_slot.clear();
+    cut_slot.clear();
+    for (auto& kv : fin_buf) fin_pool.push_back(std::move(kv.second));
+    fin_buf.clear();
+    n_slots = 0;
+  }
 
   samu_status run(uint64_t seed, int T_total, int algo, samu_plan* plan) {
+    double t_stage = now_s();
+    g_trace_jobs_s = 0.0;
+    g_trace_jobs_n = 0;
     RET(setup(seed, T_total));
+    if (trace_on()) std::fprintf(stderr, "[samu trace] setup %.4f s\n", now_s() - t_stage);
     std::memset(plan, 0, sizeof(*plan));
     for (;;) {
+      if (trace_on()) { t_stage = now_s(); g_trace_jobs_s = 0.0; g_trace_jobs_n = 0; }
       // unfinished nodes (in any trial of any rank)
       std::vector<int> undone(c->n_nodes, 0);
       RET(node_status(undone));
@@ -1419,6 +1479,9 @@ struct Greedy {
       PS.mean_tE = chosen.mean_tE;
       PS.T_E = chosen.TE;
       plan->total += chosen.mean_tE;
+      if (trace_on())
+        std::fprintf(stderr, "[samu trace] stage %d: %.4f s wall, %.4f s in %lld simulate batches, %d entries\n",
+                     plan->n_stages - 1, now_s() - t_stage, g_trace_jobs_s, (long long)g_trace_jobs_n, PS.n_entries);
     }
     plan->n_cand_evals = evals;
     return SAMU_OK;

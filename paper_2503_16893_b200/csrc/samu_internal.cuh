@@ -100,6 +100,7 @@ cudaError_t launch_combine(const samu_trial_rec* rep_rec, const DevCand* cands, 
                            double* over, int32_t n_nodes, cudaStream_t s);
 cudaError_t launch_summary(const samu_trial_rec* recs, int32_t n_cands, int32_t n_trials,
                            samu_cand_summary* out, cudaStream_t s);
+cudaError_t launch_fill_f64(double* p, int64_t n, double v, cudaStream_t s);
 cudaError_t launch_rebase(uint32_t* st, double* fin_t, int64_t n_total, const samu_trial_rec* fstar_rec,
                           int32_t n_req, cudaStream_t s);
 cudaError_t launch_node_done(const uint32_t* st, int32_t n_trials, int32_t n_req, const int32_t* node,
