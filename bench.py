@@ -182,8 +182,9 @@ def main():
     ap.add_argument("--trials", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--planner-trials", type=int, default=128,
-                    help="also time one full Algorithm 1 run (samu_plan_greedy, rows a1-a12) at this trial count; 0 = off")
+    ap.add_argument("--planner-trials", type=int, default=-1,
+                    help="also time one full Algorithm 1 run (samu_plan_greedy, rows a1-a12) at this trial count "
+                         "(default: the workload's trials; 0 = off)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -283,8 +284,8 @@ def main():
     # the whole planner (Algorithm 1: every greedy inner step incl. truncated sims, stage scoring
     # and argmax, row a12) once, wall time around the call (synchronising), max over ranks
     planner = None
-    if args.planner_trials > 0:
-        Tp = min(args.planner_trials, T)
+    if args.planner_trials != 0:
+        Tp = T if args.planner_trials < 0 else min(args.planner_trials, T)
         S.samu_plan_greedy(w.seed, 1)            # warm-up: allocations for the planner's buffers
         barrier()
         t0 = time.perf_counter()

@@ -4,7 +4,7 @@ set -x
 mkdir -p gpurun_out
 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv \
-    python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/bench_under_ncu.log 2>&1
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --planner-trials 0 > gpurun_out/bench_under_ncu.log 2>&1
 # K2 = one launch per mode (FRESH chain summariser, LEAN ensembling / routing): the FRESH launch
 # from a two-launch capture, the LEAN one alone (its counters come back nan as the second launch)
 ncu --set full --clock-control none --import-source on -k regex:k_simulate -s 2 -c 2 -f -o gpurun_out/k2_bench \
