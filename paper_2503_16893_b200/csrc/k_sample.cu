@@ -140,19 +140,21 @@ __global__ void k_ecdf_table(const uint32_t* __restrict__ values, const uint32_t
 }
 
 // v = v0 + (v1 - v0) * ((B - B0) / (B1 - B0)), clamped outside the profiled buckets (c11).
-__global__ void k_dense_coeff(const uint32_t* __restrict__ bucket_B, int32_t nb, const double* __restrict__ coeff,
+__global__ void k_dense_coeff(const double* __restrict__ bucket_B, int32_t nb, const double* __restrict__ coeff,
                               uint32_t max_seqs, double* __restrict__ out) {
   const int32_t B = blockIdx.x * blockDim.x + threadIdx.x + 1;
   const int32_t pa = blockIdx.y;   // phase * 2 + (a|b)
   if (B > (int32_t)max_seqs) return;
   const double* v = coeff + (size_t)pa * nb;
+  // bucket B values arrive as exact doubles (one staging buffer with the coefficients)
+  auto bk = [&](int32_t i) { return (uint32_t)bucket_B[i]; };
   double r;
-  if ((uint32_t)B <= bucket_B[0]) r = v[0];
-  else if ((uint32_t)B >= bucket_B[nb - 1]) r = v[nb - 1];
+  if ((uint32_t)B <= bk(0)) r = v[0];
+  else if ((uint32_t)B >= bk(nb - 1)) r = v[nb - 1];
   else {
     int32_t k = 0;
-    while (!((uint32_t)B >= bucket_B[k] && (uint32_t)B < bucket_B[k + 1])) ++k;
-    const double w = __ddiv_rn((double)(B - (int32_t)bucket_B[k]), (double)(bucket_B[k + 1] - bucket_B[k]));
+    while (!((uint32_t)B >= bk(k) && (uint32_t)B < bk(k + 1))) ++k;
+    const double w = __ddiv_rn((double)(B - (int32_t)bk(k)), (double)(bk(k + 1) - bk(k)));
     r = __dadd_rn(v[k], __dmul_rn(__dsub_rn(v[k + 1], v[k]), w));
   }
   out[(size_t)(B - 1) * 8 + pa] = r;   // [B][a_c b_c a_p b_p a_s b_s pad pad]: 3 x 16-byte loads per B
@@ -178,7 +180,7 @@ cudaError_t launch_ecdf_table(const uint32_t* values, const uint32_t* cum, int32
   return cudaGetLastError();
 }
 
-cudaError_t launch_dense_coeff(const uint32_t* bucket_B, int32_t nb, const double* coeff_slot, uint32_t max_seqs,
+cudaError_t launch_dense_coeff(const double* bucket_B, int32_t nb, const double* coeff_slot, uint32_t max_seqs,
                                double* out, cudaStream_t s) {
   dim3 grid((max_seqs + 127) / 128, 6);
   k_dense_coeff<<<grid, 128, 0, s>>>(bucket_B, nb, coeff_slot, max_seqs, out);

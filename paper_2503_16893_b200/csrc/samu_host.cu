@@ -121,11 +121,14 @@ struct samu_ctx {
   int32_t smem_tab_bytes = 0;
   std::vector<DevBuf> d_waves;
   std::map<std::pair<int, int>, DevBuf> coef;                      // (model, tp slot) -> dense table
-  std::map<std::pair<int, int>, std::pair<DevBuf, DevBuf>> rep;    // (node, dp) -> (off, req)
+  struct RepLists { DevBuf off, req; uint64_t gen = 0; };
+  std::map<std::pair<int, int>, RepLists> rep;    // (node, dp) -> replica CSR, built for app load `gen`
+  uint64_t app_gen = 1;                            // bumped by every samu_app_load (buffers are reused)
   std::map<std::pair<int, int>, std::vector<uint32_t>> rep_off_host;
 
   // launch scratch
   DevBuf d_cand_sum;   // per-candidate summaries of samu_simulate_batch
+  DevBuf d_stage;      // staging for app-load tables (eCDF knots, coefficient rows)
   PlanBufs pb;         // planner buffers (borrowed by Greedy / Replay for the duration of a call)
   DevBuf d_cands, d_items, d_counter, d_rep_rec, d_scratch_q, d_scratch_key, d_scratch_idx, d_error;
   DevBuf d_sum, d_gather_send, d_gather_recv;
@@ -478,17 +481,25 @@ extern "C" samu_status samu_app_load(samu_ctx* c, const samu_engine_cfg* engine,
       }
     }
     CK(c, c->d_tab.ensure(sizeof(uint16_t) * std::max(toff[SAMU_MAX_NODES], 8)));
+    // every model's knots in one staging upload (values | cumulative counts), one table launch each
+    std::vector<uint32_t> knots;
+    std::vector<size_t> kat(SAMU_MAX_NODES, 0);
+    for (int m = 0; m < SAMU_MAX_NODES; ++m) {
+      if (!c->models[m].ecdf_set) continue;
+      kat[m] = knots.size();
+      knots.insert(knots.end(), c->models[m].ev.begin(), c->models[m].ev.end());
+      knots.insert(knots.end(), c->models[m].ec.begin(), c->models[m].ec.end());
+    }
+    CK(c, upload(c->d_stage, knots, s));
     int32_t max_bytes = 0;
     for (int m = 0; m < SAMU_MAX_NODES; ++m) {
       if (!c->models[m].ecdf_set) continue;
-      DevBuf v, cu;
-      CK(c, upload(v, c->models[m].ev, s));
-      CK(c, upload(cu, c->models[m].ec, s));
-      CK(c, samu_count(c, launch_ecdf_table(v.as<uint32_t>(), cu.as<uint32_t>(), (int32_t)c->models[m].ev.size(), nobs[m],
-                                            c->d_tab.as<uint16_t>() + toff[m], s)));
-      CK(c, cudaStreamSynchronize(s));
+      const uint32_t* kv = c->d_stage.as<uint32_t>() + kat[m];
+      const size_t K = c->models[m].ev.size();
+      CK(c, samu_count(c, launch_ecdf_table(kv, kv + K, (int32_t)K, nobs[m], c->d_tab.as<uint16_t>() + toff[m], s)));
       max_bytes = std::max(max_bytes, (toff[m + 1] - toff[m]) * 2);
     }
+    CK(c, cudaStreamSynchronize(s));   // the staging buffer is reused below
     c->smem_tab_bytes = std::min(max_bytes, 200 * 1024);
     for (int v = 0; v < n_nodes; ++v) lmax[v] = c->models[node_model[v]].spec.l_max;
     CK(c, upload(c->d_tab_off, toff, s));
@@ -496,25 +507,40 @@ extern "C" samu_status samu_app_load(samu_ctx* c, const samu_engine_cfg* engine,
     CK(c, upload(c->d_mnode, c->node_model, s));
     CK(c, upload(c->d_lmax, lmax, s));
   }
-  // dense coefficient tables for every (model of a node, allowed tp) (reading c11)
-  c->coef.clear();
-  for (int v = 0; v < n_nodes; ++v) {
-    const int m = node_model[v];
-    const ModelReg& M = c->models[m];
-    for (int slot = 0; slot < SAMU_N_TP_SLOTS; ++slot) {
-      if (!((M.spec.tp_mask >> slot) & 1u) || c->coef.count({m, slot})) continue;
-      const int nb = (int)M.bucket_B.size();
-      DevBuf bb, cs;
-      CK(c, upload(bb, M.bucket_B, s));
-      std::vector<double> part(M.coeff.begin() + (size_t)slot * 6 * nb, M.coeff.begin() + (size_t)(slot + 1) * 6 * nb);
-      CK(c, upload(cs, part, s));
-      DevBuf& out = c->coef[{m, slot}];
-      CK(c, out.ensure(sizeof(double) * 8 * e.max_num_seqs));
-      CK(c, samu_count(c, launch_dense_coeff(bb.as<uint32_t>(), nb, cs.as<double>(), e.max_num_seqs, out.as<double>(), s)));
-      CK(c, cudaStreamSynchronize(s));
+  // dense coefficient tables for every (model of a node, allowed tp) (reading c11): one staging
+  // upload of all bucket lists and coefficient rows, table buffers kept across app loads
+  {
+    std::vector<std::pair<int, int>> keys;
+    for (int v = 0; v < n_nodes; ++v) {
+      const int m = node_model[v];
+      for (int slot = 0; slot < SAMU_N_TP_SLOTS; ++slot)
+        if (((c->models[m].spec.tp_mask >> slot) & 1u) &&
+            std::find(keys.begin(), keys.end(), std::make_pair(m, slot)) == keys.end())
+          keys.emplace_back(m, slot);
     }
+    std::vector<double> stage;   // per key: bucket B values (as doubles) | 6 nb coefficients
+    std::vector<size_t> at;
+    for (auto& k : keys) {
+      const ModelReg& M = c->models[k.first];
+      const size_t nb = M.bucket_B.size();
+      at.push_back(stage.size());
+      for (uint32_t b : M.bucket_B) stage.push_back((double)b);
+      stage.insert(stage.end(), M.coeff.begin() + (size_t)k.second * 6 * nb, M.coeff.begin() + (size_t)(k.second + 1) * 6 * nb);
+    }
+    CK(c, upload(c->d_stage, stage, s));
+    for (auto it = c->coef.begin(); it != c->coef.end();)
+      it = std::find(keys.begin(), keys.end(), it->first) == keys.end() ? c->coef.erase(it) : std::next(it);
+    for (size_t i = 0; i < keys.size(); ++i) {
+      const ModelReg& M = c->models[keys[i].first];
+      const int nb = (int)M.bucket_B.size();
+      DevBuf& out = c->coef[keys[i]];
+      CK(c, out.ensure(sizeof(double) * 8 * e.max_num_seqs));
+      const double* base = c->d_stage.as<double>() + at[i];
+      CK(c, samu_count(c, launch_dense_coeff(base, nb, base + nb, e.max_num_seqs, out.as<double>(), s)));
+    }
+    CK(c, cudaStreamSynchronize(s));
   }
-  c->rep.clear();
+  c->app_gen += 1;   // replica lists are rebuilt lazily into their existing buffers
   c->rep_off_host.clear();
   c->app_loaded = true;
   return SAMU_OK;
@@ -546,7 +572,7 @@ static DevApp dev_app(const samu_ctx* c) {
 static samu_status replicas(samu_ctx* c, int node, int dp, const uint32_t** off, const uint32_t** lst) {
   auto key = std::make_pair(node, dp);
   auto it = c->rep.find(key);
-  if (it == c->rep.end()) {
+  if (it == c->rep.end() || it->second.gen != c->app_gen) {
     std::vector<std::vector<uint32_t>> L(dp);
     for (int r = c->node_begin[node]; r < c->node_end[node]; ++r) {
       const int kk = c->req[r].chain >= 0 ? c->req[r].chain : r - c->node_begin[node];
@@ -555,13 +581,14 @@ static samu_status replicas(samu_ctx* c, int node, int dp, const uint32_t** off,
     std::vector<uint32_t> o(dp + 1, 0), l;
     for (int j = 0; j < dp; ++j) { o[j + 1] = o[j] + (uint32_t)L[j].size(); l.insert(l.end(), L[j].begin(), L[j].end()); }
     auto& pr = c->rep[key];
-    CK(c, upload(pr.first, o, c->stream));
-    CK(c, upload(pr.second, l, c->stream));
+    CK(c, upload(pr.off, o, c->stream));
+    CK(c, upload(pr.req, l, c->stream));
+    pr.gen = c->app_gen;
     c->rep_off_host[key] = o;
     it = c->rep.find(key);
   }
-  *off = it->second.first.as<uint32_t>();
-  *lst = it->second.second.as<uint32_t>();
+  *off = it->second.off.as<uint32_t>();
+  *lst = it->second.req.as<uint32_t>();
   return SAMU_OK;
 }
 

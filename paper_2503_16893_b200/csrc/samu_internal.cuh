@@ -89,7 +89,7 @@ cudaError_t launch_sample(const DevApp& app, const DevEcdf& e, const int32_t* se
                           uint16_t* l_out, uint16_t* l_in, cudaStream_t s);
 cudaError_t launch_ecdf_table(const uint32_t* values, const uint32_t* cum, int32_t K, uint32_t n, uint16_t* tab,
                               cudaStream_t s);
-cudaError_t launch_dense_coeff(const uint32_t* bucket_B, int32_t nb, const double* coeff_slot,
+cudaError_t launch_dense_coeff(const double* bucket_B, int32_t nb, const double* coeff_slot,
                                uint32_t max_seqs, double* out, cudaStream_t s);
 cudaError_t launch_simulate(const SimLaunch& L, const DevCand* host_cands, int32_t n_blocks, uint32_t block_size,
                             int mode, cudaStream_t s);
