@@ -576,6 +576,20 @@ def test_local_ranks_greedy_plan_identical(world):
         assert pg["total"] == ref["total"]
 
 
+def test_local_ranks_greedy_fewer_trials_than_ranks():
+    # T < world: one rank holds no trial (bench.py's planner warm-up uses min(world, T) trials)
+    w = W.make_workload("c2", n_prompts=80, n_trials=2)
+    ref = O.Problem(w).plan_greedy(SEED, 2)
+
+    def fn(S, r, st):
+        S.load_workload(w)
+        return S.samu_plan_greedy(SEED, 2)
+
+    for pg in _run_ranks(3, fn):
+        assert [s["entries"] for s in pg["stages"]] == [s["entries"] for s in ref["stages"]]
+        assert pg["total"] == ref["total"]
+
+
 def test_local_ranks_replay_identical():
     w = W.make_workload("c5", n_prompts=40, n_docs=30, n_trials=1)
     P = O.Problem(w)
