@@ -723,6 +723,51 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1>&
             // increments), then the chunk's costs are added to t one by one in iteration order
             // (c23, c24: bit-identical to the sequential loop)
             bool stopped = false;
+            // FRESH (chain summariser: long runs of small B): 64 iterations per scan (lane j:
+            // iterations 2j and 2j + 1), the same exact binade form (only in that instantiation:
+            // elsewhere the extra live values cost more than the saved scans)
+            while (MODE == 2 && !stopped && m_run - done_it >= 64u) {
+              const uint64_t eb = (uint64_t)__double_as_longlong(t) & 0x7FF0000000000000ull;
+              if (!(t > 0.0 && eb >= (64ull << 52) && eb < (0x7F0ull << 52))) break;
+              const uint32_t ja = done_it + 2u * (uint32_t)lane;
+              const uint32_t Sa = m.S + B * ja, Sb = Sa + B;
+              const double c0 = __dadd_rn(__dadd_rn(__fma_rn(ac, __ull2double_rn(K0 + (uint64_t)K1 * Sa), bc),
+                                                    __fma_rn(ap, __uint2double_rn(B * (smax0 + ja)), bp)),
+                                          __fma_rn(as_, __uint2double_rn(Sa), bs_));
+              const double c1 = __dadd_rn(__dadd_rn(__fma_rn(ac, __ull2double_rn(K0 + (uint64_t)K1 * Sb), bc),
+                                                    __fma_rn(ap, __uint2double_rn(B * (smax0 + ja + 1u)), bp)),
+                                          __fma_rn(as_, __uint2double_rn(Sb), bs_));
+              const double r0 = __dsub_rn(__dadd_rn(t, c0), t), r1 = __dsub_rn(__dadd_rn(t, c1), t);
+              const double e0 = __dsub_rn(c0, r0), e1 = __dsub_rn(c1, r1);
+              const double halfu = __longlong_as_double((long long)(eb - (53ull << 52)));
+              const double top = __longlong_as_double((long long)(eb + (1ull << 52)));
+              const double rp = __dadd_rn(r0, r1);
+              double psum = rp;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const double nb2 = __shfl_up_sync(FULL, psum, o);
+                if (lane >= o) psum = __dadd_rn(psum, nb2);
+              }
+              const double acc_b = __dadd_rn(t, psum);                              // after 2j + 1
+              const double acc_a = __dadd_rn(t, __dadd_rn(__dsub_rn(psum, rp), r0));   // after 2j
+              const bool stop_a = !(acc_a < stop_t);
+              const uint32_t bstop = __ballot_sync(FULL, stop_a || !(acc_b < stop_t));
+              const uint32_t L = bstop ? (uint32_t)(__ffs(bstop) - 1) : 31u;
+              const bool chk_b = (uint32_t)lane < L || ((uint32_t)lane == L && !stop_a);
+              const bool bad = (uint32_t)lane <= L &&
+                               (c0 < 0.0 || fabs(e0) == halfu || !(acc_a < top) ||
+                                (chk_b && (c1 < 0.0 || fabs(e1) == halfu || !(acc_b < top))));
+              if (__any_sync(FULL, bad)) break;   // the 32-iteration chunks below take over
+              if (bstop) {
+                const bool sa = __shfl_sync(FULL, stop_a, L);
+                t = sa ? __shfl_sync(FULL, acc_a, L) : __shfl_sync(FULL, acc_b, L);
+                done_it += 2u * L + (sa ? 1u : 2u);
+                stopped = true;
+              } else {
+                t = __shfl_sync(FULL, acc_b, 31);
+                done_it += 64u;
+              }
+            }
             while (done_it < m_run && !stopped) {
               const uint32_t cnt = min(32u, m_run - done_it);
               double cj = 0.0;
