@@ -100,16 +100,16 @@ def peaks():
         return {}
 
 
-def ncu_traffic(workload):
-    """dram bytes per K2 launch from the committed ncu --set full summary, if it matches."""
+def ncu_summary(workload):
+    """The committed ncu --set full summary of K2 (profiles/ncu_k2_summary.json), if it matches."""
     p = os.path.join(ROOT, "profiles", "ncu_k2_summary.json")
     try:
         d = json.load(open(p))
         if d.get("workload") == workload:
-            return d.get("dram_bytes_per_launch")
+            return d
     except Exception:
         pass
-    return None
+    return {}
 
 
 # ------------------------------------------------------------------------------------------
@@ -321,7 +321,12 @@ def main():
             "roofline": {"bound": "alu", "kernel": "k_simulate (K2: one launch per mode, FRESH + LEAN at C5)",
                          "achieved": achieved / 1e12, "peak": peak / 1e12,
                          "unit": "TFLOP/s", "frac": achieved / peak,
-                         "traffic": ncu_traffic(w.name),
+                         "traffic": ncu_summary(w.name).get("dram_bytes_per_launch"),
+                         # context (from the committed ncu capture, not this run): the resource
+                         # that binds K2 is the warp-instruction issue rate, not fp64 or HBM
+                         "ncu_issue_slots_active_pct": ncu_summary(w.name).get("issue_active_pct"),
+                         "ncu_fp64_pipe_pct": ncu_summary(w.name).get("fp64_pipe_pct"),
+                         "ncu_source": "profiles/ncu_k2_summary.json",
                          "peak_source": "fp64: 148 SM x 64 FMA lanes x 2 x sm clock (derived, DESIGN.md section 6)",
                          "work_per_unit": "9 fp64 flops per simulated iteration (latency model, reading c24)",
                          "sim_iters_per_launch": iters_per_launch, "k2_ms_per_launch": k2_ms},
