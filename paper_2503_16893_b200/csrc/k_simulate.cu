@@ -1269,27 +1269,55 @@ static void launch_variant(const SimLaunch& L, uint32_t block_size, int mode, in
   else k_simulate<-1, CONSTC, 0><<<n_blocks, blk, smem, s>>>(L);
 }
 
-cudaError_t launch_simulate(const SimLaunch& L, const DevCand* host_cands, int32_t n_blocks, uint32_t block_size,
-                            int mode, cudaStream_t s) {
-  const int smem = simulate_smem_bytes(mode);
-  if (L.n_cands <= SAMU_K2_CONST_CANDS) {
-    // The table is one per device and process while contexts may launch on their own streams:
-    // the copy waits for the previous table user (any stream) and this launch becomes the next.
-    static std::mutex mu;
-    static cudaEvent_t last[64] = {};
-    std::lock_guard<std::mutex> lock(mu);
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+// Launch the K2 kernels of one simulate batch, one per mode present (Ls[i] / modes[i] / n_blocks[i]).
+// General and FRESH launches share the per-warp scratch and run in order on s; a LEAN launch uses
+// no scratch and runs concurrently on s2 (forked after the table copy, joined back into s), so
+// its items fill the SMs beside the long chain replica-sims of a FRESH launch instead of after
+// them (the FRESH launch's longest item is its critical path at small trial shares).
+cudaError_t launch_simulate(const SimLaunch* Ls, const int* modes, const int32_t* n_blocks, int n_launch,
+                            const DevCand* host_cands, uint32_t block_size, cudaStream_t s, cudaStream_t s2,
+                            cudaEvent_t ev_fork, cudaEvent_t ev_join) {
+  if (n_launch == 0) return cudaSuccess;
+  const bool constc = Ls[0].n_cands <= SAMU_K2_CONST_CANDS;
+  // The constant table is one per device and process while contexts may launch on their own
+  // streams: the copy waits for the previous table user (any stream) and this batch becomes the
+  // next (host mutex: copy + launches + event record are one unit).
+  static std::mutex mu;
+  static cudaEvent_t last[64] = {};
+  std::unique_lock<std::mutex> lock(mu, std::defer_lock);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (constc) {
+    lock.lock();
     if (!last[dev] && (e = cudaEventCreateWithFlags(&last[dev], cudaEventDisableTiming)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(s, last[dev], 0)) != cudaSuccess) return e;
-    e = cudaMemcpyToSymbolAsync(c_cands, host_cands, sizeof(DevCand) * (size_t)L.n_cands, 0, cudaMemcpyHostToDevice, s);
+    e = cudaMemcpyToSymbolAsync(c_cands, host_cands, sizeof(DevCand) * (size_t)Ls[0].n_cands, 0, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return e;
-    launch_variant<true>(L, block_size, mode, n_blocks, smem, s);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    return cudaEventRecord(last[dev], s);
   }
-  launch_variant<false>(L, block_size, mode, n_blocks, smem, s);
-  return cudaGetLastError();
+  int lean = -1;
+  for (int i = 0; i < n_launch; ++i) if (modes[i] == 1) lean = i;
+  const bool fork = lean >= 0 && n_launch > 1 && s2 != nullptr;
+  if (fork) {   // s2 starts after the table copy (and everything before it on s)
+    if ((e = cudaEventRecord(ev_fork, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(s2, ev_fork, 0)) != cudaSuccess) return e;
+  }
+  for (int i = 0; i < n_launch; ++i) {
+    if (fork && i == lean) continue;
+    const int smem = simulate_smem_bytes(modes[i]);
+    if (constc) launch_variant<true>(Ls[i], block_size, modes[i], n_blocks[i], smem, s);
+    else launch_variant<false>(Ls[i], block_size, modes[i], n_blocks[i], smem, s);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  if (fork) {
+    const int smem = simulate_smem_bytes(1);
+    if (constc) launch_variant<true>(Ls[lean], block_size, 1, n_blocks[lean], smem, s2);
+    else launch_variant<false>(Ls[lean], block_size, 1, n_blocks[lean], smem, s2);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(ev_join, s2)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(s, ev_join, 0)) != cudaSuccess) return e;
+  }
+  if (constc) return cudaEventRecord(last[dev], s);
+  return cudaSuccess;
 }

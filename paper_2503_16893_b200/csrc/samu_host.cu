@@ -98,6 +98,8 @@ struct PlanBufs {
 struct samu_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t aux_stream = nullptr;        // K2 LEAN launches beside the general / FRESH ones
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool own_stream = false;
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
@@ -332,6 +334,12 @@ extern "C" void samu_ctx_destroy(samu_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  if (c->aux_stream) {
+    cudaStreamSynchronize(c->aux_stream);
+    cudaStreamDestroy(c->aux_stream);
+  }
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c;
 }
 
@@ -836,18 +844,33 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
       L.scratch_idx = c->d_scratch_idx.as<uint32_t>();
       L.max_q = (int32_t)max_q;
       L.max_p = (int32_t)max_p;
-      int n_launched = 0;
-      for (int md : {0, 2, 1}) {
+      SimLaunch LM[3];
+      int modes[3], nb[3], n_launch = 0;
+      for (int md : {0, 2, 1}) {   // general, FRESH (on s, in order), LEAN (concurrent on the aux stream)
         if (n_items[md] == 0) continue;
-        SimLaunch LM = L;
-        LM.ord = c->d_items.as<uint32_t>() + ord_at[md];
-        LM.off = c->d_items.as<uint32_t>() + off_at[md];
-        LM.n_ord = n_ord[md];
-        LM.n_items = (int32_t)n_items[md];
-        LM.next_item = c->d_counter.as<uint32_t>() + md;
-        CK(c, launch_simulate(LM, dc.data(), n_blocks[md], (uint32_t)c->eng.block_size, md, s));
-        c->launches += n_launched++ ? 1 : 0;
+        SimLaunch& X = LM[n_launch];
+        X = L;
+        X.ord = c->d_items.as<uint32_t>() + ord_at[md];
+        X.off = c->d_items.as<uint32_t>() + off_at[md];
+        X.n_ord = n_ord[md];
+        X.n_items = (int32_t)n_items[md];
+        X.next_item = c->d_counter.as<uint32_t>() + md;
+        modes[n_launch] = md;
+        nb[n_launch] = n_blocks[md];
+        ++n_launch;
       }
+      if (n_launch > 1 && !c->aux_stream) {
+        CK(c, cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
+        CK(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        CK(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+      }
+      // concurrent LEAN launch only when the other launch is short (a few waves): then its
+      // longest replica-sims are the critical path and the LEAN items fill the idle warps; with
+      // many waves the two kernels only compete for the instruction cache (~2 % slower)
+      const bool overlap = n_items[0] + n_items[2] < 8 * (int64_t)c->n_sm * 24;
+      CK(c, launch_simulate(LM, modes, nb, n_launch, dc.data(), (uint32_t)c->eng.block_size, s,
+                            overlap ? c->aux_stream : nullptr, c->ev_fork, c->ev_join));
+      c->launches += n_launch > 1 ? n_launch - 1 : 0;
     }
     CK(c, launch_combine(L.rep_rec, L.cands, (int32_t)idx.size(), T, S.over, c->n_nodes, s));
     c->launches += 2;

@@ -91,8 +91,9 @@ cudaError_t launch_ecdf_table(const uint32_t* values, const uint32_t* cum, int32
                               cudaStream_t s);
 cudaError_t launch_dense_coeff(const double* bucket_B, int32_t nb, const double* coeff_slot,
                                uint32_t max_seqs, double* out, cudaStream_t s);
-cudaError_t launch_simulate(const SimLaunch& L, const DevCand* host_cands, int32_t n_blocks, uint32_t block_size,
-                            int mode, cudaStream_t s);
+cudaError_t launch_simulate(const SimLaunch* Ls, const int* modes, const int32_t* n_blocks, int n_launch,
+                            const DevCand* host_cands, uint32_t block_size, cudaStream_t s, cudaStream_t s2,
+                            cudaEvent_t ev_fork, cudaEvent_t ev_join);
 cudaError_t simulate_prepare(int blocks_per_sm[3]);   // per K2 mode
 
 int32_t simulate_smem_bytes(int mode);
