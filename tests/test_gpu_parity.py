@@ -462,22 +462,25 @@ def test_fit_coeffs_edge_cases():
 # ------------------------------------------------------------------------------------------
 # full size, bench launch configuration: sampled (candidate, trial) pairs vs the oracle
 # ------------------------------------------------------------------------------------------
-def test_full_size_c5_bench_config_sampled_parity():
-    w = W.make_workload("c5")                      # 50,000 requests, 1024 trials, 12 nodes
+@pytest.mark.parametrize("T", [1024, 128])
+def test_full_size_c5_bench_config_sampled_parity(T):
+    # T = 1024: the N = 1 bench step (FRESH then LEAN launch); T = 128: one rank's share at 8
+    # GPUs, where the LEAN launch runs concurrently with the FRESH one on the auxiliary stream
+    w = W.make_workload("c5", n_trials=T)          # 50,000 requests, 12 nodes
     S = gpu(w)
     ready = [v for v in range(w.n_nodes) if not np.any((w.pred[w.node == v] >= 0) &
                                                       (w.node[np.maximum(w.pred[w.node == v], 0)] != v))]
     cands = [(v, dp, tp) for v in ready for (dp, tp) in S.samu_enumerate_plans(v)]
     glo, gli = S.samu_sample_lengths(SEED, 0, w.n_trials)
-    g = recs(S.samu_simulate_batch(cands, glo, gli))          # [165, 1024]
+    g = recs(S.samu_simulate_batch(cands, glo, gli))          # [165, T]
     P = O.Problem(w)
     rng = np.random.default_rng(2503)
     picks = [(cands.index(c), int(k)) for c, k in
-             [(cands[0], 0), (cands[-1], 1023)] + [(cands[int(i)], int(k)) for i, k in
-                                                   zip(rng.integers(0, len(cands), 10), rng.integers(0, 1024, 10))]]
+             [(cands[0], 0), (cands[-1], T - 1)] + [(cands[int(i)], int(k)) for i, k in
+                                                    zip(rng.integers(0, len(cands), 10), rng.integers(0, T, 10))]]
     # the longest replica-sims: the chain summariser with dp = 1
     summ = [i for i, c in enumerate(cands) if c[0] == 10 and c[1] == 1]
-    picks += [(summ[0], 777)]
+    picks += [(summ[0], 777 % T)]
     for ci, k in picks:
         lo, li = P.sample(SEED, k, 1)
         node, dp, tp = cands[ci]
