@@ -286,7 +286,7 @@ def main():
     planner = None
     if args.planner_trials != 0:
         Tp = T if args.planner_trials < 0 else min(args.planner_trials, T)
-        S.samu_plan_greedy(w.seed, min(world, T))   # warm-up (every rank gets a trial)
+        S.samu_plan_greedy(w.seed, Tp)   # warm-up: the planner's buffers are kept by the context (steady state)
         barrier()
         t0 = time.perf_counter()
         plan = S.samu_plan_greedy(w.seed, Tp)

@@ -16,7 +16,7 @@ for name, T in [(a.split(":")[0], int(a.split(":")[1])) for a in (sys.argv[1:] o
     w = W.make_workload(name, n_trials=T)
     S = Samu(0)
     S.load_workload(w)
-    S.samu_plan_greedy(W.SAMPLING_SEED, 1)      # warm-up (kernel load, allocations)
+    S.samu_plan_greedy(W.SAMPLING_SEED, T)      # warm-up (kernel load; the context keeps the planner's buffers)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     plan = S.samu_plan_greedy(W.SAMPLING_SEED, T)
