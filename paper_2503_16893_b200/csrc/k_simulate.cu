@@ -870,11 +870,13 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1>&
           K2STAT(8, done_it);
           if (m_run > 4) K2STAT(14, 1);
           // closed-form exact updates for the done_it iterations of the run
-          const uint64_t mm = done_it;
-          // sum_j (K0 + K1 (S + B j)) = L c (B mm) + K1 (mm S + B mm (mm - 1) / 2)
-          m.a1 += (uint64_t)B * mm;
-          m.a2 += mm * (uint64_t)m.S + (uint64_t)B * (mm * (mm - 1) / 2);
-          m.reqit += (uint64_t)B * mm;
+          // sum_j (K0 + K1 (S + B j)) = L c (B mm) + K1 (mm S + B mm (mm - 1) / 2); mm <= l_max < 2^16,
+          // so mm (mm - 1) fits 32 bits and every product is one widening 32 x 32 multiply
+          const uint32_t mm = done_it;
+          const uint64_t Bmm = (uint64_t)B * mm;
+          m.a1 += Bmm;
+          m.a2 += (uint64_t)mm * m.S + (uint64_t)B * ((mm * (mm - 1u)) >> 1);
+          m.reqit += Bmm;
           m.iter += done_it;
           const uint32_t rr = bs.mod(done_it);
           const uint32_t need_rr = rr == 0 ? 0u
