@@ -691,7 +691,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1>&
         uint32_t i_pre = 0x7fffffffu;   // first run iteration that must preempt
         uint32_t pre = 0;
         // each bs decodes need exactly B blocks: no search (and no scan) when the run cannot run out
-        const bool tight = (uint64_t)(uint32_t)m.F < (uint64_t)B * ((uint64_t)bs.div(m_fin) + 1);
+        const bool tight = (uint32_t)m.F < B * (bs.div(m_fin) + 1u);   // <= 256 * (65535 + 1): 32 bits
         if (tight) {
           pre = warp_incl_scan(hv, lane);
           {
@@ -987,9 +987,15 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1>&
           if (ninv <= 4) {
             // transposed scan: 8-lane group g reads the 8 slots of the g-th involved lane
             const int g = lane >> 3, jj = lane & 7;
-            if ((inv >> lane) & 1u) W.adm_req[__popc(inv & lanemask_lt())] = (uint32_t)lane;
-            __syncwarp();
-            const uint32_t Lg = (uint32_t)g < ninv ? W.adm_req[g] : 0u;
+            // one involved lane (common): its id is the ballot's only bit, no lane table
+            uint32_t Lg;
+            if (ninv == 1) {
+              Lg = (uint32_t)(__ffs(inv) - 1);
+            } else {
+              if ((inv >> lane) & 1u) W.adm_req[__popc(inv & lanemask_lt())] = (uint32_t)lane;
+              __syncwarp();
+              Lg = (uint32_t)g < ninv ? W.adm_req[g] : 0u;
+            }
             const uint32_t occ_g = __shfl_sync(FULL, occ, Lg);
             const bool has = (uint32_t)g < ninv && ((occ_g >> jj) & 1u);
             const int s = (int)Lg + 32 * jj;
