@@ -2,19 +2,28 @@
 // c13, c15, c18, c19, c23-c25), one warp per (candidate, trial, dp replica).
 //
 // Design (B200-first, not a translation of the per-request oracle loop):
-//  * persistent grid, one work item per warp, pulled from an atomic counter over a host-sorted
-//    longest-first item list (replica-sims differ ~100x in length);
+//  * persistent grid, one work item per warp, pulled from an atomic counter; items are decoded on
+//    the device from the launch's longest-first candidate order and item offsets (replica-sims
+//    differ ~100x in length);
+//  * three instantiations per block size, one launch each (MODE): LEAN (fresh state, independent
+//    requests: the queue is the replica list), FRESH (fresh state with chain successors) and the
+//    general one (carried state, commit, time limits, cross-node arrivals); candidate
+//    descriptors are read from the constant bank;
 //  * the running set lives in shared memory: 256 slots, lane L owns slots L + 32 j (bank-conflict
-//    free), with the lane's occupancy bits in a register;
+//    free), with the lane's occupancy bits in a register; a 32-entry register window, circular
+//    over the lanes, caches the head of the waiting queue;
 //  * between events every running request advances one token per decode, so a "decode run" has
 //    fixed B while S and B*s grow by B per iteration and the KV-block need of decode d follows
 //    from a histogram over the request phases (l - 1 - d) mod bs fixed at admission.  The run
 //    evaluates the contract's per-iteration latency sum in fp64 — every iteration is visited
-//    (c23) — while FLOPs (u128), request-iterations and block counts of the run are folded in
-//    exact integer closed form;
+//    (c23), in 32- / 64-iteration chunks summed in parallel yet bit-identically to the
+//    sequential adds (binade-local rounding + warp scan, sequential walk on ties) — while FLOPs
+//    (folded into u128 once per item), request-iterations and block counts are exact integer
+//    closed forms;
 //  * events (admission = prefill iteration, finish, preemption) are warp-cooperative: admission
-//    is a warp prefix-scan over the next 32 queue heads (tokens, KV blocks), retirement a slot
-//    scan + ballot / REDUX reductions.
+//    is a warp REDUX / prefix-scan over the next 32 queue heads (tokens, KV blocks), retirement
+//    a transposed slot scan + ballot / REDUX reductions, preemption a max over packed
+//    (admission rank, slot) keys.
 #include "samu_internal.cuh"
 
 #include <math_constants.h>
