@@ -214,6 +214,29 @@ def test_candidate_table_both_paths():
             assert_rec_equal(big[ci + r * len(cands)], o, f"global table {cd} copy {r}")
 
 
+@pytest.mark.parametrize("seed", range(6))
+def test_simulate_fuzz_chains_tight_kv(seed):
+    # random chains (successor prompt = base + predecessor's output) under tight KV,
+    # slot and token budgets: the general path (with per-request outputs) and, for block size
+    # 16, the FRESH path (without) against the oracle
+    rng = np.random.default_rng(500 + seed)
+    n_chains = int(rng.integers(3, 25))
+    l_in, l_out, pred, chain = [], [], [], []
+    for c in range(n_chains):
+        for j in range(int(rng.integers(1, 7))):
+            pred.append(-1 if j == 0 else len(l_in) - 1)
+            chain.append(c)
+            l_in.append(int(rng.integers(1, 40)))
+            l_out.append(int(rng.integers(1, 60)))
+    eng = F.engine(kv_cap=int(rng.integers(14, 48)) * 16, min_batched_tokens=int(rng.integers(200, 500)),
+                   max_num_seqs=int(rng.integers(2, 24)), block_size=[16, 8, 16, 12, 16, 4][seed], n_gpus=4)
+    cf = rng.uniform(1e-4, 1e-2, (W.N_TP_SLOTS, 3, 2, F.NB))
+    cf[:, 0, 0, :] = 1e-12
+    w = F.tiny(np.array(l_in), np.array(l_out), sp=F.spec(l_max=200, tp_values=(1, 2), L=2, h=16, c=1000), eng=eng,
+               cf=cf, pred=np.array(pred), chain=np.array(chain), n_trials=2)
+    _sim_parity(w, [(0, 1, 1), (0, 2, 1), (0, 2, 2), (0, 3, 1)], 2)
+
+
 def test_hand_traces_on_gpu():
     for kind, expect_t in (("const", 63.0), ("B", 80.0), ("S", 32 + 784 + 1012 + 33 + 979)):
         w = F.tiny([16, 16], [40, 40], sp=F.spec(l_max=64), cf=kind, eng=F.engine(kv_cap=64, min_batched_tokens=64))
