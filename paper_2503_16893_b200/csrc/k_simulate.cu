@@ -59,7 +59,6 @@ struct WarpSmT {
   uint32_t stk_req[SLOTS];   // preempted stack, top = front of W
   uint32_t stk_g[SLOTS];
   uint32_t tmp[SMALL ? 1 : SLOTS];    // finished requests of the current iteration / radix histogram
-  uint32_t tmp2[SMALL ? 1 : SLOTS];   // staging / released successors
   uint32_t hist[32];         // running requests per phase
   uint32_t adm_req[32], adm_meta[32];
   int2 adm_fo[32];
@@ -1037,7 +1036,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1>&
               occ &= ~((fb >> gl) & 0xFFu);
             }
           } else {
-            uint32_t mn = FULL, cnt = 0;
+            uint32_t mn = FULL, cnt = 0, finm = 0;   // finm: this lane's finishing slots
             int32_t mx = INT_MIN;
 #pragma unroll
             for (int jj = 0; jj < 8; ++jj) {
@@ -1050,7 +1049,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1>&
                   sfin_l += l_now;
                   atomicSub(&W.hist[W.s_meta[s] & 31u], 1u);
                   occ &= ~(1u << jj);
-                  if (need_rel) W.tmp2[cnt * 32 + lane] = W.s_req[s];   // staged per lane (<= 8 each)
+                  finm |= 1u << jj;
                   ++cnt;
                 } else {
                   mn = min(mn, (uint32_t)fo.x);
@@ -1061,9 +1060,9 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1>&
             cnt_l = cnt;
             lminf = mn;
             lmaxo = mx;
-            if (need_rel) {
-              const uint32_t ex = warp_incl_scan(cnt, lane) - cnt;
-              for (uint32_t c2 = 0; c2 < cnt; ++c2) W.tmp[ex + c2] = W.tmp2[c2 * 32 + lane];
+            if (need_rel) {   // finished requests listed from their (not yet reused) slots
+              uint32_t ex = warp_incl_scan(cnt, lane) - cnt;
+              for (uint32_t f = finm; f; f &= f - 1) W.tmp[ex++] = W.s_req[lane + 32 * (__ffs(f) - 1)];
             }
           }
           if (BSK >= 16) {
@@ -1111,6 +1110,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1>&
             if (sr >= 0) q[m.q_tail + rank] = (uint32_t)sr;
             m.q_tail += __popc(br);
           }
+          __syncwarp();   // the finisher list is rewritten by the next retirement
         } else {
           uint32_t nrel = 0;
           for (uint32_t base = 0; base < n_fin; base += 32) {
@@ -1126,17 +1126,20 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1>&
               }
               if (C.has_succ) sr = __ldg(A.succ + r);
             }
+            // compacted in place: the k-th successor overwrites finisher slot <= k, already read
+            // by every lane of this pass (the __syncwarp orders those reads before the writes)
+            __syncwarp();
             const uint32_t br = __ballot_sync(FULL, sr >= 0);
-            if (sr >= 0) W.tmp2[nrel + __popc(br & lanemask_lt())] = (uint32_t)sr;
+            if (sr >= 0) W.tmp[nrel + __popc(br & lanemask_lt())] = (uint32_t)sr;
             nrel += __popc(br);
+            __syncwarp();
           }
-          __syncwarp();
           if (nrel) {
             // append in index order: rank of each released id among the released set
             for (uint32_t i = lane; i < nrel; i += 32) {
-              const uint32_t x = W.tmp2[i];
+              const uint32_t x = W.tmp[i];
               uint32_t rank = 0;
-              for (uint32_t jj = 0; jj < nrel; ++jj) rank += W.tmp2[jj] < x ? 1u : 0u;
+              for (uint32_t jj = 0; jj < nrel; ++jj) rank += W.tmp[jj] < x ? 1u : 0u;
               q[m.q_tail + rank] = x;
             }
             m.q_tail += nrel;
