@@ -160,7 +160,9 @@ samu_status samu_nccl_unique_id(uint8_t out[128]);
  *   coeff     host [SAMU_N_TP_SLOTS][3 phases comp/prep/samp][2 (a,b)][n_buckets]
  *             (only slots allowed by tp_mask are read)
  *   load_s    host [SAMU_N_TP_SLOTS][SAMU_MAX_DP] seconds, load_s[slot][dp-1]
- * The dense per-B table (reading c11) is built on the device. */
+ * The dense per-B table (reading c11) is built on the device.
+ * SAMU_E_INVALID: bad spec (l_max > 65535, tp_mask empty, ...), unsorted buckets, 2 L h >= 2^32
+ * (a 32-bit FLOPs factor of K2), or a per-iteration FLOPs bound that could overflow u64. */
 samu_status samu_model_register(samu_ctx* ctx, int32_t model_id, const samu_model_spec* spec,
                                 int32_t n_buckets, const uint32_t* bucket_B, const double* coeff,
                                 const double* load_s);
@@ -209,7 +211,13 @@ samu_status samu_known_lengths(samu_ctx* ctx, const uint32_t* l_true, uint16_t* 
  *   out_fin_iter device [n_cands][n_trials][n_req] u32 or NULL: iteration (within its replica)
  *               in which each request of the candidate's node finished, 0xFFFFFFFF otherwise
  *   out_fin_t   device [n_cands][n_trials][n_req] f64 or NULL: finish time (stage clock), +inf
- * Candidates with commit = 1 must be distinct nodes and need `state`. */
+ * Candidates with commit = 1 must be distinct nodes and need `state`.
+ * SAMU_E_INVALID also when n_trials x n_req >= 2^32 (K2 indexes [trial][request] with 32 bits)
+ * or the batch has >= 2^31 work items (trials x dp replicas).
+ * Execution: one K2 launch per path present — LEAN (fresh state, independent requests, no time
+ * limit, no per-request outputs), FRESH (the same with chain successors) and the general one;
+ * SAMU_K2_MODES=always|never in the environment overrides the batch-size rule that picks them.
+ * The results do not depend on the path. */
 samu_status samu_simulate_batch(samu_ctx* ctx, const samu_candidate* cands, int32_t n_cands,
                                 const uint16_t* l_out, const uint16_t* l_in_eff, int32_t n_trials,
                                 uint32_t* st, uint16_t* g, double* fin_t, double* overshoot,
