@@ -32,6 +32,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     inc = ["-I", os.path.join(nccl, "include")] if nccl else []
     flags = ARCH + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3"] + inc
     flags += [f"-D{d}" for d in os.environ.get("SAMU_DEFINES", "").split()]
+    flags += os.environ.get("SAMU_NVCC_EXTRA", "").split()   # experiments (scripts/variants.sh)
     build_dir = os.path.join(HERE, "build")
     os.makedirs(build_dir, exist_ok=True)
 
