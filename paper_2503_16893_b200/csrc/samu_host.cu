@@ -115,6 +115,7 @@ struct samu_ctx {
   int n_nodes = 0, n_req = 0;
   std::vector<int32_t> node_model, node_begin, node_end, node_input, node_has_succ;
   std::vector<samu_request> req;
+  std::vector<double> node_exp_out;   // mean expected output tokens of a node's requests (work-item ordering only)
   std::vector<int32_t> succ;
   std::vector<uint8_t> cross;
   std::vector<std::vector<int32_t>> waves;
@@ -550,6 +551,25 @@ extern "C" samu_status samu_app_load(samu_ctx* c, const samu_engine_cfg* engine,
   }
   c->app_gen += 1;   // replica lists are rebuilt lazily into their existing buffers
   c->rep_off_host.clear();
+  // expected output length per node, E[min(X, cap, l_max - l_in)] with X ~ the model's eCDF
+  // (chain inputs taken at their base length): orders K2's work items longest-first
+  c->node_exp_out.assign(n_nodes, 1.0);
+  for (int v = 0; v < n_nodes; ++v) {
+    const ModelReg& M = c->models[node_model[v]];
+    if (!M.ecdf_set || c->node_end[v] <= c->node_begin[v]) continue;
+    const size_t K = M.ev.size();
+    const double nobs = (double)M.ec.back();
+    std::vector<double> part(K + 1, 0.0);   // part[k] = sum_{j<k} v_j * count_j
+    for (size_t k = 0; k < K; ++k) part[k + 1] = part[k] + (double)M.ev[k] * (double)(M.ec[k] - (k ? M.ec[k - 1] : 0u));
+    double acc = 0.0;
+    for (int r = c->node_begin[v]; r < c->node_end[v]; ++r) {
+      const uint32_t lim = std::min<uint32_t>(c->req[r].cap_y, M.spec.l_max - std::min(M.spec.l_max, c->req[r].l_in_base));
+      const size_t k = (size_t)(std::lower_bound(M.ev.begin(), M.ev.end(), lim) - M.ev.begin());   // v_j < lim for j < k
+      const double below = k ? (double)M.ec[k - 1] : 0.0;
+      acc += (part[k] + (double)lim * (nobs - below)) / nobs;
+    }
+    c->node_exp_out[v] = std::max(1.0, acc / (double)(c->node_end[v] - c->node_begin[v]));
+  }
   c->app_loaded = true;
   return SAMU_OK;
 }
@@ -757,7 +777,7 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
       for (int j = 0; j < cd.dp; ++j) mx = std::max(mx, ho[j + 1] - ho[j]);
       max_q = std::max(max_q, mx);
       if (c->node_input[node] >= 0 || S.st) max_p = std::max(max_p, mx);
-      cost[x] = mx;
+      cost[x] = (uint64_t)((double)mx * c->node_exp_out[node]);   // replica requests x expected output
     }
     // longest-first work items (cand, trial, replica)
     std::vector<int> order(idx.size());
