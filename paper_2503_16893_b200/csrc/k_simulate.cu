@@ -200,15 +200,15 @@ static_assert(sizeof(DevCand) * SAMU_K2_CONST_CANDS <= 64 * 1024, "candidate tab
 __constant__ DevCand c_cands[SAMU_K2_CONST_CANDS];
 
 // One work item (candidate, trial, replica): the whole simulation of one replica-sim.
-// MODE (DevCand::mode): 0 general; 2 FRESH: fresh state, no cross-node arrivals, no time limit,
+// MODE (DevCand::mode; 3 / 4 = LEAN / FRESH with a time limit tau, i.e. cut simulations): 0 general; 2 FRESH: fresh state, no cross-node arrivals, no time limit,
 // no per-request outputs (chain successors allowed) — the event loop carries no commit / cut /
 // arrival machinery; 1 LEAN: FRESH without chain successors (e.g. the first greedy step of
 // ensembling / routing nodes) — the queue is then the replica's request list itself.  Fewer live
 // registers: ~10 % faster on those items.
 template <int BSK, bool CONSTC, int MODE>
-__device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1>& W, const int lane, uint32_t* q, uint64_t* pkey,
+__device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1 || MODE == 3>& W, const int lane, uint32_t* q, uint64_t* pkey,
                                          uint32_t* pidx, const uint32_t item) {
-  constexpr bool LEAN = MODE == 1, FRESH = MODE != 0;
+  constexpr bool LEAN = MODE == 1 || MODE == 3, FRESH = MODE != 0, CUT = MODE == 3 || MODE == 4;
   const DevApp& A = P.app;
   const int n = A.n_req;
     // decode the item: candidate by binary search over the launch's offsets, then (trial, replica)
@@ -246,7 +246,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1>&
 
     Sim m;
     m.t = C.resume ? (over ? over[j] : 0.0) : C.load_s;
-    double tau = FRESH ? CUDART_INF : C.tau ? C.tau[k] : (C.tau_rec ? C.tau_rec[k].t_end : CUDART_INF);
+    double tau = (FRESH && !CUT) ? CUDART_INF : C.tau ? C.tau[k] : (C.tau_rec ? C.tau_rec[k].t_end : CUDART_INF);
     m.a1 = m.a2 = m.reqit = 0;
     m.iter = 0; m.d = 0; m.needidx = 0; m.B = 0; m.S = 0; m.next_rank = 0;
     m.F = C.blocks; m.maxO = INT_MIN; m.next_fin = FULL;
@@ -285,7 +285,8 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1>&
       if (succ_wait && st && (st[pr] >> 28) == SAMU_ST_DONE) { m.err = SAMU_E_STATE; site = 1; }
       if (valid && s > SAMU_ST_DONE) { m.err = SAMU_E_STATE; site = 2; }
       const uint32_t bh = __ballot_sync(FULL, head);
-      if (head && !st) q[n_heads + __popc(bh & lanemask_lt())] = r;   // fresh state: no front region
+      // fresh state (no state, or a never-committed node on the FRESH paths): no front region
+      if (head && (!st || FRESH)) q[n_heads + __popc(bh & lanemask_lt())] = r;
       n_heads += __popc(bh);
       // carried entries: class 0 running (reload) | 1 preempted | 3 queued | 4 running (resume)
       uint32_t cls = 7;
@@ -429,6 +430,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1>&
     // ---- main loop (c25) ----
     while (!m.err) {
       K2STAT(1, 1);
+      if (CUT && m.t >= m.stop) { cut = true; break; }   // no arrivals in these modes: stop = tau
       if (!FRESH && m.t >= m.stop) {   // stop time or a pending arrival reached
         const double tau_w = W.tau;
         if (m.t >= tau_w) { cut = true; break; }
@@ -734,7 +736,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1>&
             // FRESH (chain summariser: long runs of small B): 64 iterations per scan (lane j:
             // iterations 2j and 2j + 1), the same exact binade form (only in that instantiation:
             // elsewhere the extra live values cost more than the saved scans)
-            while (MODE == 2 && !stopped && m_run - done_it >= 64u) {
+            while ((MODE == 2 || MODE == 4) && !stopped && m_run - done_it >= 64u) {
               const uint64_t eb = (uint64_t)__double_as_longlong(t) & 0x7FF0000000000000ull;
               if (!(t > 0.0 && eb >= (64ull << 52) && eb < (0x7F0ull << 52))) break;
               const uint32_t ja = done_it + 2u * (uint32_t)lane;
@@ -1221,7 +1223,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1>&
 // A launch holds only items of one MODE (DevCand::mode); the host issues one launch per mode
 // present (one kernel holding several paths is slower: a multiple of the code footprint).
 template <int BSK, bool CONSTC, int MODE>
-__global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, MODE == 1 ? SAMU_K2_MINB_LEAN : SAMU_K2_MINB)
+__global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, (MODE == 1 || MODE == 3) ? SAMU_K2_MINB_LEAN : SAMU_K2_MINB)
     k_simulate(SimLaunch P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // lane id kept in a register: an opaque copy cannot be rematerialised from SR_TID (an S2R
@@ -1232,7 +1234,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, MODE == 1 ? SAMU_K2
   int warp_v = threadIdx.x >> 5;   // the same for the warp index, i.e. the warp's shared block (-3.3 %)
   asm volatile("" : "+r"(warp_v));
   const int warp = warp_v;
-  WarpSmT<MODE == 1>& W = reinterpret_cast<WarpSmT<MODE == 1>*>(smem_raw)[warp];
+  WarpSmT<MODE == 1 || MODE == 3>& W = reinterpret_cast<WarpSmT<MODE == 1 || MODE == 3>*>(smem_raw)[warp];
   const int gw = blockIdx.x * SAMU_WARPS_PER_BLOCK + warp;
   uint32_t* q = P.scratch_q + (size_t)gw * P.max_q;
   uint64_t* pkey = P.scratch_key + (size_t)gw * 4 * P.max_p;
@@ -1247,7 +1249,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, MODE == 1 ? SAMU_K2
 }
 
 int32_t simulate_smem_bytes(int mode) {
-  return (int32_t)((mode == 1 ? sizeof(WarpSmT<true>) : sizeof(WarpSmT<false>)) * SAMU_WARPS_PER_BLOCK);
+  return (int32_t)(((mode == 1 || mode == 3) ? sizeof(WarpSmT<true>) : sizeof(WarpSmT<false>)) * SAMU_WARPS_PER_BLOCK);
 }
 
 template <int BSK, bool CONSTC, int MODE>
@@ -1263,12 +1265,16 @@ static cudaError_t prepare_one(int* bpsm_modes) {
 }
 
 // resident blocks per SM for each K2 mode (the minimum over that mode's instantiations)
-cudaError_t simulate_prepare(int blocks_per_sm[3]) {
-  blocks_per_sm[0] = blocks_per_sm[1] = blocks_per_sm[2] = 1 << 30;
+cudaError_t simulate_prepare(int blocks_per_sm[5]) {
+  for (int md = 0; md < 5; ++md) blocks_per_sm[md] = 1 << 30;
   cudaError_t e;
   if ((e = prepare_one<16, true, 0>(blocks_per_sm)) != cudaSuccess) return e;
   if ((e = prepare_one<16, true, 1>(blocks_per_sm)) != cudaSuccess) return e;
   if ((e = prepare_one<16, true, 2>(blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<16, true, 3>(blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<16, true, 4>(blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<16, false, 3>(blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<16, false, 4>(blocks_per_sm)) != cudaSuccess) return e;
   if ((e = prepare_one<16, false, 0>(blocks_per_sm)) != cudaSuccess) return e;
   if ((e = prepare_one<16, false, 1>(blocks_per_sm)) != cudaSuccess) return e;
   if ((e = prepare_one<16, false, 2>(blocks_per_sm)) != cudaSuccess) return e;
@@ -1284,6 +1290,8 @@ static void launch_variant(const SimLaunch& L, uint32_t block_size, int mode, in
   const dim3 blk(32 * SAMU_WARPS_PER_BLOCK);
   if (block_size == 16 && mode == 1) k_simulate<16, CONSTC, 1><<<n_blocks, blk, smem, s>>>(L);
   else if (block_size == 16 && mode == 2) k_simulate<16, CONSTC, 2><<<n_blocks, blk, smem, s>>>(L);
+  else if (block_size == 16 && mode == 3) k_simulate<16, CONSTC, 3><<<n_blocks, blk, smem, s>>>(L);
+  else if (block_size == 16 && mode == 4) k_simulate<16, CONSTC, 4><<<n_blocks, blk, smem, s>>>(L);
   else if (block_size == 16) k_simulate<16, CONSTC, 0><<<n_blocks, blk, smem, s>>>(L);
   else if ((block_size & (block_size - 1)) == 0) k_simulate<0, CONSTC, 0><<<n_blocks, blk, smem, s>>>(L);
   else k_simulate<-1, CONSTC, 0><<<n_blocks, blk, smem, s>>>(L);

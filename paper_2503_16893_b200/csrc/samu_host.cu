@@ -135,7 +135,7 @@ struct samu_ctx {
   PlanBufs pb;         // planner buffers (borrowed by Greedy / Replay for the duration of a call)
   DevBuf d_cands, d_items, d_counter, d_rep_rec, d_scratch_q, d_scratch_key, d_scratch_idx, d_error;
   DevBuf d_sum, d_gather_send, d_gather_recv;
-  int sim_blocks_per_sm[3] = {0, 0, 0};   // resident K2 blocks per SM, per K2 mode
+  int sim_blocks_per_sm[5] = {0, 0, 0, 0, 0};   // resident K2 blocks per SM, per K2 mode
 
   // stats
   int64_t n_sims = 0;
@@ -724,10 +724,11 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
   int max_phase = 0;
   for (auto& j : jobs) max_phase = std::max(max_phase, j.phase);
   if (!c->sim_blocks_per_sm[0]) {
-    int bpsm[3] = {0, 0, 0};
+    int bpsm[5] = {0, 0, 0, 0, 0};
     CK(c, simulate_prepare(bpsm));
-    if (bpsm[0] < 1 || bpsm[1] < 1 || bpsm[2] < 1) FAIL(c, SAMU_E_CUDA, "simulate: kernel does not fit on an SM");
-    for (int md = 0; md < 3; ++md) c->sim_blocks_per_sm[md] = bpsm[md];
+    for (int md = 0; md < 5; ++md)
+      if (bpsm[md] < 1) FAIL(c, SAMU_E_CUDA, "simulate: kernel does not fit on an SM");
+    for (int md = 0; md < 5; ++md) c->sim_blocks_per_sm[md] = bpsm[md];
   }
   CK(c, c->d_error.ensure(2 * sizeof(int32_t)));
   CK(c, cudaMemsetAsync(c->d_error.p, 0, 2 * sizeof(int32_t), s));
@@ -767,11 +768,12 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
       D.fin_t_out = J.fin_t_out;
       D.fin_iter_out = J.fin_iter_out;
       D.out_rec = J.out_rec;
-      // K2 path (DevCand::mode): FRESH = fresh state, no cross-node arrivals, no cut, no per-request
-      // outputs; LEAN = FRESH without chain successors
-      const bool fresh = (S.st == nullptr || J.fresh_node) && !D.resume && !D.commit && !D.src_fin && !D.tau && !D.tau_rec &&
+      // K2 path (DevCand::mode): FRESH = fresh state, no cross-node arrivals, no per-request
+      // outputs; LEAN = FRESH without chain successors; 3 / 4 = LEAN / FRESH cut at a time limit
+      const bool fresh = (S.st == nullptr || J.fresh_node) && !D.resume && !D.commit && !D.src_fin &&
                          !D.fin_t_out && !D.fin_iter_out && c->node_input[node] < 0 && c->eng.block_size == 16;
-      D.mode = !fresh ? 0 : D.has_succ ? 2 : 1;
+      const bool cut = D.tau != nullptr || D.tau_rec != nullptr;
+      D.mode = !fresh ? 0 : D.has_succ ? (cut ? 4 : 2) : (cut ? 3 : 1);
       const std::vector<uint32_t>& ho = c->rep_off_host.at({node, cd.dp});
       uint32_t mx = 0;
       for (int j = 0; j < cd.dp; ++j) mx = std::max(mx, ho[j + 1] - ho[j]);
@@ -788,14 +790,14 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
     {
       // small batches (e.g. the planner's later inner steps) run as one general launch: a launch per
       // mode only pays off when each covers several waves of the persistent grid
-      int64_t cnt[3] = {0, 0, 0};
+      int64_t cnt[5] = {0, 0, 0, 0, 0};
       for (size_t x = 0; x < dc.size(); ++x) cnt[dc[x].mode] += (int64_t)T * dc[x].dp;
       const int64_t wave = (int64_t)c->n_sm * 24;
       // SAMU_K2_MODES=always|never overrides the size rule (tests run the LEAN / FRESH paths on
       // small batches; "never" runs everything on the general path)
       const char* pol = std::getenv("SAMU_K2_MODES");
       const bool always = pol && std::strcmp(pol, "always") == 0, never = pol && std::strcmp(pol, "never") == 0;
-      const bool split = !never && (always || cnt[0] + cnt[1] + cnt[2] >= 4 * wave);
+      const bool split = !never && (always || cnt[0] + cnt[1] + cnt[2] + cnt[3] + cnt[4] >= 4 * wave);
       for (DevCand& D : dc)
         if (!split || (!always && cnt[D.mode] < wave)) D.mode = 0;
     }
@@ -805,11 +807,11 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
       if (total >= ((int64_t)1 << 31)) FAIL(c, SAMU_E_INVALID, "simulate: too many work items (trials x replicas)");
     }
     // per mode: candidate order and item offsets (the device decodes item -> (candidate, trial, replica))
-    std::vector<uint32_t> ord_off;   // [mode 0 ord | off][mode 1 ...][mode 2 ...]
-    size_t ord_at[3], off_at[3];
-    int64_t n_items[3];
-    int n_ord[3];
-    for (int md = 0; md < 3; ++md) {
+    std::vector<uint32_t> ord_off;   // [mode 0 ord | off][mode 1 ...] ... [mode 4 ...]
+    size_t ord_at[5], off_at[5];
+    int64_t n_items[5];
+    int n_ord[5];
+    for (int md = 0; md < 5; ++md) {
       std::vector<uint32_t> ordm, offm{0};
       for (int x : order)
         if (dc[x].mode == md) {
@@ -838,20 +840,20 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
     L.error = c->d_error.as<int32_t>();
     {
       // persistent grid per mode: resident blocks x SMs, no more warps than items
-      int n_blocks[3];
-      size_t n_warps = SAMU_WARPS_PER_BLOCK;   // scratch rings: modes 0 and 2 (LEAN uses none)
-      for (int md = 0; md < 3; ++md) {
+      int n_blocks[5];
+      size_t n_warps = SAMU_WARPS_PER_BLOCK;   // scratch rings: modes 0, 2, 4 (LEAN modes 1, 3 use none)
+      for (int md = 0; md < 5; ++md) {
         const int64_t want = (n_items[md] + SAMU_WARPS_PER_BLOCK - 1) / SAMU_WARPS_PER_BLOCK;
         n_blocks[md] = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->n_sm * c->sim_blocks_per_sm[md], want));
-        if (md != 1) n_warps = std::max(n_warps, (size_t)n_blocks[md] * SAMU_WARPS_PER_BLOCK);
+        if (md != 1 && md != 3) n_warps = std::max(n_warps, (size_t)n_blocks[md] * SAMU_WARPS_PER_BLOCK);
       }
       CK(c, c->d_scratch_q.ensure(sizeof(uint32_t) * n_warps * max_q));
       CK(c, c->d_scratch_key.ensure(sizeof(uint64_t) * n_warps * 4 * max_p));
       CK(c, c->d_scratch_idx.ensure(sizeof(uint32_t) * n_warps * 4 * max_p));
       CK(c, upload(c->d_cands, dc, s));
       CK(c, upload(c->d_items, ord_off, s));
-      CK(c, c->d_counter.ensure(3 * sizeof(uint32_t)));
-      CK(c, cudaMemsetAsync(c->d_counter.p, 0, 3 * sizeof(uint32_t), s));
+      CK(c, c->d_counter.ensure(5 * sizeof(uint32_t)));
+      CK(c, cudaMemsetAsync(c->d_counter.p, 0, 5 * sizeof(uint32_t), s));
       CK(c, c->d_rep_rec.ensure(sizeof(samu_trial_rec) * 16 * idx.size() * T));
       L.cands = c->d_cands.as<DevCand>();
       L.ord = nullptr;
@@ -864,9 +866,9 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
       L.scratch_idx = c->d_scratch_idx.as<uint32_t>();
       L.max_q = (int32_t)max_q;
       L.max_p = (int32_t)max_p;
-      SimLaunch LM[3];
-      int modes[3], nb[3], n_launch = 0;
-      for (int md : {0, 2, 1}) {   // general, FRESH (on s, in order), LEAN (concurrent on the aux stream)
+      SimLaunch LM[5];
+      int modes[5], nb[5], n_launch = 0;
+      for (int md : {0, 2, 4, 3, 1}) {   // in order on s; the LEAN launch (1) concurrent on the aux stream
         if (n_items[md] == 0) continue;
         SimLaunch& X = LM[n_launch];
         X = L;
@@ -887,7 +889,7 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
       // concurrent LEAN launch only when the other launch is short (a few waves): then its
       // longest replica-sims are the critical path and the LEAN items fill the idle warps; with
       // many waves the two kernels only compete for the instruction cache (~2 % slower)
-      const bool overlap = n_items[0] + n_items[2] < 8 * (int64_t)c->n_sm * 24;
+      const bool overlap = n_items[0] + n_items[2] + n_items[3] + n_items[4] < 8 * (int64_t)c->n_sm * 24;
       CK(c, launch_simulate(LM, modes, nb, n_launch, dc.data(), (uint32_t)c->eng.block_size, s,
                             overlap ? c->aux_stream : nullptr, c->ev_fork, c->ev_join));
       c->launches += n_launch > 1 ? n_launch - 1 : 0;

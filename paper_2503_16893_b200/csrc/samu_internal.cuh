@@ -38,7 +38,7 @@ struct DevEcdf {
 // One candidate (node, plan) as the simulation kernel sees it.
 struct DevCand {
   int32_t node, dp, tp, resume, commit, has_succ;
-  int32_t mode;                // K2 path: 0 general, 2 FRESH (fresh state, no arrivals / cut / outputs), 1 LEAN (FRESH, no successors)
+  int32_t mode;                // K2 path: 0 general, 2 FRESH (fresh state, no arrivals / cut / outputs), 1 LEAN (FRESH, no successors), 3 / 4 = LEAN / FRESH cut at tau
   uint32_t max_seqs, bs, budget;
   int32_t blocks;              // KV blocks per replica (c5)
   uint32_t L, h_tp;            // layers, h / tp
@@ -94,7 +94,7 @@ cudaError_t launch_dense_coeff(const double* bucket_B, int32_t nb, const double*
 cudaError_t launch_simulate(const SimLaunch* Ls, const int* modes, const int32_t* n_blocks, int n_launch,
                             const DevCand* host_cands, uint32_t block_size, cudaStream_t s, cudaStream_t s2,
                             cudaEvent_t ev_fork, cudaEvent_t ev_join);
-cudaError_t simulate_prepare(int blocks_per_sm[3]);   // per K2 mode
+cudaError_t simulate_prepare(int blocks_per_sm[5]);   // per K2 mode
 
 int32_t simulate_smem_bytes(int mode);
 cudaError_t launch_combine(const samu_trial_rec* rep_rec, const DevCand* cands, int32_t n_cands, int32_t n_trials,

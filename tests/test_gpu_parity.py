@@ -390,6 +390,33 @@ def test_no_preemption_plan_bit_exact(name, kw, T, algo):
     assert pg == po
 
 
+@pytest.mark.parametrize("preemption", [True, False])
+def test_planner_all_k2_paths(preemption):
+    # every planner simulation that qualifies runs on K2's LEAN / FRESH / cut paths
+    # (SAMU_K2_MODES=always), including never-committed chain nodes without dependents (FRESH
+    # with a WorkloadState buffer present) and their cut simulations; the plan must not change
+    rng = np.random.default_rng(77)
+    l_in, l_out, pred, chain = [], [], [], []
+    for c in range(12):
+        for j in range(int(rng.integers(1, 5))):
+            pred.append(-1 if j == 0 else len(l_in) - 1)
+            chain.append(c)
+            l_in.append(int(rng.integers(20, 200)))
+            l_out.append(int(rng.integers(5, 80)))
+    sp = F.spec(l_max=600, tp_values=(1, 2), L=2, h=16, c=1000)
+    ld = F.zero_load() + 0.5
+    w = F.multi([dict(l_in=np.array(l_in), l_out=np.array(l_out), pred=np.array(pred), chain=np.array(chain), sp=sp,
+                      load=ld),
+                 dict(l_in=rng.integers(5, 100, 40), l_out=rng.integers(5, 120, 40), sp=sp, load=ld),
+                 dict(l_in=rng.integers(5, 100, 30), l_out=rng.integers(5, 90, 30), sp=sp, load=ld)],
+                eng=F.engine(n_gpus=4, max_num_seqs=16, kv_cap=2000), n_trials=3)
+    po = O.Problem(w).plan_greedy(SEED, 3, "greedy", preemption=preemption)
+    with k2_modes("always"):
+        pg = gpu(w).samu_plan_greedy(SEED, 3, "greedy", preemption=preemption)
+    pg.pop("n_sims")
+    assert pg == po
+
+
 def test_known_lengths_bit_exact():
     w = W.make_workload("c5", n_prompts=200, n_docs=60, n_trials=1)
     rng = np.random.default_rng(7)
