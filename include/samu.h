@@ -214,8 +214,9 @@ samu_status samu_known_lengths(samu_ctx* ctx, const uint32_t* l_true, uint16_t* 
  * Candidates with commit = 1 must be distinct nodes and need `state`.
  * SAMU_E_INVALID also when n_trials x n_req >= 2^32 (K2 indexes [trial][request] with 32 bits)
  * or the batch has >= 2^31 work items (trials x dp replicas).
- * Execution: one K2 launch per path present — LEAN (fresh state, independent requests, no time
- * limit, no per-request outputs), FRESH (the same with chain successors) and the general one;
+ * Execution: one K2 launch per path present — LEAN (fresh state, independent requests, no
+ * per-request outputs), FRESH (the same with chain successors), each with or without a time
+ * limit, and the general one;
  * SAMU_K2_MODES=always|never in the environment overrides the batch-size rule that picks them.
  * The results do not depend on the path. */
 samu_status samu_simulate_batch(samu_ctx* ctx, const samu_candidate* cands, int32_t n_cands,

@@ -5,10 +5,11 @@
 //  * persistent grid, one work item per warp, pulled from an atomic counter; items are decoded on
 //    the device from the launch's longest-first candidate order and item offsets (replica-sims
 //    differ ~100x in length);
-//  * three instantiations per block size, one launch each (MODE): LEAN (fresh state, independent
-//    requests: the queue is the replica list), FRESH (fresh state with chain successors) and the
-//    general one (carried state, commit, time limits, cross-node arrivals); candidate
-//    descriptors are read from the constant bank;
+//  * instantiations per block size, one launch each (MODE): LEAN (fresh state, independent
+//    requests: the queue is the replica list), FRESH (fresh state with chain successors), both
+//    also with a time limit (cut simulations), and the general one (carried state, commit,
+//    resume, cross-node arrivals, finish records); candidate descriptors are read from the
+//    constant bank;
 //  * the running set lives in shared memory: 256 slots, lane L owns slots L + 32 j (bank-conflict
 //    free), with the lane's occupancy bits in a register; a 32-entry register window, circular
 //    over the lanes, caches the head of the waiting queue;
