@@ -20,6 +20,9 @@ for name, kw in [("c2", dict(n_prompts=60)), ("c4", dict(n_docs=20)), ("c5", dic
     S.samu_simulate_batch([cands[0][:3] + (0, -1, 1)], lo, li, state=st, time_limit=np.array([[5.0, 7.0]]))
     S.samu_simulate_batch([cands[0][:3] + (1, -1, 0), (cands[0][0], 1, 1, 0, -1, 0)], lo, li, state=st)
     print(name, "greedy stages", len(S.samu_plan_greedy(w.seed, 2)["stages"]))
+    os.environ["SAMU_K2_MODES"] = "always"   # the planner's fresh full and cut simulations on LEAN / FRESH
+    print(name, "greedy stages (all K2 paths)", len(S.samu_plan_greedy(w.seed, 2)["stages"]))
+    del os.environ["SAMU_K2_MODES"]
     S.close()
 torch.cuda.synchronize()
 print("sanitize run ok")
