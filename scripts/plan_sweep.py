@@ -1,4 +1,4 @@
-"""Randomised planner sweep: small multi-node workloads (chain and independent nodes), greedy /
+"""Randomised planner sweep: small multi-node workloads (chain, evaluator and independent nodes), greedy /
 Max / Min with and without preemption, default and SAMU_K2_MODES=always, GPU plan vs oracle plan.
 
   python scripts/plan_sweep.py [n_seeds]"""
@@ -33,7 +33,14 @@ for seed in range(n_seeds):
                     l_out.append(int(rng.integers(3, 70)))
             nodes.append(dict(l_in=np.array(l_in), l_out=np.array(l_out), pred=np.array(pred), chain=np.array(chain),
                               sp=sp, load=ld))
+            finals = [base + i for i in range(len(l_in)) if i + 1 == len(l_in) or chain[i + 1] != chain[i]]
             base += len(l_in)
+            if rng.random() < 0.6:   # an evaluator node fed by every chain's final summary
+                e_pred = np.repeat(np.array(finals), int(rng.integers(1, 3)))
+                nodes.append(dict(l_in=np.full(len(e_pred), int(rng.integers(10, 60))),
+                                  l_out=rng.integers(1, 40, len(e_pred)), pred=e_pred, sp=sp,
+                                  load=F.zero_load() + float(rng.uniform(0, 1.5))))
+                base += len(e_pred)
         else:
             m = int(rng.integers(5, 60))
             nodes.append(dict(l_in=rng.integers(5, 120, m), l_out=rng.integers(1, 100, m), sp=sp, load=ld))
