@@ -719,3 +719,18 @@ def test_nccl_path_one_rank_matches_oracle():
         for x in rec["t_end"]:
             s += float(x)
         assert mean == s / 3
+
+
+# ------------------------------------------------------------------------------------------
+# randomised sweeps (the long versions: scripts/fuzz_sweep.py 2000, scripts/plan_sweep.py 200)
+# ------------------------------------------------------------------------------------------
+def test_random_simulation_sweep():
+    import scripts.fuzz_sweep as fs
+    checked, bad = fs.sweep(120)
+    assert checked > 500 and bad == 0
+
+
+def test_random_planner_sweep():
+    import scripts.plan_sweep as ps
+    checked, bad = ps.sweep(24)
+    assert checked > 150 and bad == 0
