@@ -696,6 +696,9 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1 |
         K2STAT(7, 1);
         const uint32_t B = m.B;
         const double stop_t = m.stop;
+        // modes 1 / 2: no time limit and no arrivals, stop_t = +inf; in the exact-sum chunks a
+        // partial sum that is not below it is not below 2^(e+1) either (already a fallback)
+        constexpr bool NOSTOP = MODE == 1 || MODE == 2;
         // KV need of the run's decodes: histogram rotated to start at needidx, prefix sums
         const uint32_t hv = (uint32_t)lane < bs.v() ? W.hist[bs.mod(m.needidx + bs.v() - (uint32_t)lane)] : 0u;
         const uint32_t m_fin = m.next_fin - m.d;
@@ -761,8 +764,8 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1 |
               }
               const double acc_b = __dadd_rn(t, psum);                              // after 2j + 1
               const double acc_a = __dadd_rn(t, __dadd_rn(__dsub_rn(psum, rp), r0));   // after 2j
-              const bool stop_a = !(acc_a < stop_t);
-              const uint32_t bstop = __ballot_sync(FULL, stop_a || !(acc_b < stop_t));
+              const bool stop_a = !NOSTOP && !(acc_a < stop_t);
+              const uint32_t bstop = NOSTOP ? 0u : __ballot_sync(FULL, stop_a || !(acc_b < stop_t));
               const uint32_t L = bstop ? (uint32_t)(__ffs(bstop) - 1) : 31u;
               const bool chk_b = (uint32_t)lane < L || ((uint32_t)lane == L && !stop_a);
               const bool bad = (uint32_t)lane <= L &&
@@ -815,7 +818,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1 |
                   }
                   const double acc_j = __dadd_rn(t, psum);   // partial sum after iteration lane
                   const bool in = (uint32_t)lane < cnt;
-                  const uint32_t bstop = __ballot_sync(FULL, in && !(acc_j < stop_t));
+                  const uint32_t bstop = NOSTOP ? 0u : __ballot_sync(FULL, in && !(acc_j < stop_t));
                   const uint32_t upto = bstop ? (uint32_t)(__ffs(bstop) - 1) : cnt - 1;   // last lane used
                   const bool bad = (uint32_t)lane <= upto && (cj < 0.0 || fabs(err) == halfu || !(acc_j < top));
                   if (!__any_sync(FULL, bad)) {
