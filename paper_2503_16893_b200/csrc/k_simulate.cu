@@ -31,6 +31,10 @@
 
 #include <mutex>
 
+#ifndef SAMU_K2_CHUNK_MIN
+#define SAMU_K2_CHUNK_MIN 4   // decode runs longer than this take the lane-parallel chunk sums
+#endif
+
 #ifdef SAMU_K2_STATS   // debug build only: event counters (scripts/k2_stats.py)
 __device__ unsigned long long g_k2_stats[16];
 #define K2STAT(i, v) do { if (lane == 0) atomicAdd(&g_k2_stats[i], (unsigned long long)(v)); } while (0)
@@ -731,7 +735,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1 |
           const double2 cc = __ldg(cb), cp = __ldg(cb + 1), cs = __ldg(cb + 2);
           const double ac = cc.x, bc = cc.y, ap = cp.x, bp = cp.y, as_ = cs.x, bs_ = cs.y;
           double t = m.t;
-          if (m_run > 4) {
+          if (m_run > SAMU_K2_CHUNK_MIN) {
             // lane j evaluates iteration done_it + j of a 32-iteration chunk (the x of every
             // iteration are exact integers, so their conversions equal the sequential
             // increments), then the chunk's costs are added to t one by one in iteration order
@@ -882,7 +886,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1 |
           }
           m.t = t;
           K2STAT(8, done_it);
-          if (m_run > 4) K2STAT(14, 1);
+          if (m_run > SAMU_K2_CHUNK_MIN) K2STAT(14, 1);
           // closed-form exact updates for the done_it iterations of the run
           // sum_j (K0 + K1 (S + B j)) = L c (B mm) + K1 (mm S + B mm (mm - 1) / 2); mm <= l_max < 2^16,
           // so mm (mm - 1) fits 32 bits and every product is one widening 32 x 32 multiply
