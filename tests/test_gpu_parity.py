@@ -582,6 +582,18 @@ def test_greedy_plan_bit_exact_mixed_c5_shape():
     assert pg["total"] == po["total"] and pg["n_cand_evals"] == po["n_cand_evals"]
 
 
+@pytest.mark.parametrize("algo", ["greedy", "max", "min"])
+def test_full_size_c5_plan_bit_exact(algo):
+    # the full bench workload (12 nodes, 50k requests, every K2 path the planner takes: LEAN /
+    # FRESH / cut / general), one trial so the oracle finishes in ~30 s: every stage, f*, mean
+    # end time, T_E and the planned total bit for bit
+    w = W.make_workload("c5", n_trials=1)
+    po = O.Problem(w).plan_greedy(SEED, 1, algo)
+    pg = gpu(w).samu_plan_greedy(SEED, 1, algo)
+    pg.pop("n_sims")
+    assert pg == po
+
+
 # ------------------------------------------------------------------------------------------
 # multi-rank trial sharding on one GPU: in-process rank group (same collectives as NCCL)
 # ------------------------------------------------------------------------------------------
