@@ -583,13 +583,14 @@ def test_greedy_plan_bit_exact_mixed_c5_shape():
 
 
 @pytest.mark.parametrize("algo", ["greedy", "max", "min"])
-def test_full_size_c5_plan_bit_exact(algo):
-    # the full bench workload (12 nodes, 50k requests, every K2 path the planner takes: LEAN /
-    # FRESH / cut / general), one trial so the oracle finishes in ~30 s: every stage, f*, mean
-    # end time, T_E and the planned total bit for bit
-    w = W.make_workload("c5", n_trials=1)
-    po = O.Problem(w).plan_greedy(SEED, 1, algo)
-    pg = gpu(w).samu_plan_greedy(SEED, 1, algo)
+@pytest.mark.parametrize("name,T", [("c2", 2), ("c3", 2), ("c4", 1), ("c5", 1)])
+def test_full_size_plan_bit_exact(name, T, algo):
+    # the full BASELINE workloads (C5 = the bench workload: 12 nodes, 50k requests, every K2 path
+    # the planner takes: LEAN / FRESH / cut / general), few trials so the oracle finishes in
+    # ~30 s: every stage, f*, mean end time, T_E and the planned total bit for bit
+    w = W.make_workload(name, n_trials=T)
+    po = O.Problem(w).plan_greedy(SEED, T, algo)
+    pg = gpu(w).samu_plan_greedy(SEED, T, algo)
     pg.pop("n_sims")
     assert pg == po
 
