@@ -457,6 +457,23 @@ def test_replay_bit_exact(name, kw, algo):
     assert S.samu_replay_plan(plan, 0, known_l_out=l_true) == P.replay(plan, 0, known_l_out=l_true)
 
 
+@pytest.mark.parametrize("name", ["c4", "c5"])
+def test_full_size_replay_and_ablation_bit_exact(name):
+    # full BASELINE workloads: replay of the oracle's Max-heuristic plan against mispredicted and
+    # known lengths, and the Min-heuristic plan without preemption on known lengths (§5.5)
+    w = W.make_workload(name, n_trials=1)
+    P = O.Problem(w)
+    plan = P.plan_greedy(SEED, 1, "max")
+    S = gpu(w)
+    assert S.samu_replay_plan(plan, 4242) == P.replay(plan, 4242)
+    l_true = np.random.default_rng(5).integers(1, 2000, w.n_req).astype(np.uint32)
+    assert S.samu_replay_plan(plan, 0, known_l_out=l_true) == P.replay(plan, 0, known_l_out=l_true)
+    po = P.plan_greedy(SEED, 1, "min", preemption=False, known_l_out=l_true)
+    pg = S.samu_plan_greedy(SEED, 1, "min", preemption=False, known_l_out=l_true)
+    pg.pop("n_sims")
+    assert pg == po
+
+
 def test_replay_hand_fixtures_bit_exact():
     from tests.test_oracle_pins import _hand_plan, _replay_fixture
     cases = [(_replay_fixture([2, 3, 4], 4, cap=8), [[(0, 1, 1), (1, 1, 1), (2, 1, 1)], [(1, 1, 1), (2, 2, 1)]],
