@@ -66,3 +66,22 @@ def test_no_cpu_fallback():
     from paper_2503_16893_b200 import Samu
     with pytest.raises(RuntimeError):
         Samu(0)
+
+
+def test_product_and_oracle_share_nothing():
+    # the CUDA path and the oracle are independent: no imports, includes or links either way
+    import re
+    pkg = os.path.join(ROOT, "paper_2503_16893_b200")
+    for d, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(d, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", src, re.M), f
+                assert not re.search(r'#include\s*[<"][^>"]*oracle', src), f
+                assert "liboracle" not in src, f
+    for f in os.listdir(os.path.join(ROOT, "oracle")):
+        if f.endswith((".py", ".cpp", ".h")):
+            src = open(os.path.join(ROOT, "oracle", f)).read()
+            assert not re.search(r"^\s*(import|from)\s+paper_2503_16893_b200\b", src, re.M), f
+            assert "libsamu" not in src, f
+            assert not re.search(r'#include\s*[<"][^>"]*samu', src), f
