@@ -67,6 +67,19 @@ REC_DTYPE = np.dtype([("t_end", "<f8"), ("flops_lo", "<u8"), ("flops_hi", "<u8")
                       ("req_iters", "<u8"), ("iters", "<u4"), ("flags", "<u4")])
 
 
+class or_summary(C.Structure):
+    _fields_ = [("mean_t", C.c_double), ("p50_t", C.c_double), ("p90_t", C.c_double), ("p99_t", C.c_double),
+                ("mean_flops", C.c_double), ("mean_req_iters", C.c_double)]
+
+
+SUMMARY_DTYPE = np.dtype([("mean_t", "<f8"), ("p50_t", "<f8"), ("p90_t", "<f8"), ("p99_t", "<f8"),
+                          ("mean_flops", "<f8"), ("mean_req_iters", "<f8")])
+
+ITER_DTYPE = np.dtype([("t_start", "<f8"), ("lat", "<f8"), ("flops", "<u8"), ("s", "<u8"), ("S", "<u8"),
+                       ("free_blocks", "<i8"), ("kind", "<u4"), ("B", "<u4"), ("n_preempted", "<u4"),
+                       ("n_finished", "<u4")])
+
+
 class or_stage(C.Structure):
     _fields_ = [("n_entries", C.c_int32), ("node", C.c_int32 * 16), ("dp", C.c_int32 * 16),
                 ("tp", C.c_int32 * 16), ("fstar", C.c_int32), ("mean_tE", C.c_double),
@@ -97,7 +110,8 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        L = C.CDLL(build())
+        # SAMU_ORACLE_SO: an alternative build of the same source (the sanitizer test)
+        L = C.CDLL(os.environ.get("SAMU_ORACLE_SO") or build())
         P = C.c_void_p
         L.or_last_error.restype = C.c_char_p
         L.or_problem_create.restype = P
@@ -120,6 +134,9 @@ def lib():
         L.or_simulate.argtypes = [P, C.POINTER(or_cand), C.c_int32, P, P, P, P, P, P, P, P,
                                   C.c_int32, P, P, P]
         L.or_simulate_many.argtypes = [P, C.c_int32, P, C.c_int32, P, P, C.c_int32, P]
+        L.or_summarise.argtypes = [C.c_int32, C.c_int32, P, P]
+        L.or_trace_replica.argtypes = [P, C.POINTER(or_cand), P, P, C.c_int32, C.c_int64, P, C.c_int64, P, P, P,
+                                       C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.or_plan_greedy.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(or_plan)]
         L.or_plan_max_heuristic.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(or_plan)]
         L.or_plan_min_heuristic.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(or_plan)]
@@ -276,6 +293,24 @@ class Problem:
         _check(lib().or_simulate_many(self.h, len(cands), cs, T, _ptr(l_out), _ptr(l_in), n_threads, _ptr(rec)))
         return rec
 
+    def trace(self, node, dp, tp, l_out_row, l_in_row, replica=0):
+        """Per-iteration descriptors of one fresh replica-sim and the running set
+        [(request, g)] after every iteration."""
+        lo = np.ascontiguousarray(l_out_row, np.uint16)
+        li = np.ascontiguousarray(l_in_row, np.uint16)
+        cand = or_cand(node, dp, tp, 0)
+        nd, nr = C.c_int64(0), C.c_int64(0)
+        lib().or_trace_replica(self.h, C.byref(cand), _ptr(lo), _ptr(li), replica, 0, None, 0, None, None, None,
+                               C.byref(nd), C.byref(nr))
+        desc = np.zeros(nd.value, ITER_DTYPE)
+        req = np.zeros(max(nr.value, 1), np.uint32)
+        g = np.zeros(max(nr.value, 1), np.uint32)
+        off = np.zeros(nd.value + 1, np.int64)
+        _check(lib().or_trace_replica(self.h, C.byref(cand), _ptr(lo), _ptr(li), replica, nd.value, _ptr(desc),
+                                      nr.value, _ptr(req), _ptr(g), _ptr(off), C.byref(nd), C.byref(nr)))
+        running = [list(zip(req[off[i]:off[i + 1]].tolist(), g[off[i]:off[i + 1]].tolist())) for i in range(nd.value)]
+        return desc, running
+
     def replay(self, plan, seed, known_l_out=None):
         """Run `plan` (a dict from plan_greedy) against true lengths with the dynamic scheduler
         (P:620-627): known_l_out [n_req], or trial 0 of the sampler with `seed`."""
@@ -329,6 +364,15 @@ def fit_coeffs(off, x, y, trim_permille=10):
     n_used, flags = np.zeros(nb, np.int32), np.zeros(nb, np.int32)
     rc = lib().or_fit_coeffs(nb, _ptr(off), _ptr(x), _ptr(y), trim_permille, _ptr(a), _ptr(b), _ptr(n_used), _ptr(flags))
     return a, b, n_used, flags, rc
+
+
+def summarise(recs) -> np.ndarray:
+    """Per-candidate mean / nearest-rank p50, p90, p99 of t_end, mean FLOPs and mean
+    request-iterations over trials (reading c17); recs [n_cands][T] (REC_DTYPE)."""
+    r = np.ascontiguousarray(np.atleast_2d(recs), REC_DTYPE)
+    out = np.zeros(r.shape[0], SUMMARY_DTYPE)
+    _check(lib().or_summarise(r.shape[0], r.shape[1], _ptr(r), _ptr(out)))
+    return out
 
 
 def rec_flops(rec) -> np.ndarray:

@@ -341,6 +341,10 @@ struct SimCtx {
   bool commit;
   uint32_t* out_fin_iter;
   double* out_fin_t;
+  // optional per-iteration trace (or_trace_replica): descriptors and the running set after each
+  std::vector<or_iter_desc>* trace = nullptr;
+  std::vector<std::pair<uint32_t, uint32_t>>* trace_run = nullptr;
+  std::vector<int64_t>* trace_off = nullptr;
 };
 
 struct RepOut { double t_end; u128 flops; uint64_t req_iters; uint32_t iters; bool done; bool cut; int err; };
@@ -446,6 +450,7 @@ static RepOut sim_replica(SimCtx& C, const std::vector<int>& reqs, double t0, in
     }
     uint64_t it_flops, B, s, S;
     std::vector<int> finished;
+    uint32_t n_victims = 0;
     if (!A.empty()) {
       // (4) prefill iteration: prompt (+ already generated tokens when recomputing) of every
       // admitted request; it emits one token each (c4)
@@ -472,6 +477,7 @@ static RepOut sim_replica(SimCtx& C, const std::vector<int>& reqs, double t0, in
         if ((l - 1) % C.bs == 0) --need;
         R.pop_back();
         W.push_front({v, PRE});
+        ++n_victims;
         if (R.empty()) { out.err = OR_E_INFEASIBLE; return out; }
       }
       F -= need;
@@ -493,6 +499,7 @@ static RepOut sim_replica(SimCtx& C, const std::vector<int>& reqs, double t0, in
     for (int ph = 0; ph < 3; ++ph) { av[ph] = C.a[ph * C.max_seqs + (B - 1)]; bv[ph] = C.b[ph * C.max_seqs + (B - 1)]; }
     a3 = av;
     double lat = or_iter_latency(a3, bv, it_flops, B * s, S);
+    const double t_start = t;
     t = t + lat;
     out.flops += it_flops;
     out.req_iters += B;
@@ -506,6 +513,15 @@ static RepOut sim_replica(SimCtx& C, const std::vector<int>& reqs, double t0, in
     }
     std::sort(released.begin(), released.end());
     for (int sr : released) W.push_back({sr, QUEUED});   // ready at t, (t, index) order (c19)
+    if (C.trace) {
+      or_iter_desc d;
+      d.t_start = t_start; d.lat = lat; d.flops = it_flops; d.s = s; d.S = S; d.free_blocks = F;
+      d.kind = A.empty() ? 1u : 0u; d.B = (uint32_t)B; d.n_preempted = n_victims;
+      d.n_finished = (uint32_t)finished.size();
+      C.trace->push_back(d);
+      for (int r : R) C.trace_run->push_back({(uint32_t)r, G(r)});
+      C.trace_off->push_back((int64_t)C.trace_run->size());
+    }
     ++iter;
   }
   out.t_end = t;
@@ -646,6 +662,87 @@ extern "C" int32_t or_simulate_many(const or_problem* p, int32_t n_cands, const 
   for (int i = 0; i < std::max(1, n_threads); ++i) th.emplace_back(work);
   for (auto& x : th) x.join();
   return err.load();
+}
+
+// Per-iteration trace of one fresh replica-sim: the same sim_replica, with the trace hook.
+extern "C" int32_t or_trace_replica(const or_problem* p, const or_cand* cand, const uint16_t* l_out, const uint16_t* l_in,
+                                    int32_t replica, int64_t cap_desc, or_iter_desc* out_desc, int64_t cap_run,
+                                    uint32_t* run_req, uint32_t* run_g, int64_t* run_off, int64_t* n_desc, int64_t* n_run) {
+  if (cand->node < 0 || cand->node >= (int)p->node_model.size() || replica < 0 || replica >= cand->dp) {
+    set_err("trace: bad candidate or replica");
+    return OR_E_INVALID;
+  }
+  SimCtx C;
+  if (prepare_ctx(p, *cand, C)) { set_err("trace: invalid plan for model"); return OR_E_INVALID; }
+  C.p = p; C.node = cand->node; C.model = p->node_model[cand->node]; C.dp = cand->dp; C.tp = cand->tp;
+  C.resume = false;
+  C.l_out = l_out; C.l_in = l_in;
+  C.st = nullptr; C.g_st = nullptr; C.fin_t = nullptr; C.over = nullptr; C.src_fin = nullptr;
+  C.tau = std::numeric_limits<double>::infinity(); C.commit = false;
+  C.out_fin_iter = nullptr; C.out_fin_t = nullptr;
+  std::vector<or_iter_desc> tr;
+  std::vector<std::pair<uint32_t, uint32_t>> run;
+  std::vector<int64_t> off{0};
+  C.trace = &tr; C.trace_run = &run; C.trace_off = &off;
+  // the replica's requests (c13), as in sim_candidate_trial
+  std::vector<int> reqs;
+  for (int r = p->node_begin[cand->node]; r < p->node_end[cand->node]; ++r) {
+    const Req& q = p->req[r];
+    const int key = q.chain >= 0 ? q.chain : (r - p->node_begin[cand->node]);
+    if (key % cand->dp == replica) reqs.push_back(r);
+  }
+  const Model& M = p->models[C.model];
+  const double t0 = M.load[(size_t)log2_exact((uint32_t)cand->tp) * OR_MAX_DP + (cand->dp - 1)];
+  RepOut o = sim_replica(C, reqs, t0, replica);
+  if (o.err) { set_err("trace: simulation error"); return o.err; }
+  *n_desc = (int64_t)tr.size();
+  *n_run = (int64_t)run.size();
+  if ((int64_t)tr.size() > cap_desc || (int64_t)run.size() > cap_run || !out_desc || !run_req || !run_g || !run_off) {
+    set_err("trace: capacity too small");   // (a size query passes null buffers)
+    return OR_E_INVALID;
+  }
+  for (size_t i = 0; i < tr.size(); ++i) out_desc[i] = tr[i];
+  for (size_t i = 0; i < run.size(); ++i) { run_req[i] = run[i].first; run_g[i] = run[i].second; }
+  for (size_t i = 0; i < off.size(); ++i) run_off[i] = off[i];
+  return OR_OK;
+}
+
+// Per-candidate trial summaries (north star: "a segmented reduction to per-candidate mean and
+// percentile latency"; reading c17), written as the definitions: mean = left-to-right fp64 sum
+// of the trial totals in trial order / T; the p-th percentile = the nearest-rank order statistic
+// sorted[ceil(p T / 100) - 1]; mean FLOPs = dbl(exact u128 sum) / T; mean request-iterations
+// = dbl(exact u64 sum) / T.
+static double u128_dbl(u128 x) {   // c17: dbl(hi) * 2^64 + dbl(lo), each step RN
+  return (double)(uint64_t)(x >> 64) * 18446744073709551616.0 + (double)(uint64_t)x;
+}
+
+extern "C" int32_t or_summarise(int32_t n_cands, int32_t n_trials, const or_rec* recs, or_summary* out) {
+  if (n_cands < 0 || n_trials < 1 || !recs || !out) { set_err("summarise: bad arguments"); return OR_E_INVALID; }
+  for (int c = 0; c < n_cands; ++c) {
+    const or_rec* r = recs + (size_t)c * n_trials;
+    double sum = 0.0;
+    u128 fl = 0;
+    uint64_t ri = 0;
+    std::vector<double> v(n_trials);
+    for (int k = 0; k < n_trials; ++k) {
+      sum = sum + r[k].t_end;
+      fl += ((u128)r[k].flops_hi << 64) | r[k].flops_lo;
+      ri += r[k].req_iters;
+      v[k] = r[k].t_end;
+    }
+    std::sort(v.begin(), v.end());
+    auto rank = [&](int pct) {   // ceil(pct * T / 100) - 1, at least 0
+      const int64_t q = ((int64_t)pct * n_trials + 99) / 100;
+      return v[(size_t)std::max<int64_t>(q - 1, 0)];
+    };
+    out[c].mean_t = sum / (double)n_trials;
+    out[c].p50_t = rank(50);
+    out[c].p90_t = rank(90);
+    out[c].p99_t = rank(99);
+    out[c].mean_flops = u128_dbl(fl) / (double)n_trials;
+    out[c].mean_req_iters = (double)ri / (double)n_trials;
+  }
+  return OR_OK;
 }
 
 // ---------------------------------------------------------------------------------------------

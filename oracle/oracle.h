@@ -128,6 +128,33 @@ int32_t or_simulate_many(const or_problem* p, int32_t n_cands, const or_cand* ca
                          const uint16_t* l_out, const uint16_t* l_in_eff, int32_t n_threads,
                          or_rec* out_rec /*[n_cands][T]*/);
 
+/* per-candidate summaries over T trials (north star "segmented reduction to per-candidate mean
+ * and percentile latency"; reading c17): mean = sequential fp64 sum in trial order / T,
+ * percentiles nearest rank sorted[ceil(p T / 100) - 1], mean FLOPs = dbl(u128 sum) / T */
+typedef struct or_summary {
+  double mean_t, p50_t, p90_t, p99_t, mean_flops, mean_req_iters;
+} or_summary;
+int32_t or_summarise(int32_t n_cands, int32_t n_trials, const or_rec* recs /*[n_cands][T]*/, or_summary* out);
+
+/* per-iteration descriptor of one replica-sim ("per-iteration trace dump":
+ * t_start, kind, B, s, S, flops, latency), plus the KV state after the iteration */
+typedef struct or_iter_desc {
+  double t_start, lat;         /* clock at the iteration's start; its latency */
+  uint64_t flops, s, S;        /* Eq. prefill / decode FLOPs; max and total length fed */
+  int64_t free_blocks;         /* KV blocks free after the iteration (reading c5) */
+  uint32_t kind;               /* 0 prefill, 1 decode */
+  uint32_t B;                  /* batch size */
+  uint32_t n_preempted;        /* victims of this (decode) iteration (c7) */
+  uint32_t n_finished;
+} or_iter_desc;
+/* fresh-state full simulation of replica `replica` of one candidate in one trial (l_out, l_in
+ * [n_req] of that trial); after every iteration the running set is listed as (request, g)
+ * pairs, run_off[i]..run_off[i+1] for iteration i.  *n_desc / *n_run receive the needed sizes;
+ * returns OR_E_INVALID (after filling them) when a capacity is too small. */
+int32_t or_trace_replica(const or_problem* p, const or_cand* cand, const uint16_t* l_out, const uint16_t* l_in,
+                         int32_t replica, int64_t cap_desc, or_iter_desc* out_desc, int64_t cap_run,
+                         uint32_t* run_req, uint32_t* run_g, int64_t* run_off, int64_t* n_desc, int64_t* n_run);
+
 /* Algorithm 1 greedy search with the estimator */
 int32_t or_plan_greedy(const or_problem* p, uint64_t seed, int32_t n_trials, or_plan* out);
 

@@ -85,3 +85,35 @@ def even_split_4x8():
     sp = spec(tp_values=(1, 2))
     nodes = [dict(l_in=[4] * n, l_out=[3] * n, sp=sp) for n in (40, 400, 400, 400)]
     return multi(nodes, eng=engine(n_gpus=8, max_num_seqs=16))
+
+
+def reload_fixture(coeff_kind="const"):
+    """Carried state cut mid-decode, then reloaded under another plan (S:406, P:494-496,
+    reading c18).  One node with tp in {1, 2}, block size 4, KV 20 tokens per GPU (5 blocks at
+    tp = 1, 10 at tp = 2), 2 slots, token budget 16 (l_max 16), 2 planned GPUs; requests
+    A (l_in 4, l_out 7), B (l_in 4, l_out 8) and C (l_in 4, l_out 2); loading (dp 1, tp 2) costs 10 s, everything
+    else 0.  The hand traces are in tests/test_oracle_state_pins.py."""
+    sp = spec(l_max=16, tp_values=(1, 2))
+    load = zero_load()
+    load[1, 0] = 10.0
+    return tiny([4, 4, 4], [7, 8, 2], sp=sp, cf=coeff_kind, load=load,
+                eng=engine(block_size=4, kv_cap=20, min_batched_tokens=1, max_num_seqs=2, n_gpus=2))
+
+
+def chatglm_fixture():
+    """AC6 ("it takes 48s to run chatglm3-6b on 1 GPU and 32s on 8 GPUs"): model 0
+    completes 1000 one-token requests in 48 simulated seconds at (dp 1, tp 1) (21 slots: 48
+    prefill iterations of 1 s) and in 32 s at (1, 8) (2/3 s per iteration); its dp > 1 plans
+    pay a 100 s load.  Model 1 has the same requests and scales linearly with dp (125
+    requests per replica at dp 8: 6 iterations), tp 1 only.  8 planned GPUs.  Per-layer weights
+    c = 10^6 >> h s, so stage throughput (FLOPs / time) follows the run times."""
+    sp0 = spec(c=10 ** 6, tp_values=(1, 8))     # FLOPs dominated by the linear layers (c >> h s)
+    sp1 = spec(c=10 ** 6, tp_values=(1,))
+    cf0 = np.zeros((W.N_TP_SLOTS, 3, 2, NB))
+    cf0[0, 0, 1, :] = 1.0
+    cf0[3, 0, 1, :] = 2.0 / 3.0
+    load0 = zero_load()
+    load0[:, 1:] = 100.0
+    nodes = [dict(l_in=[4] * 1000, l_out=[1] * 1000, sp=sp0, cf=cf0, load=load0),
+             dict(l_in=[4] * 1000, l_out=[1] * 1000, sp=sp1, cf="const")]
+    return multi(nodes, eng=engine(n_gpus=8, max_num_seqs=21))
