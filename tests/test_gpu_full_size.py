@@ -1,0 +1,200 @@
+"""GPU parity, round 2: exhaustive full-size checks at the bench configuration, the carried-state
+hand traces through the C ABI, summaries against the oracle's, and a cuRAND cross-check of K1.
+
+P:<line> = PAPER.md, S:<line> = SPEC.md.  Every test needs a B200 (-m gpu).
+"""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle as O
+import samu_workloads as W
+from tests import fixtures as F
+
+pytestmark = pytest.mark.gpu
+SEED = W.SAMPLING_SEED
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+N_THREADS = os.cpu_count() or 8
+
+
+def gpu(w):
+    from paper_2503_16893_b200 import Samu
+    S = Samu(0)
+    S.load_workload(w)
+    return S
+
+
+def u16(t):
+    return t.cpu().numpy().view(np.uint16)
+
+
+def recs(out):
+    from paper_2503_16893_b200 import recs_to_numpy
+    return recs_to_numpy(out["recs"])
+
+
+def assert_rec_equal(g, o, ctx=""):
+    for f in ("t_end", "flops_lo", "flops_hi", "req_iters", "iters", "flags"):
+        bad = np.nonzero(np.ravel(g[f] != o[f]))[0]
+        assert bad.size == 0, f"{ctx}: field {f} differs at {bad[:8]} of {np.size(g[f])}"
+
+
+def ready_cands(S, w):
+    ready = [v for v in range(w.n_nodes) if not np.any((w.pred[w.node == v] >= 0) &
+                                                      (w.node[np.maximum(w.pred[w.node == v], 0)] != v))]
+    return [(v, dp, tp) for v in ready for (dp, tp) in S.samu_enumerate_plans(v)]
+
+
+# ------------------------------------------------------------------------------------------
+# full size C5 (BASELINE configs[4], the bench workload): every sampled length, every record
+# ------------------------------------------------------------------------------------------
+@pytest.fixture(scope="module")
+def c5_full():
+    """Oracle side of the bench step, computed once: all 1024 x 50,000 sampled lengths and all
+    165 x 1024 (candidate, trial) records of the first greedy inner step (~2 min of oracle time
+    on the box's host cores)."""
+    w = W.make_workload("c5")
+    P = O.Problem(w)
+    lo, li = P.sample(SEED, 0, w.n_trials)
+    S = gpu(w)
+    cands = ready_cands(S, w)
+    orec = P.simulate_many(cands, lo, li, N_THREADS)
+    return w, S, cands, lo, li, orec
+
+
+def test_full_size_c5_all_sampled_lengths(c5_full):
+    w, S, cands, lo, li, _ = c5_full
+    glo, gli = S.samu_sample_lengths(SEED, 0, w.n_trials)
+    assert np.array_equal(u16(glo), lo) and np.array_equal(u16(gli), li)     # 2 x 51.2M values
+
+
+@pytest.mark.parametrize("T", [1024, 128])
+def test_full_size_c5_every_record(c5_full, T):
+    """T = 1024: the N = 1 bench step; T = 128: one rank's share at 8 GPUs (its LEAN launch
+    runs concurrently with the FRESH one).  Every (candidate, trial) record, bit for bit."""
+    w, S, cands, lo, li, orec = c5_full
+    glo, gli = S.samu_sample_lengths(SEED, 0, T)
+    g = recs(S.samu_simulate_batch(cands, glo, gli))
+    assert g.shape == (len(cands), T)
+    assert_rec_equal(g, orec[:, :T], f"C5 full size, T = {T}")
+
+
+def test_full_size_c5_summaries(c5_full):
+    w, S, cands, lo, li, orec = c5_full
+    glo, gli = S.samu_sample_lengths(SEED, 0, w.n_trials)
+    out = S.samu_simulate_batch(cands, glo, gli, summary=True)
+    osum = O.summarise(orec)
+    for f in ("mean_t", "p50_t", "p90_t", "p99_t", "mean_flops", "mean_req_iters"):
+        assert np.array_equal(np.array([s[f] for s in out["summary"]]), osum[f]), f
+
+
+@pytest.mark.parametrize("name,kw", [("c2", {}), ("c3", {}), ("c4", {})])
+def test_full_size_c2_c4_every_record(name, kw):
+    """BASELINE configs[1..3] at full size and 64 trials: every record of the first inner step."""
+    w = W.make_workload(name, **kw)
+    P = O.Problem(w)
+    S = gpu(w)
+    cands = ready_cands(S, w)
+    lo, li = P.sample(SEED, 0, w.n_trials)
+    glo, gli = S.samu_sample_lengths(SEED, 0, w.n_trials)
+    assert np.array_equal(u16(glo), lo) and np.array_equal(u16(gli), li)
+    g = recs(S.samu_simulate_batch(cands, glo, gli))
+    assert_rec_equal(g, P.simulate_many(cands, lo, li, N_THREADS), name)
+
+
+# ------------------------------------------------------------------------------------------
+# carried state cut mid-decode, then reloaded / resumed (reading c18): hand traces
+# ------------------------------------------------------------------------------------------
+def _state_np(s):
+    return dict(st=s["st"].cpu().numpy().view(np.uint32), g=s["g"].cpu().numpy().view(np.uint16),
+                fin_t=s["fin_t"].cpu().numpy(), over=s["over"].cpu().numpy())
+
+
+@pytest.mark.parametrize("kind,tau,reload_t", [("const", 5.5, 14.0), ("B", 10.5, 16.0)])
+def test_reload_and_resume_hand_traces_on_gpu(kind, tau, reload_t):
+    # the traces of tests/test_oracle_state_pins.py, through libsamu
+    w = F.reload_fixture(kind)
+    S = gpu(w)
+    glo, gli = S.samu_sample_lengths(SEED, 0, 1)
+    for resume in (0, 1):
+        st = S.fresh_state(1)
+        r1 = recs(S.samu_simulate_batch([(0, 1, 1, 0, -1, 1)], glo, gli, state=st, time_limit=np.array([[tau]])))
+        assert r1["iters"][0, 0] == 6 and r1["flags"][0, 0] == 2
+        s = _state_np(st)
+        assert s["g"][0].tolist() == [6, 5, 0] and s["over"][0, 0, 0] == 0.5
+        assert [x >> 28 for x in s["st"][0]] == [O.ST_RUNNING, O.ST_PREEMPTED, O.ST_FRESH]
+        plan = (0, 1, 1, 1, -1, 1) if resume else (0, 1, 2, 0, -1, 1)
+        out = S.samu_simulate_batch([plan], glo, gli, state=st, want_fin_iter=True)
+        r2 = recs(out)
+        fi = out["fin_iter"].cpu().numpy().view(np.uint32)[0, 0]
+        if resume:
+            if kind == "const":
+                assert r2["t_end"][0, 0] == 4.5
+            assert r2["iters"][0, 0] == 4 and fi.tolist() == [0, 3, 2]
+        else:
+            assert r2["t_end"][0, 0] == reload_t and r2["iters"][0, 0] == 4 and r2["req_iters"][0, 0] == 6
+            assert fi.tolist() == [0, 3, 2]
+        assert np.all(_state_np(st)["st"][0] >> 28 == O.ST_DONE)
+
+
+# ------------------------------------------------------------------------------------------
+# summaries: GPU K3 against the oracle's or_summarise on the same records
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("T", [1, 2, 37, 100, 1000])
+def test_summaries_match_oracle(T):
+    w = W.make_workload("c2", n_prompts=60, n_trials=T)
+    S = gpu(w)
+    glo, gli = S.samu_sample_lengths(SEED, 0, T)
+    out = S.samu_simulate_batch([(0, 1, 1), (5, 2, 4), (3, 8, 1)], glo, gli, summary=True)
+    osum = O.summarise(recs(out))
+    for f in ("mean_t", "p50_t", "p90_t", "p99_t", "mean_flops", "mean_req_iters"):
+        assert np.array_equal(np.array([s[f] for s in out["summary"]]), osum[f]), f
+
+
+# ------------------------------------------------------------------------------------------
+# K1 against cuRAND's Philox4x32-10 (NVIDIA's implementation of the same generator, reading c1)
+# ------------------------------------------------------------------------------------------
+@pytest.fixture(scope="module")
+def curand_lib(tmp_path_factory):
+    so = tmp_path_factory.mktemp("curand") / "libcurand_check.so"
+    subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O2",
+                           "-Xcompiler", "-fPIC", "-shared", "-o", str(so),
+                           os.path.join(ROOT, "tests", "native", "curand_philox_check.cu")])
+    return ctypes.CDLL(str(so))
+
+
+@pytest.mark.parametrize("name,kw", [("c2", dict(n_prompts=500)), ("c5", {})])
+def test_sampler_matches_curand_philox(curand_lib, name, kw):
+    """u = word (r & 3) of Philox4x32-10(ctr = (r >> 2, trial, node, 0), key = (seed lo, hi)) from
+    cuRAND, then X = the floor(u n / 2^32)-th element of the eCDF's sorted multiset and
+    l_out = min(X, y, l_max - l_in) (reading c2), for every root request."""
+    T = 3
+    w = W.make_workload(name, n_trials=T, **kw)
+    S = gpu(w)
+    glo, gli = S.samu_sample_lengths(SEED, 0, T)
+    lo_g, li_g = u16(glo), u16(gli)
+    roots = np.nonzero(w.pred < 0)[0].astype(np.uint32)
+    for k in range(T):
+        ctr = np.zeros((roots.size, 4), np.uint32)
+        ctr[:, 0] = roots >> 2
+        ctr[:, 1] = k
+        ctr[:, 2] = w.node[roots]
+        words = np.zeros((roots.size, 4), np.uint32)
+        rc = curand_lib.curand_philox_words(ctr.ctypes.data_as(ctypes.c_void_p), SEED & 0xFFFFFFFF, SEED >> 32,
+                                            words.ctypes.data_as(ctypes.c_void_p), roots.size)
+        assert rc == 0
+        u = words[np.arange(roots.size), roots & 3].astype(np.uint64)
+        for v in range(w.n_nodes):
+            m = int(w.node_model[v])
+            multiset = np.repeat(w.ecdf_values[m], np.diff(np.r_[0, w.ecdf_cum[m]]))
+            n = multiset.size
+            sel = w.node[roots] == v
+            X = multiset[(u[sel] * np.uint64(n)) >> np.uint64(32)].astype(np.int64)
+            r = roots[sel]
+            l_max = w.models[m]["l_max"]
+            expect = np.minimum(np.minimum(X, w.cap_y[r].astype(np.int64)), l_max - w.l_in_base[r].astype(np.int64))
+            assert np.array_equal(lo_g[k, r].astype(np.int64), expect), (name, k, v)
+            assert np.array_equal(li_g[k, r], w.l_in_base[r])
