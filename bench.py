@@ -182,6 +182,9 @@ def main():
     ap.add_argument("--trials", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--per-config", default="c2,c3,c4",
+                    help="other BASELINE configs measured in the same run (value, ms_per_step, roofline, "
+                         "cpu_baseline per config); '' = off")
     ap.add_argument("--planner-trials", type=int, default=-1,
                     help="also time one full Algorithm 1 run (samu_plan_greedy, rows a1-a12) at this trial count "
                          "(default: the workload's trials; 0 = off)")
@@ -208,6 +211,61 @@ def main():
     else:
         nccl_id = None
     S = Samu(local, rank, world, nccl_id)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=torch.device("cuda", local))
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    def sum_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=torch.device("cuda", local))
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return t.item()
+
+    def measure_config(wc, steps, warmup):
+        """The bench step on another workload: sample + simulate the first greedy step's candidates
+        over the rank's trial share + summaries; device time (CUDA events), max over ranks."""
+        S.load_workload(wc)
+        Tc = wc.n_trials
+        tbc, Tlc = trial_share(Tc, world, rank)
+        rdy = [v for v in range(wc.n_nodes) if not np.any((wc.pred[wc.node == v] >= 0) &
+                                                          (wc.node[np.maximum(wc.pred[wc.node == v], 0)] != v))]
+        cc = first_step_candidates(rdy, S.samu_enumerate_plans)
+        dv = torch.device("cuda", local)
+        lo_c = torch.empty((Tlc, wc.n_req), dtype=torch.int16, device=dv)
+        li_c = torch.empty((Tlc, wc.n_req), dtype=torch.int16, device=dv)
+        rc = torch.empty((len(cc), Tlc, 40), dtype=torch.uint8, device=dv)
+
+        def st():
+            S.samu_sample_lengths(wc.seed, tbc, Tlc, out=(lo_c, li_c))
+            return S.samu_simulate_batch(cc, lo_c, li_c, summary=True, out_recs=rc)
+
+        for _ in range(max(3, warmup)):
+            st()
+        barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(steps):
+            st()
+        a1.record()
+        barrier()
+        msc = max_over_ranks(a0.elapsed_time(a1) / steps)
+        gc = recs_to_numpy(rc)
+        it_c = sum_over_ranks(float(gc["iters"].astype(np.float64).sum()))
+        ri_c = sum_over_ranks(float(gc["req_iters"].astype(np.float64).sum()))
+        return dict(workload=wc.name, trials=Tc, candidates=len(cc), requests=wc.n_req, ms_per_step=msc,
+                    value=len(cc) * Tc / (msc / 1e3), unit="candidate-trials/s", sim_iters=it_c, req_iters=ri_c,
+                    cands=cc)
+
     S.load_workload(w)
     T = w.n_trials
     tb, Tl = trial_share(T, world, rank)
@@ -223,11 +281,6 @@ def main():
     def step():
         S.samu_sample_lengths(w.seed, tb, Tl, out=(lo, li))
         return S.samu_simulate_batch(cands, lo, li, summary=True, out_recs=recs)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -301,6 +354,12 @@ def main():
                    "candidate_trial_sims": plan["n_sims"], "candidate_trial_sims_per_s": plan["n_sims"] / plan_s,
                    "planned_total_s": plan["total"]}
 
+    # the other BASELINE configs (C2 ensembling, C3 routing, C4 chain summary; 64 trials each), same
+    # step, measured after the headline region (north star: throughput per paper-shaped workload)
+    per_config = []
+    for name in [x for x in args.per_config.split(",") if x and x != w.name]:
+        per_config.append(measure_config(W.make_workload(name), max(3, args.steps), max(3, args.warmup)))
+
     if rank == 0:
         pk = peaks()
         clock = clk.summary()
@@ -309,6 +368,10 @@ def main():
         iters_per_launch = iters / world          # per rank launch (strong scaling: each rank its share)
         achieved = FP64_FLOPS_PER_ITER * iters_per_launch / (k2_ms / 1e3)
         value = nc * T / (ms / 1e3)
+        ncu = ncu_summary(w.name)
+        hbm_peak = pk.get("hbm_gbs", 6454.0) * 1e9
+        dram = ncu.get("dram_bytes_per_launch")
+        ncu_ms = ncu.get("gpu_time_ms")
         line = {
             "metric": "simulated candidate-trials/s", "value": value, "unit": "candidate-trials/s",
             "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
@@ -324,10 +387,19 @@ def main():
                          "traffic": ncu_summary(w.name).get("dram_bytes_per_launch"),
                          # context (from the committed ncu capture, not this run): the resource
                          # that binds K2 is the warp-instruction issue rate, not fp64 or HBM
-                         "ncu_issue_slots_active_pct": ncu_summary(w.name).get("issue_active_pct"),
-                         "ncu_fp64_pipe_pct": ncu_summary(w.name).get("fp64_pipe_pct"),
+                         "ncu_issue_slots_active_pct": ncu.get("issue_active_pct"),
+                         "ncu_fp64_pipe_pct": ncu.get("fp64_pipe_pct"),
+                         "ncu_warps_active_pct": ncu.get("warps_active_pct"),
+                         # HBM side (BASELINE's "HBM roofline %"): measured DRAM bytes of K2 (ncu, per
+                         # launch set) over this run's K2 time, against the measured copy bandwidth
+                         "hbm_gbs": (dram / (k2_ms / 1e3) / 1e9) if dram else None,
+                         "hbm_frac": (dram / (k2_ms / 1e3) / hbm_peak) if dram else None,
+                         "hbm_peak_gbs": hbm_peak / 1e9, "hbm_peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                         "ncu_gpu_time_ms": ncu_ms,
                          "ncu_source": "profiles/ncu_k2_summary.json",
-                         "peak_source": "fp64: 148 SM x 64 FMA lanes x 2 x sm clock (derived, DESIGN.md section 6)",
+                         "peak_derived": True,
+                         "peak_source": "fp64: 148 SM x 64 FMA lanes x 2 x sm clock (derived from unit counts and the "
+                                        "measured max clock; MEASURED_PEAKS.json has no fp64 entry; DESIGN.md section 6)",
                          "work_per_unit": "9 fp64 flops per simulated iteration (latency model, reading c24)",
                          "sim_iters_per_launch": iters_per_launch, "k2_ms_per_launch": k2_ms},
             "e2e": {"value": nc * T / e2e_s, "unit": "candidate-trials/s", "h2d_bytes_per_step": int(h2d),
@@ -336,9 +408,23 @@ def main():
         }
         if planner:
             line["planner"] = planner
-        if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = {k: v for k, v in time_oracle(w, cands, args.cpu_seconds).items()
-                                    if k in ("value", "unit", "cores", "kind", "sample", "req_iters_per_s")}
+        keep = ("value", "unit", "cores", "kind", "sample", "req_iters_per_s")
+        if not args.no_cpu_baseline:   # rank 0 at every world size (the other ranks wait)
+            line["cpu_baseline"] = {k: v for k, v in time_oracle(w, cands, args.cpu_seconds).items() if k in keep}
+        if per_config:
+            line["per_config"] = []
+            for pc in per_config:
+                wc = W.make_workload(pc["workload"])
+                k_ach = FP64_FLOPS_PER_ITER * (pc["sim_iters"] / world) / (pc["ms_per_step"] / 1e3)
+                d = {k: pc[k] for k in ("workload", "trials", "candidates", "requests", "value", "unit", "ms_per_step")}
+                d["req_iters_per_s"] = pc["req_iters"] / (pc["ms_per_step"] / 1e3)
+                d["roofline"] = {"bound": "alu", "achieved": k_ach / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
+                                 "frac": k_ach / peak, "peak_derived": True,
+                                 "note": "whole step time (K1 + K2 + K3) as the launch duration"}
+                if not args.no_cpu_baseline:
+                    d["cpu_baseline"] = {k: v for k, v in time_oracle(wc, pc["cands"], args.cpu_seconds / 3).items()
+                                         if k in keep}
+                line["per_config"].append(d)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -153,6 +153,11 @@ samu_status samu_ctx_create_local(samu_ctx** out, int32_t cuda_device, void* cud
 const char* samu_last_error(const samu_ctx* ctx);
 /* Number of CUDA kernels this context has launched so far (instrumentation). */
 uint64_t samu_launch_count(const samu_ctx* ctx);
+/* Schedule-sharing counters of this context since creation (instrumentation): out[0] shared-
+ * schedule work items (a (node, dp) group's head replica-sim carrying up to 3 tp variants),
+ * out[1] member items those carried, out[2] member items that fell out of sync (KV blocks bound
+ * below the head's count, or a preemption) and were re-simulated on their own. */
+void samu_share_stats(const samu_ctx* ctx, int64_t out[3]);
 samu_status samu_nccl_unique_id(uint8_t out[128]);
 
 /* Register model `model_id` (0..63): spec, per-B coefficient buckets and the loading table.

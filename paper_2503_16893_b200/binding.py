@@ -86,7 +86,7 @@ class samu_plan_opts(C.Structure):
 ALGOS = {"greedy": 0, "max": 1, "min": 2}
 
 EXPORTED = ["samu_ctx_create", "samu_ctx_destroy", "samu_local_group_create", "samu_local_group_destroy",
-            "samu_ctx_create_local", "samu_last_error", "samu_launch_count", "samu_nccl_unique_id",
+            "samu_ctx_create_local", "samu_last_error", "samu_launch_count", "samu_share_stats", "samu_nccl_unique_id",
             "samu_model_register",
             "samu_ecdf_load", "samu_app_load", "samu_enumerate_plans", "samu_sample_lengths", "samu_simulate_batch",
             "samu_plan_greedy", "samu_plan_max_heuristic", "samu_plan_min_heuristic", "samu_plan_run", "samu_known_lengths",
@@ -115,6 +115,8 @@ def lib():
         L.samu_nccl_unique_id.argtypes = [P]
         L.samu_launch_count.argtypes = [P]
         L.samu_launch_count.restype = C.c_uint64
+        L.samu_share_stats.argtypes = [P, P]
+        L.samu_share_stats.restype = None
         L.samu_model_register.argtypes = [P, C.c_int32, C.POINTER(samu_model_spec), C.c_int32, P, P, P]
         L.samu_ecdf_load.argtypes = [P, C.c_int32, P, P, C.c_int32]
         L.samu_app_load.argtypes = [P, C.POINTER(samu_engine_cfg), C.c_int32, P, C.c_int32, P]
@@ -218,6 +220,11 @@ class Samu:
 
     def samu_launch_count(self) -> int:
         return int(lib().samu_launch_count(self.h))
+
+    def samu_share_stats(self) -> Dict[str, int]:
+        out = (C.c_int64 * 3)()
+        lib().samu_share_stats(self.h, out)
+        return dict(group_items=int(out[0]), member_items=int(out[1]), fallbacks=int(out[2]))
 
     # ---- registration -------------------------------------------------------------------
     def samu_model_register(self, model_id: int, spec: Dict, bucket_B, coeff, load):

@@ -6,6 +6,7 @@
 #include "samu_internal.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 #include <math_constants.h>
 
@@ -56,7 +57,7 @@ __global__ void k_combine(const samu_trial_rec* __restrict__ rep, const DevCand*
 }
 
 // per-candidate summary over T trials: sequential mean, nearest-rank percentiles via an
-// in-shared-memory bitonic sort (T <= 8192)
+// in-shared-memory bitonic sort (T <= 8192; more trials: k_summary_select)
 __global__ void k_summary(const samu_trial_rec* __restrict__ recs, int32_t T, samu_cand_summary* __restrict__ out) {
   extern __shared__ double sv[];
   const int32_t c = blockIdx.x;
@@ -92,6 +93,76 @@ __global__ void k_summary(const samu_trial_rec* __restrict__ recs, int32_t T, sa
     o.p50_t = pct(50);
     o.p90_t = pct(90);
     o.p99_t = pct(99);
+    o.mean_flops = __ddiv_rn(u128_to_double(hi, lo), (double)T);
+    o.mean_req_iters = __ddiv_rn(__ull2double_rn(ri), (double)T);
+    out[c] = o;
+  }
+}
+
+// T > 8192 trials: the same summary, the nearest-rank order statistics found by an MSB radix
+// select over the order-preserving 64-bit keys of t_end (8 passes of 8 bits per percentile, a
+// 256-bin shared histogram), so any trial count fits
+__device__ __forceinline__ uint64_t order_key(double x) {
+  const uint64_t b = (uint64_t)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double key_double(uint64_t k) {
+  const uint64_t b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+
+__global__ void k_summary_select(const samu_trial_rec* __restrict__ recs, int32_t T, samu_cand_summary* __restrict__ out) {
+  __shared__ uint32_t hist[256];
+  __shared__ uint64_t s_prefix;
+  __shared__ uint32_t s_rank;
+  const int32_t c = blockIdx.x;
+  const samu_trial_rec* r = recs + (size_t)c * T;
+  double pv[3];
+  const int32_t pcts[3] = {50, 90, 99};
+  for (int q = 0; q < 3; ++q) {
+    const int64_t nr = ((int64_t)pcts[q] * T + 99) / 100;     // nearest rank, 1-based
+    uint32_t rank = (uint32_t)(nr > 0 ? nr - 1 : 0);
+    uint64_t prefix = 0;
+    for (int pass = 0; pass < 8; ++pass) {
+      const int sh = 56 - 8 * pass;
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+      __syncthreads();
+      for (int32_t k = threadIdx.x; k < T; k += blockDim.x) {
+        const uint64_t key = order_key(r[k].t_end);
+        if (pass == 0 || (key >> (sh + 8)) == (prefix >> (sh + 8))) atomicAdd(&hist[(key >> sh) & 255u], 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+        int b = 0;
+        for (; b < 255; ++b) {
+          if (acc + hist[b] > rank) break;
+          acc += hist[b];
+        }
+        s_rank = rank - acc;
+        s_prefix = prefix | ((uint64_t)b << sh);
+      }
+      __syncthreads();
+      prefix = s_prefix;
+      rank = s_rank;
+      __syncthreads();
+    }
+    pv[q] = key_double(prefix);
+  }
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    uint64_t hi = 0, lo = 0;
+    uint64_t ri = 0;
+    for (int32_t k = 0; k < T; ++k) {
+      s = __dadd_rn(s, r[k].t_end);
+      add128(hi, lo, r[k].flops_hi, r[k].flops_lo);
+      ri += r[k].req_iters;
+    }
+    samu_cand_summary o;
+    o.mean_t = __ddiv_rn(s, (double)T);
+    o.p50_t = pv[0];
+    o.p90_t = pv[1];
+    o.p99_t = pv[2];
     o.mean_flops = __ddiv_rn(u128_to_double(hi, lo), (double)T);
     o.mean_req_iters = __ddiv_rn(__ull2double_rn(ri), (double)T);
     out[c] = o;
@@ -190,7 +261,34 @@ __global__ void k_stage_score(const samu_trial_rec* __restrict__ cache, int32_t 
   }
 }
 
+// all-gathered record blocks [world][n][Tmax] -> rows slots[x] of dst [*][T], trial order.  Rank w
+// holds trial block w % Wt (contiguous split of T over Wt blocks) of the jobs of class w / Wt.
+__global__ void k_unpack_gather(const samu_trial_rec* __restrict__ recv, int32_t world, int32_t n, int32_t Tmax,
+                                int32_t T, int32_t Wt, const int32_t* __restrict__ slots,
+                                const int32_t* __restrict__ job_class, samu_trial_rec* __restrict__ dst) {
+  const int64_t total = (int64_t)world * n * Tmax;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t k = (int32_t)(i % Tmax);
+    const int32_t x = (int32_t)((i / Tmax) % n);
+    const int32_t w = (int32_t)(i / ((int64_t)n * Tmax));
+    if (job_class[x] != w / Wt) continue;
+    const int32_t blk = w % Wt, base = T / Wt, rem = T % Wt;
+    const int32_t cnt = base + (blk < rem ? 1 : 0), b0 = blk * base + min(blk, rem);
+    if (k < cnt) dst[(size_t)slots[x] * T + b0 + k] = recv[i];
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_unpack_gather(const samu_trial_rec* recv, int32_t world, int32_t n, int32_t Tmax, int32_t T,
+                                 int32_t Wt, const int32_t* slots, const int32_t* job_class, samu_trial_rec* dst,
+                                 cudaStream_t s) {
+  const int64_t total = (int64_t)world * n * Tmax;
+  if (total <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 8);
+  k_unpack_gather<<<(unsigned)blocks, 256, 0, s>>>(recv, world, n, Tmax, T, Wt, slots, job_class, dst);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_combine(const samu_trial_rec* rep_rec, const DevCand* cands, int32_t n_cands, int32_t n_trials,
                            double* over, int32_t n_nodes, cudaStream_t s) {
@@ -202,9 +300,13 @@ cudaError_t launch_combine(const samu_trial_rec* rep_rec, const DevCand* cands, 
 
 cudaError_t launch_summary(const samu_trial_rec* recs, int32_t n_cands, int32_t n_trials, samu_cand_summary* out,
                            cudaStream_t s) {
+  if (n_cands <= 0 || n_trials <= 0) return cudaSuccess;
   int32_t P2 = 1;
   while (P2 < n_trials) P2 <<= 1;
-  if (P2 > 8192) return cudaErrorInvalidValue;
+  if (P2 > 8192 || std::getenv("SAMU_SUMMARY_SELECT")) {   // (the env var forces this path in tests)
+    k_summary_select<<<n_cands, 256, 0, s>>>(recs, n_trials, out);
+    return cudaGetLastError();
+  }
   const size_t smem = sizeof(double) * P2;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_summary, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

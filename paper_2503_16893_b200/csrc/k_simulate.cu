@@ -55,6 +55,10 @@ namespace {
 constexpr uint32_t FULL = 0xFFFFFFFFu;
 constexpr int SLOTS = 256;
 
+// K2 modes (DevCand::mode) whose items never hold per-request outputs or successors: the smaller
+// shared block and the LEAN launch bounds
+__host__ __device__ constexpr bool is_lean(int mode) { return mode == 1 || mode == 3 || mode == 5; }
+
 // SMALL (LEAN launches): no finish / release lists, 2 KB less, so 28 warps fit an SM
 template <bool SMALL>
 struct WarpSmT {
@@ -68,6 +72,11 @@ struct WarpSmT {
   uint32_t adm_req[32], adm_meta[32];
   int2 adm_fo[32];
   double cbuf[32];           // per-iteration costs of a decode-run chunk (lane j = iteration j)
+  const double* vcoef[32];   // schedule sharing: lane v's member's dense coefficients and 2 L (h/tp),
+  uint32_t vK1[32];          // candidate index, and the group size
+  uint32_t vci[32];
+  uint32_t nv;
+  int32_t minF;              // minimum free KV blocks so far (INT_MIN once a preemption happened)
   // warp-uniform state off the hot path (kept out of registers); every lane writes the same
   // value and reads back its own write, so no synchronisation is needed
   double tau, next_ready;    // time limit, ready time of the next pending cross-node arrival
@@ -194,6 +203,142 @@ __device__ const uint64_t* warp_radix_sort(uint64_t* ka, uint32_t* ia, uint64_t*
   return ka;
 }
 
+// Decode-run latency sums in 32-iteration chunks (64 in the FRESH modes), evaluated in parallel
+// and bit-identically to the sequential adds (see the exact binade form below; c23, c24): lane j
+// evaluates iteration done_it + j (the x of every iteration are exact integers, so their
+// conversions equal the sequential increments).  t = clock (updated), coef / K1 = the member's
+// dense coefficients and 2 L (h/tp); B, K0 = L c B, S0, smax0 = the run's first S and s.
+// Returns the iterations done (m_run, or fewer when t reached stop_t).
+template <int MODE>
+__device__ __forceinline__ uint32_t run_chunks(double& t, const double* __restrict__ coef, const uint32_t K1,
+                                               const uint32_t B, const uint64_t K0, const uint32_t S0,
+                                               const uint32_t smax0, const uint32_t m_run, const double stop_t,
+                                               const int lane, double* cbuf) {
+  // modes 1 / 2: no time limit and no arrivals, stop_t = +inf; in the exact-sum chunks a
+  // partial sum that is not below it is not below 2^(e+1) either (already a fallback)
+  constexpr bool NOSTOP = MODE == 1 || MODE == 2 || MODE == 5 || MODE == 6;
+  const double2* cb = reinterpret_cast<const double2*>(coef + (size_t)(B - 1) * 8);
+  const double2 cc = __ldg(cb), cp = __ldg(cb + 1), cs = __ldg(cb + 2);
+  const double ac = cc.x, bc = cc.y, ap = cp.x, bp = cp.y, as_ = cs.x, bs_ = cs.y;
+  uint32_t done_it = 0;
+    bool stopped = false;
+    // FRESH (chain summariser: long runs of small B): 64 iterations per scan (lane j:
+    // iterations 2j and 2j + 1), the same exact binade form (only in that instantiation:
+    // elsewhere the extra live values cost more than the saved scans)
+    while ((MODE == 2 || MODE == 4 || MODE == 6) && !stopped && m_run - done_it >= 64u) {
+      const uint64_t eb = (uint64_t)__double_as_longlong(t) & 0x7FF0000000000000ull;
+      if (!(t > 0.0 && eb >= (64ull << 52) && eb < (0x7F0ull << 52))) break;
+      const uint32_t ja = done_it + 2u * (uint32_t)lane;
+      const uint32_t Sa = S0 + B * ja, Sb = Sa + B;
+      const double c0 = __dadd_rn(__dadd_rn(__fma_rn(ac, __ull2double_rn(K0 + (uint64_t)K1 * Sa), bc),
+                                            __fma_rn(ap, __uint2double_rn(B * (smax0 + ja)), bp)),
+                                  __fma_rn(as_, __uint2double_rn(Sa), bs_));
+      const double c1 = __dadd_rn(__dadd_rn(__fma_rn(ac, __ull2double_rn(K0 + (uint64_t)K1 * Sb), bc),
+                                            __fma_rn(ap, __uint2double_rn(B * (smax0 + ja + 1u)), bp)),
+                                  __fma_rn(as_, __uint2double_rn(Sb), bs_));
+      const double r0 = __dsub_rn(__dadd_rn(t, c0), t), r1 = __dsub_rn(__dadd_rn(t, c1), t);
+      const double e0 = __dsub_rn(c0, r0), e1 = __dsub_rn(c1, r1);
+      const double halfu = __longlong_as_double((long long)(eb - (53ull << 52)));
+      const double top = __longlong_as_double((long long)(eb + (1ull << 52)));
+      const double rp = __dadd_rn(r0, r1);
+      double psum = rp;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double nb2 = __shfl_up_sync(FULL, psum, o);
+        if (lane >= o) psum = __dadd_rn(psum, nb2);
+      }
+      const double acc_b = __dadd_rn(t, psum);                              // after 2j + 1
+      const double acc_a = __dadd_rn(t, __dadd_rn(__dsub_rn(psum, rp), r0));   // after 2j
+      const bool stop_a = !NOSTOP && !(acc_a < stop_t);
+      const uint32_t bstop = NOSTOP ? 0u : __ballot_sync(FULL, stop_a || !(acc_b < stop_t));
+      const uint32_t L = bstop ? (uint32_t)(__ffs(bstop) - 1) : 31u;
+      const bool chk_b = (uint32_t)lane < L || ((uint32_t)lane == L && !stop_a);
+      const bool bad = (uint32_t)lane <= L &&
+                       (c0 < 0.0 || fabs(e0) == halfu || !(acc_a < top) ||
+                        (chk_b && (c1 < 0.0 || fabs(e1) == halfu || !(acc_b < top))));
+      if (__any_sync(FULL, bad)) break;   // the 32-iteration chunks below take over
+      if (bstop) {
+        const bool sa = __shfl_sync(FULL, stop_a, L);
+        t = sa ? __shfl_sync(FULL, acc_a, L) : __shfl_sync(FULL, acc_b, L);
+        done_it += 2u * L + (sa ? 1u : 2u);
+        stopped = true;
+      } else {
+        t = __shfl_sync(FULL, acc_b, 31);
+        done_it += 64u;
+      }
+    }
+    while (done_it < m_run && !stopped) {
+      const uint32_t cnt = min(32u, m_run - done_it);
+      double cj = 0.0;
+      if ((uint32_t)lane < cnt) {
+        // S_j and B (s + j) stay below 256 * l_max < 2^24 (kernel limits)
+        const uint32_t jj = done_it + (uint32_t)lane;
+        const uint32_t S_j = S0 + B * jj;
+        const double xc = __ull2double_rn(K0 + (uint64_t)K1 * S_j);
+        const double xp = __uint2double_rn(B * (smax0 + jj));
+        const double xs = __uint2double_rn(S_j);
+        cj = __dadd_rn(__dadd_rn(__fma_rn(ac, xc, bc), __fma_rn(ap, xp, bp)), __fma_rn(as_, xs, bs_));
+      }
+      // Exact parallel form of the sequential sum (same doubles as the one-by-one adds):
+      // while every partial sum stays in t's binade [2^e, 2^(e+1)) (ulp u), each add
+      // RN(acc + c) = acc + round_u(c), where round_u(c) = RN(t + c) - t (exact), unless c
+      // sits exactly half-way between multiples of u (a tie, whose even-rounding depends
+      // on acc): the partial sums are then t + prefix sums of the round_u(c), all
+      // multiples of u below 2^(e+1), hence exact in any order (a warp scan).  Chunks with
+      // a negative cost, a tie or a binade crossing take the sequential walk below.
+      {
+        const uint64_t eb = (uint64_t)__double_as_longlong(t) & 0x7FF0000000000000ull;
+        const bool tok = t > 0.0 && eb >= (64ull << 52) && eb < (0x7F0ull << 52);
+        if (tok) {
+          const double s = __dadd_rn(t, cj);
+          const double r = __dsub_rn(s, t);
+          const double err = __dsub_rn(cj, r);   // exact (Fast2Sum, t >= c when in binade)
+          const double halfu = __longlong_as_double((long long)(eb - (53ull << 52)));
+          const double top = __longlong_as_double((long long)(eb + (1ull << 52)));   // 2^(e+1)
+          double psum = r;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const double nb2 = __shfl_up_sync(FULL, psum, o);
+            if (lane >= o) psum = __dadd_rn(psum, nb2);
+          }
+          const double acc_j = __dadd_rn(t, psum);   // partial sum after iteration lane
+          const bool in = (uint32_t)lane < cnt;
+          const uint32_t bstop = NOSTOP ? 0u : __ballot_sync(FULL, in && !(acc_j < stop_t));
+          const uint32_t upto = bstop ? (uint32_t)(__ffs(bstop) - 1) : cnt - 1;   // last lane used
+          const bool bad = (uint32_t)lane <= upto && (cj < 0.0 || fabs(err) == halfu || !(acc_j < top));
+          if (!__any_sync(FULL, bad)) {
+            t = __shfl_sync(FULL, acc_j, upto);
+            done_it += upto + 1;
+            stopped = bstop != 0;
+            continue;
+          }
+        }
+      }
+      cbuf[lane] = cj;
+      const bool mono = __all_sync(FULL, !(cj < 0.0));
+      __syncwarp();
+      double acc = t;
+#pragma unroll 8
+      for (uint32_t q2 = 0; q2 < cnt; ++q2) acc = __dadd_rn(acc, cbuf[q2]);
+      if (mono && acc < stop_t) {
+        t = acc;
+        done_it += cnt;
+      } else {   // the chunk reaches stop_t (or costs are not monotone): step and check
+        acc = t;
+        uint32_t q2 = 0;
+        do {
+          acc = __dadd_rn(acc, cbuf[q2]);
+          ++q2;
+        } while (q2 < cnt && acc < stop_t);
+        t = acc;
+        done_it += q2;
+        stopped = acc >= stop_t;
+      }
+      __syncwarp();
+    }
+  return done_it;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------------------------
@@ -211,20 +356,14 @@ __constant__ DevCand c_cands[SAMU_K2_CONST_CANDS];
 // ensembling / routing nodes) — the queue is then the replica's request list itself.  Fewer live
 // registers: ~10 % faster on those items.
 template <int BSK, bool CONSTC, int MODE>
-__device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1 || MODE == 3>& W, const int lane, uint32_t* q, uint64_t* pkey,
-                                         uint32_t* pidx, const uint32_t item) {
-  constexpr bool LEAN = MODE == 1 || MODE == 3, FRESH = MODE != 0, CUT = MODE == 3 || MODE == 4;
+__device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MODE)>& W, const int lane, uint32_t* q, uint64_t* pkey,
+                                         uint32_t* pidx, const uint32_t ci, const uint32_t rel, const uint4 grp) {
+  constexpr bool LEAN = is_lean(MODE), FRESH = MODE != 0, CUT = MODE == 3 || MODE == 4;
+  constexpr bool GRP = MODE == 5 || MODE == 6;   // schedule sharing across a (node, dp) group's tp variants
   const DevApp& A = P.app;
   const int n = A.n_req;
-    // decode the item: candidate by binary search over the launch's offsets, then (trial, replica)
-    uint32_t lo_x = 0, hi_x = (uint32_t)P.n_ord;   // off[lo_x] <= item < off[hi_x]
-    while (hi_x - lo_x > 1) {
-      const uint32_t mid = (lo_x + hi_x) >> 1;
-      if (__ldg(P.off + mid) <= item) lo_x = mid; else hi_x = mid;
-    }
-    const uint32_t ci = __ldg(P.ord + lo_x);
     const DevCand& C = CONSTC ? c_cands[ci] : P.cands[ci];
-    const uint32_t rel = item - __ldg(P.off + lo_x), dpc = (uint32_t)C.dp;
+    const uint32_t dpc = (uint32_t)C.dp;
     const uint32_t k = rel / dpc, j = rel - k * dpc;
     const size_t tb = (size_t)k * n;
     // sampled lengths of this trial, indexed with 32-bit offsets from the kernel parameters (the
@@ -251,6 +390,24 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1 |
 
     Sim m;
     m.t = C.resume ? (over ? over[j] : 0.0) : C.load_s;
+    // schedule sharing (GRP): the group is simulated once with the head's KV blocks; lane v
+    // carries the clock (and cost coefficients) of member min(v, nv - 1), every integer of the
+    // schedule is shared.  Member v's schedule equals the head's iff no preemption happened and
+    // the peak block use never exceeded its own count: min F >= blocks_head - blocks_v.
+    if (GRP) {
+      W.minF = C.blocks;
+      uint32_t my_ci = ci;
+      if (grp.x > 1) {
+        const uint32_t v = min((uint32_t)lane, grp.x - 1);
+        my_ci = v == 0 ? ci : v == 1 ? grp.y : v == 2 ? grp.z : grp.w;
+      }
+      const DevCand& Cl = CONSTC ? c_cands[my_ci] : P.cands[my_ci];
+      m.t = Cl.load_s;
+      W.vcoef[lane] = Cl.coef;
+      W.vK1[lane] = (uint32_t)Cl.K1;
+      W.vci[lane] = my_ci;
+      W.nv = grp.x;
+    }
     double tau = (FRESH && !CUT) ? CUDART_INF : C.tau ? C.tau[k] : (C.tau_rec ? C.tau_rec[k].t_end : CUDART_INF);
     m.a1 = m.a2 = m.reqit = 0;
     m.iter = 0; m.d = 0; m.needidx = 0; m.B = 0; m.S = 0; m.next_rank = 0;
@@ -409,6 +566,9 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1 |
     __syncwarp();
     m.stop = fmin(tau, next_ready0);
     const uint32_t K1 = (uint32_t)C.K1;   // 2 L (h/tp) (< 2^32, checked by the host)
+    // this lane's member (GRP: read from the warp's shared block, off the register budget)
+#define K1_l (GRP ? W.vK1[lane] : K1)
+#define coef_l (GRP ? W.vcoef[lane] : C.coef)
     const uint64_t LC = C.LC;   // L c
     const bool need_rel = LEAN ? false : FRESH ? (bool)C.has_succ : (fio || fto || commit || C.has_succ);
     bool cut = false;
@@ -656,13 +816,14 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1 |
           if (mm < 32) break;
         }
         m.F -= blk;
+        if (GRP) W.minF = min(W.minF, m.F);
         K2STAT(2, 1);
         K2STAT(3, k_adm);
         // Eq. prefill FLOPs: L (c B s + 2 B h s^2 / tp)
         // = B s (L c + 2 L (h/tp) s): the same integer, fewer 64-bit products (B s < 2^24)
         const uint32_t Bs32 = k_adm * smaxp;
-        const uint64_t fl = (LC + (uint64_t)K1 * smaxp) * Bs32;
-        const double lat = iter_cost(C.coef, k_adm, fl, Bs32, tok);
+        const uint64_t fl = (LC + (uint64_t)K1_l * smaxp) * Bs32;
+        const double lat = iter_cost(coef_l, k_adm, fl, Bs32, tok);
         m.t = __dadd_rn(m.t, lat);
         m.a1 += Bs32;
         m.a2 += (uint64_t)Bs32 * smaxp;
@@ -686,13 +847,14 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1 |
           // m_run = 1, without its search and closed forms (same arithmetic)
           const uint32_t B1 = m.B;
           const uint32_t smax = (uint32_t)((int32_t)m.d + m.maxO);
-          const uint64_t fl = LC * B1 + (uint64_t)K1 * m.S;
-          m.t = __dadd_rn(m.t, iter_cost(C.coef, B1, fl, B1 * smax, m.S));
+          const uint64_t fl = LC * B1 + (uint64_t)K1_l * m.S;
+          m.t = __dadd_rn(m.t, iter_cost(coef_l, B1, fl, B1 * smax, m.S));
           m.a1 += B1;
           m.a2 += m.S;
           m.reqit += B1;
           m.iter += 1;
           m.F -= (int32_t)need1;
+          if (GRP) W.minF = min(W.minF, m.F);
           m.S += B1;
           m.d += 1;
           m.needidx = m.needidx == 0 ? bs.v() - 1 : m.needidx - 1;
@@ -700,9 +862,6 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1 |
         K2STAT(7, 1);
         const uint32_t B = m.B;
         const double stop_t = m.stop;
-        // modes 1 / 2: no time limit and no arrivals, stop_t = +inf; in the exact-sum chunks a
-        // partial sum that is not below it is not below 2^(e+1) either (already a fallback)
-        constexpr bool NOSTOP = MODE == 1 || MODE == 2;
         // KV need of the run's decodes: histogram rotated to start at needidx, prefix sums
         const uint32_t hv = (uint32_t)lane < bs.v() ? W.hist[bs.mod(m.needidx + bs.v() - (uint32_t)lane)] : 0u;
         const uint32_t m_fin = m.next_fin - m.d;
@@ -731,160 +890,59 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1 |
         if (m_run > 0) {
           const uint64_t K0 = LC * B;
           const uint32_t smax0 = (uint32_t)((int32_t)m.d + m.maxO);
-          const double2* cb = reinterpret_cast<const double2*>(C.coef + (size_t)(B - 1) * 8);
-          const double2 cc = __ldg(cb), cp = __ldg(cb + 1), cs = __ldg(cb + 2);
-          const double ac = cc.x, bc = cc.y, ap = cp.x, bp = cp.y, as_ = cs.x, bs_ = cs.y;
-          double t = m.t;
           if (m_run > SAMU_K2_CHUNK_MIN) {
-            // lane j evaluates iteration done_it + j of a 32-iteration chunk (the x of every
-            // iteration are exact integers, so their conversions equal the sequential
-            // increments), then the chunk's costs are added to t one by one in iteration order
-            // (c23, c24: bit-identical to the sequential loop)
-            bool stopped = false;
-            // FRESH (chain summariser: long runs of small B): 64 iterations per scan (lane j:
-            // iterations 2j and 2j + 1), the same exact binade form (only in that instantiation:
-            // elsewhere the extra live values cost more than the saved scans)
-            while ((MODE == 2 || MODE == 4) && !stopped && m_run - done_it >= 64u) {
-              const uint64_t eb = (uint64_t)__double_as_longlong(t) & 0x7FF0000000000000ull;
-              if (!(t > 0.0 && eb >= (64ull << 52) && eb < (0x7F0ull << 52))) break;
-              const uint32_t ja = done_it + 2u * (uint32_t)lane;
-              const uint32_t Sa = m.S + B * ja, Sb = Sa + B;
-              const double c0 = __dadd_rn(__dadd_rn(__fma_rn(ac, __ull2double_rn(K0 + (uint64_t)K1 * Sa), bc),
-                                                    __fma_rn(ap, __uint2double_rn(B * (smax0 + ja)), bp)),
-                                          __fma_rn(as_, __uint2double_rn(Sa), bs_));
-              const double c1 = __dadd_rn(__dadd_rn(__fma_rn(ac, __ull2double_rn(K0 + (uint64_t)K1 * Sb), bc),
-                                                    __fma_rn(ap, __uint2double_rn(B * (smax0 + ja + 1u)), bp)),
-                                          __fma_rn(as_, __uint2double_rn(Sb), bs_));
-              const double r0 = __dsub_rn(__dadd_rn(t, c0), t), r1 = __dsub_rn(__dadd_rn(t, c1), t);
-              const double e0 = __dsub_rn(c0, r0), e1 = __dsub_rn(c1, r1);
-              const double halfu = __longlong_as_double((long long)(eb - (53ull << 52)));
-              const double top = __longlong_as_double((long long)(eb + (1ull << 52)));
-              const double rp = __dadd_rn(r0, r1);
-              double psum = rp;
-#pragma unroll
-              for (int o = 1; o < 32; o <<= 1) {
-                const double nb2 = __shfl_up_sync(FULL, psum, o);
-                if (lane >= o) psum = __dadd_rn(psum, nb2);
+            if (GRP) {
+              // the chunked exact sums once per group member (lane v keeps member v's clock)
+              const uint32_t nv = W.nv;
+              for (uint32_t v = 0; v < nv; ++v) {
+                const uint32_t civ = W.vci[v];
+                const DevCand& Cv = CONSTC ? c_cands[civ] : P.cands[civ];
+                double tv = __shfl_sync(FULL, m.t, v);
+                done_it = run_chunks<MODE>(tv, Cv.coef, (uint32_t)Cv.K1, B, K0, m.S, smax0, m_run, stop_t, lane, W.cbuf);
+                if ((uint32_t)lane == v) m.t = tv;
               }
-              const double acc_b = __dadd_rn(t, psum);                              // after 2j + 1
-              const double acc_a = __dadd_rn(t, __dadd_rn(__dsub_rn(psum, rp), r0));   // after 2j
-              const bool stop_a = !NOSTOP && !(acc_a < stop_t);
-              const uint32_t bstop = NOSTOP ? 0u : __ballot_sync(FULL, stop_a || !(acc_b < stop_t));
-              const uint32_t L = bstop ? (uint32_t)(__ffs(bstop) - 1) : 31u;
-              const bool chk_b = (uint32_t)lane < L || ((uint32_t)lane == L && !stop_a);
-              const bool bad = (uint32_t)lane <= L &&
-                               (c0 < 0.0 || fabs(e0) == halfu || !(acc_a < top) ||
-                                (chk_b && (c1 < 0.0 || fabs(e1) == halfu || !(acc_b < top))));
-              if (__any_sync(FULL, bad)) break;   // the 32-iteration chunks below take over
-              if (bstop) {
-                const bool sa = __shfl_sync(FULL, stop_a, L);
-                t = sa ? __shfl_sync(FULL, acc_a, L) : __shfl_sync(FULL, acc_b, L);
-                done_it += 2u * L + (sa ? 1u : 2u);
-                stopped = true;
-              } else {
-                t = __shfl_sync(FULL, acc_b, 31);
-                done_it += 64u;
-              }
+            } else {
+              double t = m.t;
+              done_it = run_chunks<MODE>(t, C.coef, K1, B, K0, m.S, smax0, m_run, stop_t, lane, W.cbuf);
+              m.t = t;
             }
-            while (done_it < m_run && !stopped) {
-              const uint32_t cnt = min(32u, m_run - done_it);
-              double cj = 0.0;
-              if ((uint32_t)lane < cnt) {
-                // S_j and B (s + j) stay below 256 * l_max < 2^24 (kernel limits)
-                const uint32_t jj = done_it + (uint32_t)lane;
-                const uint32_t S_j = m.S + B * jj;
-                const double xc = __ull2double_rn(K0 + (uint64_t)K1 * S_j);
-                const double xp = __uint2double_rn(B * (smax0 + jj));
-                const double xs = __uint2double_rn(S_j);
-                cj = __dadd_rn(__dadd_rn(__fma_rn(ac, xc, bc), __fma_rn(ap, xp, bp)), __fma_rn(as_, xs, bs_));
-              }
-              // Exact parallel form of the sequential sum (same doubles as the one-by-one adds):
-              // while every partial sum stays in t's binade [2^e, 2^(e+1)) (ulp u), each add
-              // RN(acc + c) = acc + round_u(c), where round_u(c) = RN(t + c) - t (exact), unless c
-              // sits exactly half-way between multiples of u (a tie, whose even-rounding depends
-              // on acc): the partial sums are then t + prefix sums of the round_u(c), all
-              // multiples of u below 2^(e+1), hence exact in any order (a warp scan).  Chunks with
-              // a negative cost, a tie or a binade crossing take the sequential walk below.
-              {
-                const uint64_t eb = (uint64_t)__double_as_longlong(t) & 0x7FF0000000000000ull;
-                const bool tok = t > 0.0 && eb >= (64ull << 52) && eb < (0x7F0ull << 52);
-                if (tok) {
-                  const double s = __dadd_rn(t, cj);
-                  const double r = __dsub_rn(s, t);
-                  const double err = __dsub_rn(cj, r);   // exact (Fast2Sum, t >= c when in binade)
-                  const double halfu = __longlong_as_double((long long)(eb - (53ull << 52)));
-                  const double top = __longlong_as_double((long long)(eb + (1ull << 52)));   // 2^(e+1)
-                  double psum = r;
-#pragma unroll
-                  for (int o = 1; o < 32; o <<= 1) {
-                    const double nb2 = __shfl_up_sync(FULL, psum, o);
-                    if (lane >= o) psum = __dadd_rn(psum, nb2);
-                  }
-                  const double acc_j = __dadd_rn(t, psum);   // partial sum after iteration lane
-                  const bool in = (uint32_t)lane < cnt;
-                  const uint32_t bstop = NOSTOP ? 0u : __ballot_sync(FULL, in && !(acc_j < stop_t));
-                  const uint32_t upto = bstop ? (uint32_t)(__ffs(bstop) - 1) : cnt - 1;   // last lane used
-                  const bool bad = (uint32_t)lane <= upto && (cj < 0.0 || fabs(err) == halfu || !(acc_j < top));
-                  if (!__any_sync(FULL, bad)) {
-                    t = __shfl_sync(FULL, acc_j, upto);
-                    done_it += upto + 1;
-                    stopped = bstop != 0;
-                    continue;
-                  }
-                }
-              }
-              W.cbuf[lane] = cj;
-              const bool mono = __all_sync(FULL, !(cj < 0.0));
-              __syncwarp();
-              double acc = t;
-#pragma unroll 8
-              for (uint32_t q2 = 0; q2 < cnt; ++q2) acc = __dadd_rn(acc, W.cbuf[q2]);
-              if (mono && acc < stop_t) {
-                t = acc;
-                done_it += cnt;
-              } else {   // the chunk reaches stop_t (or costs are not monotone): step and check
-                acc = t;
-                uint32_t q2 = 0;
-                do {
-                  acc = __dadd_rn(acc, W.cbuf[q2]);
-                  ++q2;
-                } while (q2 < cnt && acc < stop_t);
-                t = acc;
-                done_it += q2;
-                stopped = acc >= stop_t;
-              }
-              __syncwarp();
-            }
-          } else if (K0 + (uint64_t)K1 * (m.S + B * (m_run - 1)) < (1ull << 53)) {
-            // every x of the run is an integer below 2^53: exact fp64 increments == RN conversions
-            double xc = (double)(K0 + (uint64_t)K1 * m.S);
-            const double dxc = (double)((uint64_t)K1 * B), dB = (double)B;
-            double xp = (double)(B * smax0), xs = (double)m.S;
-            uint32_t jj = 0;
-            do {
-              const double tc = __fma_rn(ac, xc, bc);
-              const double tp = __fma_rn(ap, xp, bp);
-              const double ts = __fma_rn(as_, xs, bs_);
-              t = __dadd_rn(t, __dadd_rn(__dadd_rn(tc, tp), ts));
-              xc = __dadd_rn(xc, dxc);
-              xp = __dadd_rn(xp, dB);
-              xs = __dadd_rn(xs, dB);
-              ++jj;
-            } while (jj < m_run && t < stop_t);
-            done_it = jj;
           } else {
-            uint32_t jj = 0;
-            do {
-              const uint32_t S_j = m.S + B * jj;
-              const double tc = __fma_rn(ac, __ull2double_rn(K0 + (uint64_t)K1 * S_j), bc);
-              const double tp = __fma_rn(ap, __uint2double_rn(B * (smax0 + jj)), bp);
-              const double ts = __fma_rn(as_, __uint2double_rn(S_j), bs_);
-              t = __dadd_rn(t, __dadd_rn(__dadd_rn(tc, tp), ts));
-              ++jj;
-            } while (jj < m_run && t < stop_t);
-            done_it = jj;
+            // short runs: iteration by iteration (each lane its own member under GRP)
+            const double2* cb = reinterpret_cast<const double2*>(coef_l + (size_t)(B - 1) * 8);
+            const double2 cc = __ldg(cb), cp = __ldg(cb + 1), cs = __ldg(cb + 2);
+            const double ac = cc.x, bc = cc.y, ap = cp.x, bp = cp.y, as_ = cs.x, bs_ = cs.y;
+            double t = m.t;
+            if (K0 + (uint64_t)K1_l * (m.S + B * (m_run - 1)) < (1ull << 53)) {
+              // every x of the run is an integer below 2^53: exact fp64 increments == RN conversions
+              double xc = (double)(K0 + (uint64_t)K1_l * m.S);
+              const double dxc = (double)((uint64_t)K1_l * B), dB = (double)B;
+              double xp = (double)(B * smax0), xs = (double)m.S;
+              uint32_t jj = 0;
+              do {
+                const double tc = __fma_rn(ac, xc, bc);
+                const double tp = __fma_rn(ap, xp, bp);
+                const double ts = __fma_rn(as_, xs, bs_);
+                t = __dadd_rn(t, __dadd_rn(__dadd_rn(tc, tp), ts));
+                xc = __dadd_rn(xc, dxc);
+                xp = __dadd_rn(xp, dB);
+                xs = __dadd_rn(xs, dB);
+                ++jj;
+              } while (jj < m_run && t < stop_t);
+              done_it = jj;
+            } else {
+              uint32_t jj = 0;
+              do {
+                const uint32_t S_j = m.S + B * jj;
+                const double tc = __fma_rn(ac, __ull2double_rn(K0 + (uint64_t)K1_l * S_j), bc);
+                const double tp = __fma_rn(ap, __uint2double_rn(B * (smax0 + jj)), bp);
+                const double ts = __fma_rn(as_, __uint2double_rn(S_j), bs_);
+                t = __dadd_rn(t, __dadd_rn(__dadd_rn(tc, tp), ts));
+                ++jj;
+              } while (jj < m_run && t < stop_t);
+              done_it = jj;
+            }
+            m.t = t;
           }
-          m.t = t;
           K2STAT(8, done_it);
           if (m_run > SAMU_K2_CHUNK_MIN) K2STAT(14, 1);
           // closed-form exact updates for the done_it iterations of the run
@@ -902,6 +960,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1 |
                                            : __reduce_add_sync(FULL, (uint32_t)lane < rr ? hv : 0u);
           const uint32_t need_sum = bs.div(done_it) * B + need_rr;
           m.F -= (int32_t)need_sum;
+          if (GRP) W.minF = min(W.minF, m.F);
           m.S += B * done_it;
           m.d += done_it;
           m.needidx = bs.mod(m.needidx + bs.v() - rr);
@@ -909,6 +968,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1 |
         if (m.d != m.next_fin && done_it == i_pre && !(done_it > 0 && m.t >= stop_t)) {
           // ---- this decode must preempt (c7): recompute the last admitted requests ----
           uint32_t need = W.hist[m.needidx];
+          if (GRP && (int32_t)need > m.F) W.minF = INT_MIN;
           while ((int32_t)need > m.F) {
             uint32_t vmeta;
             int ol, vs;
@@ -982,8 +1042,8 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1 |
           const uint32_t B2 = m.B;
           const uint32_t smax = (uint32_t)((int32_t)m.d + m.maxO);
           m.F -= (int32_t)need;
-          const uint64_t fl = LC * B2 + (uint64_t)K1 * m.S;
-          const double lat = iter_cost(C.coef, B2, fl, B2 * smax, m.S);
+          const uint64_t fl = LC * B2 + (uint64_t)K1_l * m.S;
+          const double lat = iter_cost(coef_l, B2, fl, B2 * smax, m.S);
           m.t = __dadd_rn(m.t, lat);
           m.a1 += B2;
           m.a2 += m.S;
@@ -1196,26 +1256,41 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1 |
       }
       if (over && lane == 0) over[j] = (done || !cut) ? 0.0 : __dsub_rn(m.t, W.tau);
     }
-    if (lane == 0) {
-      samu_trial_rec rec;
-      rec.t_end = m.t;
-      {   // FLOPs = LC a1 + K1 a2 in u128
-        uint64_t lo = LC * m.a1, hi = __umul64hi(LC, m.a1);
-        const uint64_t plo = (uint64_t)K1 * m.a2, phi = __umul64hi((uint64_t)K1, m.a2);
-        lo += plo;
-        hi += phi + (lo < plo ? 1ull : 0ull);
-        rec.flops_lo = lo;
-        rec.flops_hi = hi;
+    // lane v < nv writes member v's record (lane 0 alone without groups), or queues the member's
+    // item for a simulation of its own when its schedule would have differed from the head's
+    const uint32_t nv = GRP ? W.nv : 1u;
+    const uint32_t my_ci = GRP ? W.vci[lane] : ci;
+    if ((uint32_t)lane < nv) {
+      const bool in_sync = lane == 0 || W.minF >= C.blocks - (CONSTC ? c_cands[my_ci] : P.cands[my_ci]).blocks;
+      if (in_sync) {
+        samu_trial_rec rec;
+        rec.t_end = m.t;
+        {   // FLOPs = LC a1 + K1 a2 in u128
+          uint64_t lo = LC * m.a1, hi = __umul64hi(LC, m.a1);
+          const uint64_t plo = (uint64_t)K1_l * m.a2, phi = __umul64hi((uint64_t)K1_l, m.a2);
+          lo += plo;
+          hi += phi + (lo < plo ? 1ull : 0ull);
+          rec.flops_lo = lo;
+          rec.flops_hi = hi;
+        }
+        rec.req_iters = m.reqit;
+        rec.iters = m.iter;
+        rec.flags = (done ? 1u : 0u) | (cut ? 2u : 0u) | (all_done ? 4u : 0u);
+        P.rep_rec[((size_t)my_ci * P.n_trials + k) * 16 + j] = rec;
+      } else if (GRP) {
+        const uint32_t slot = atomicAdd(P.fb_ctr, 1u);
+        atomicAdd(P.fb_count + my_ci, 1u);
+        // one 64-bit store: a reader sees either the empty marker or the whole entry
+        *reinterpret_cast<volatile unsigned long long*>(P.fb + slot) = (unsigned long long)my_ci | ((unsigned long long)rel << 32);
+        __threadfence();
       }
-      rec.req_iters = m.reqit;
-      rec.iters = m.iter;
-      rec.flags = (done ? 1u : 0u) | (cut ? 2u : 0u) | (all_done ? 4u : 0u);
-      P.rep_rec[((size_t)ci * P.n_trials + k) * 16 + j] = rec;
     }
     __syncwarp();
 }
 #undef LO_
 #undef LI_
+#undef K1_l
+#undef coef_l
 
 // Occupancy: 6 blocks of 4 warps per SM caps registers at 80 for 24 resident warps (C5 step
 // 436 -> 418 ms against 5 blocks at 96 registers, once the cold state moved to shared memory;
@@ -1231,7 +1306,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<MODE == 1 |
 // A launch holds only items of one MODE (DevCand::mode); the host issues one launch per mode
 // present (one kernel holding several paths is slower: a multiple of the code footprint).
 template <int BSK, bool CONSTC, int MODE>
-__global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, (MODE == 1 || MODE == 3) ? SAMU_K2_MINB_LEAN : SAMU_K2_MINB)
+__global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, is_lean(MODE) ? SAMU_K2_MINB_LEAN : SAMU_K2_MINB)
     k_simulate(SimLaunch P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // lane id kept in a register: an opaque copy cannot be rematerialised from SR_TID (an S2R
@@ -1242,22 +1317,79 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, (MODE == 1 || MODE 
   int warp_v = threadIdx.x >> 5;   // the same for the warp index, i.e. the warp's shared block (-3.3 %)
   asm volatile("" : "+r"(warp_v));
   const int warp = warp_v;
-  WarpSmT<MODE == 1 || MODE == 3>& W = reinterpret_cast<WarpSmT<MODE == 1 || MODE == 3>*>(smem_raw)[warp];
+  WarpSmT<is_lean(MODE)>& W = reinterpret_cast<WarpSmT<is_lean(MODE)>*>(smem_raw)[warp];
   const int gw = blockIdx.x * SAMU_WARPS_PER_BLOCK + warp;
   uint32_t* q = P.scratch_q + (size_t)gw * P.max_q;
   uint64_t* pkey = P.scratch_key + (size_t)gw * 4 * P.max_p;
   uint32_t* pidx = P.scratch_idx + (size_t)gw * 4 * P.max_p;
+  constexpr bool GRP = MODE == 5 || MODE == 6;
+  const bool groups = GRP && P.grp != nullptr;
   for (;;) {
-    uint32_t item = 0;
-    if (lane == 0) item = atomicAdd(P.next_item, 1u);
+    // next work: a queued fallback item first (lane 0 claims it), else a static item; with groups
+    // a warp leaves only once every static item has finished and every fallback is claimed
+    uint32_t kind = 1, item = 0, fb_ci = 0;
+    if (lane == 0) {
+      if (!groups) {
+        item = atomicAdd(P.next_item, 1u);
+        kind = item < (uint32_t)P.n_items ? 1u : 0u;
+      } else {
+        volatile uint32_t* ctr = P.fb_ctr;
+        for (;;) {
+          uint32_t f = ctr[1];
+          bool got = false;
+          while (f < ctr[0]) {
+            const uint32_t old = atomicCAS(P.fb_ctr + 1, f, f + 1);
+            if (old == f) { got = true; break; }
+            f = old;
+          }
+          if (got) {
+            unsigned long long e;
+            do { e = *reinterpret_cast<volatile unsigned long long*>(P.fb + f); } while ((uint32_t)e == SAMU_EMPTY);
+            kind = 2; fb_ci = (uint32_t)e; item = (uint32_t)(e >> 32);
+            break;
+          }
+          if (*reinterpret_cast<volatile uint32_t*>(P.next_item) < (uint32_t)P.n_items) {
+            item = atomicAdd(P.next_item, 1u);
+            if (item < (uint32_t)P.n_items) { kind = 1; break; }
+          }
+          if (ctr[2] >= (uint32_t)P.n_items) {   // no static item left running: no more pushes
+            __threadfence();
+            if (ctr[1] >= ctr[0]) { kind = 0; break; }
+            continue;
+          }
+          __nanosleep(256);
+        }
+      }
+    }
+    kind = __shfl_sync(FULL, kind, 0);
+    if (kind == 0) break;
     item = __shfl_sync(FULL, item, 0);
-    if (item >= (uint32_t)P.n_items) break;
-    sim_item<BSK, CONSTC, MODE>(P, W, lane, q, pkey, pidx, item);
+    uint32_t ci, rel;
+    uint4 grp = make_uint4(1u, 0u, 0u, 0u);
+    if (kind == 2) {   // fallback: a member simulated on its own (item = index within the candidate)
+      ci = __shfl_sync(FULL, fb_ci, 0);
+      rel = item;
+    } else {
+      // decode the item: candidate (group head) by binary search over the launch's offsets
+      uint32_t lo_x = 0, hi_x = (uint32_t)P.n_ord;   // off[lo_x] <= item < off[hi_x]
+      while (hi_x - lo_x > 1) {
+        const uint32_t mid = (lo_x + hi_x) >> 1;
+        if (__ldg(P.off + mid) <= item) lo_x = mid; else hi_x = mid;
+      }
+      ci = __ldg(P.ord + lo_x);
+      rel = item - __ldg(P.off + lo_x);
+      if (groups) grp = __ldg(P.grp + lo_x);
+    }
+    sim_item<BSK, CONSTC, MODE>(P, W, lane, q, pkey, pidx, ci, rel, grp);
+    if (groups && kind == 1 && lane == 0) {
+      __threadfence();
+      atomicAdd(P.fb_ctr + 2, 1u);
+    }
   }
 }
 
 int32_t simulate_smem_bytes(int mode) {
-  return (int32_t)(((mode == 1 || mode == 3) ? sizeof(WarpSmT<true>) : sizeof(WarpSmT<false>)) * SAMU_WARPS_PER_BLOCK);
+  return (int32_t)((is_lean(mode) ? sizeof(WarpSmT<true>) : sizeof(WarpSmT<false>)) * SAMU_WARPS_PER_BLOCK);
 }
 
 template <int BSK, bool CONSTC, int MODE>
@@ -1273,14 +1405,18 @@ static cudaError_t prepare_one(int* bpsm_modes) {
 }
 
 // resident blocks per SM for each K2 mode (the minimum over that mode's instantiations)
-cudaError_t simulate_prepare(int blocks_per_sm[5]) {
-  for (int md = 0; md < 5; ++md) blocks_per_sm[md] = 1 << 30;
+cudaError_t simulate_prepare(int blocks_per_sm[SAMU_K2_MODES]) {
+  for (int md = 0; md < SAMU_K2_MODES; ++md) blocks_per_sm[md] = 1 << 30;
   cudaError_t e;
   if ((e = prepare_one<16, true, 0>(blocks_per_sm)) != cudaSuccess) return e;
   if ((e = prepare_one<16, true, 1>(blocks_per_sm)) != cudaSuccess) return e;
   if ((e = prepare_one<16, true, 2>(blocks_per_sm)) != cudaSuccess) return e;
   if ((e = prepare_one<16, true, 3>(blocks_per_sm)) != cudaSuccess) return e;
   if ((e = prepare_one<16, true, 4>(blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<16, true, 5>(blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<16, true, 6>(blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<16, false, 5>(blocks_per_sm)) != cudaSuccess) return e;
+  if ((e = prepare_one<16, false, 6>(blocks_per_sm)) != cudaSuccess) return e;
   if ((e = prepare_one<16, false, 3>(blocks_per_sm)) != cudaSuccess) return e;
   if ((e = prepare_one<16, false, 4>(blocks_per_sm)) != cudaSuccess) return e;
   if ((e = prepare_one<16, false, 0>(blocks_per_sm)) != cudaSuccess) return e;
@@ -1300,6 +1436,8 @@ static void launch_variant(const SimLaunch& L, uint32_t block_size, int mode, in
   else if (block_size == 16 && mode == 2) k_simulate<16, CONSTC, 2><<<n_blocks, blk, smem, s>>>(L);
   else if (block_size == 16 && mode == 3) k_simulate<16, CONSTC, 3><<<n_blocks, blk, smem, s>>>(L);
   else if (block_size == 16 && mode == 4) k_simulate<16, CONSTC, 4><<<n_blocks, blk, smem, s>>>(L);
+  else if (block_size == 16 && mode == 5) k_simulate<16, CONSTC, 5><<<n_blocks, blk, smem, s>>>(L);
+  else if (block_size == 16 && mode == 6) k_simulate<16, CONSTC, 6><<<n_blocks, blk, smem, s>>>(L);
   else if (block_size == 16) k_simulate<16, CONSTC, 0><<<n_blocks, blk, smem, s>>>(L);
   else if ((block_size & (block_size - 1)) == 0) k_simulate<0, CONSTC, 0><<<n_blocks, blk, smem, s>>>(L);
   else k_simulate<-1, CONSTC, 0><<<n_blocks, blk, smem, s>>>(L);
@@ -1332,25 +1470,23 @@ cudaError_t launch_simulate(const SimLaunch* Ls, const int* modes, const int32_t
     e = cudaMemcpyToSymbolAsync(c_cands, host_cands, sizeof(DevCand) * (size_t)Ls[0].n_cands, 0, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return e;
   }
-  int lean = -1;
-  for (int i = 0; i < n_launch; ++i) if (modes[i] == 1) lean = i;
-  const bool fork = lean >= 0 && n_launch > 1 && s2 != nullptr;
+  // the LEAN launches without a time limit (modes 1 and 5) may run on the auxiliary stream
+  int n_lean = 0, n_other = 0;
+  for (int i = 0; i < n_launch; ++i) (modes[i] == 1 || modes[i] == 5 ? n_lean : n_other) += 1;
+  const bool fork = n_lean > 0 && n_other > 0 && s2 != nullptr;
   if (fork) {   // s2 starts after the table copy (and everything before it on s)
     if ((e = cudaEventRecord(ev_fork, s)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(s2, ev_fork, 0)) != cudaSuccess) return e;
   }
   for (int i = 0; i < n_launch; ++i) {
-    if (fork && i == lean) continue;
+    const bool on_aux = fork && (modes[i] == 1 || modes[i] == 5);
     const int smem = simulate_smem_bytes(modes[i]);
-    if (constc) launch_variant<true>(Ls[i], block_size, modes[i], n_blocks[i], smem, s);
-    else launch_variant<false>(Ls[i], block_size, modes[i], n_blocks[i], smem, s);
+    cudaStream_t st = on_aux ? s2 : s;
+    if (constc) launch_variant<true>(Ls[i], block_size, modes[i], n_blocks[i], smem, st);
+    else launch_variant<false>(Ls[i], block_size, modes[i], n_blocks[i], smem, st);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   if (fork) {
-    const int smem = simulate_smem_bytes(1);
-    if (constc) launch_variant<true>(Ls[lean], block_size, 1, n_blocks[lean], smem, s2);
-    else launch_variant<false>(Ls[lean], block_size, 1, n_blocks[lean], smem, s2);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if ((e = cudaEventRecord(ev_join, s2)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(s, ev_join, 0)) != cudaSuccess) return e;
   }

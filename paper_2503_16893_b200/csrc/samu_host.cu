@@ -4,8 +4,10 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <condition_variable>
 #include <mutex>
+#include <set>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -133,13 +135,17 @@ struct samu_ctx {
   DevBuf d_cand_sum;   // per-candidate summaries of samu_simulate_batch
   DevBuf d_stage;      // staging for app-load tables (eCDF knots, coefficient rows)
   PlanBufs pb;         // planner buffers (borrowed by Greedy / Replay for the duration of a call)
-  DevBuf d_cands, d_items, d_counter, d_rep_rec, d_scratch_q, d_scratch_key, d_scratch_idx, d_error;
-  DevBuf d_sum, d_gather_send, d_gather_recv;
-  int sim_blocks_per_sm[5] = {0, 0, 0, 0, 0};   // resident K2 blocks per SM, per K2 mode
+  DevBuf d_cands, d_items, d_counter, d_rep_rec, d_scratch_q, d_scratch_key, d_scratch_idx, d_error, d_fb;
+  DevBuf d_sum, d_gather_send, d_gather_recv, d_gather_meta, d_flag;
+  int sim_blocks_per_sm[SAMU_K2_MODES] = {};   // resident K2 blocks per SM, per K2 mode
 
   // stats
   int64_t n_sims = 0;
   uint64_t launches = 0;          // kernels launched by this context
+  int64_t share[3] = {0, 0, 0};   // schedule sharing: group items, member items, fallbacks
+  // schedule-sharing hints: (node, dp, tp, mode) -> fraction of the member's items that fell out of
+  // sync in its last grouped batch (reset by samu_app_load)
+  std::map<std::array<int, 4>, double> share_hint;
   uint64_t req_iters = 0;
 };
 
@@ -214,6 +220,24 @@ static samu_status comm_allreduce_i32(samu_ctx* c, const int32_t* send, int32_t*
     return SAMU_OK;
   }
   CKN(c, ncclAllReduce(send, recv, n, ncclInt32, op == 0 ? ncclMax : ncclSum, c->comm, s));
+  return SAMU_OK;
+}
+
+// Ranks leave a sharded call together: before the next collective, a rank-local failure (e.g. a
+// kernel-detected infeasible trial on one rank's share) is agreed on with an all-reduce, so no
+// rank waits in a collective its peers never reach.  (A poisoned context cannot take part: a
+// CUDA / NCCL failure is reported on its rank; peers then need ncclCommAbort via ctx_destroy.)
+static samu_status agree(samu_ctx* c, samu_status local) {
+  if (!(c->world > 1 || c->comm != nullptr) || c->poisoned) return local;
+  const std::string keep = c->err;
+  int32_t f[2] = {local != SAMU_OK ? 1 : 0, 0};
+  CK(c, c->d_flag.ensure(2 * sizeof(int32_t)));
+  CK(c, cudaMemcpyAsync(c->d_flag.p, f, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+  RET(comm_allreduce_i32(c, c->d_flag.as<int32_t>(), c->d_flag.as<int32_t>() + 1, 1, 0));
+  CK(c, cudaMemcpyAsync(f + 1, c->d_flag.as<int32_t>() + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  if (local != SAMU_OK) { c->err = keep; return local; }
+  if (f[1]) FAIL(c, SAMU_E_STATE, "another rank failed in this collective call");
   return SAMU_OK;
 }
 
@@ -347,6 +371,10 @@ extern "C" void samu_ctx_destroy(samu_ctx* c) {
 extern "C" const char* samu_last_error(const samu_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
 extern "C" uint64_t samu_launch_count(const samu_ctx* c) { return c ? c->launches : 0; }
+extern "C" void samu_share_stats(const samu_ctx* c, int64_t out[3]) {
+  if (!out) return;
+  for (int i = 0; i < 3; ++i) out[i] = c ? c->share[i] : 0;
+}
 
 // ---------------------------------------------------------------------------------------------
 // C ABI: registration
@@ -571,6 +599,7 @@ extern "C" samu_status samu_app_load(samu_ctx* c, const samu_engine_cfg* engine,
     c->node_exp_out[v] = std::max(1.0, acc / (double)(c->node_end[v] - c->node_begin[v]));
   }
   c->app_loaded = true;
+  c->share_hint.clear();
   return SAMU_OK;
 }
 
@@ -724,11 +753,11 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
   int max_phase = 0;
   for (auto& j : jobs) max_phase = std::max(max_phase, j.phase);
   if (!c->sim_blocks_per_sm[0]) {
-    int bpsm[5] = {0, 0, 0, 0, 0};
+    int bpsm[SAMU_K2_MODES] = {};
     CK(c, simulate_prepare(bpsm));
-    for (int md = 0; md < 5; ++md)
+    for (int md = 0; md < SAMU_K2_MODES; ++md)
       if (bpsm[md] < 1) FAIL(c, SAMU_E_CUDA, "simulate: kernel does not fit on an SM");
-    for (int md = 0; md < 5; ++md) c->sim_blocks_per_sm[md] = bpsm[md];
+    for (int md = 0; md < SAMU_K2_MODES; ++md) c->sim_blocks_per_sm[md] = bpsm[md];
   }
   CK(c, c->d_error.ensure(2 * sizeof(int32_t)));
   CK(c, cudaMemsetAsync(c->d_error.p, 0, 2 * sizeof(int32_t), s));
@@ -790,7 +819,7 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
     {
       // small batches (e.g. the planner's later inner steps) run as one general launch: a launch per
       // mode only pays off when each covers several waves of the persistent grid
-      int64_t cnt[5] = {0, 0, 0, 0, 0};
+      int64_t cnt[SAMU_K2_MODES] = {};
       for (size_t x = 0; x < dc.size(); ++x) cnt[dc[x].mode] += (int64_t)T * dc[x].dp;
       const int64_t wave = (int64_t)c->n_sm * 24;
       // SAMU_K2_MODES=always|never overrides the size rule (tests run the LEAN / FRESH paths on
@@ -806,24 +835,83 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
       for (const DevCand& D : dc) total += (int64_t)T * D.dp;
       if (total >= ((int64_t)1 << 31)) FAIL(c, SAMU_E_INVALID, "simulate: too many work items (trials x replicas)");
     }
-    // per mode: candidate order and item offsets (the device decodes item -> (candidate, trial, replica))
-    std::vector<uint32_t> ord_off;   // [mode 0 ord | off][mode 1 ...] ... [mode 4 ...]
-    size_t ord_at[5], off_at[5];
-    int64_t n_items[5];
-    int n_ord[5];
-    for (int md = 0; md < 5; ++md) {
-      std::vector<uint32_t> ordm, offm{0};
-      for (int x : order)
-        if (dc[x].mode == md) {
-          ordm.push_back((uint32_t)x);
-          offm.push_back(offm.back() + (uint32_t)(T * dc[x].dp));
+    // Schedule sharing in the modes without a time limit (1 LEAN, 2 FRESH): the candidates of one
+    // (node, dp) differ only in tp (KV blocks, coefficients, FLOPs factor, load time) and share
+    // their event schedule while KV never binds below the largest block count.  They form groups
+    // of <= 4, most blocks first, simulated once by the group launches (modes 5 / 6,
+    // SimLaunch::grp); a member that falls out of sync in an item is re-simulated alone from the
+    // launch's fallback queue.  A member that fell out of sync in most items of its last grouped
+    // batch is scheduled on its own (a scheduling hint only: every record is exact either way).
+    // SAMU_K2_GROUP=never: no groups; =always: group every member, ignoring the hints.
+    const char* gpol = std::getenv("SAMU_K2_GROUP");
+    const bool grouping = !(gpol && std::strcmp(gpol, "never") == 0);
+    const bool group_all = gpol && std::strcmp(gpol, "always") == 0;
+    auto hint_key = [&](const DevCand& D) { return std::array<int, 4>{D.node, D.dp, D.tp, D.mode}; };
+    std::vector<std::vector<int>> groups;   // member lists, head (most blocks) first
+    std::vector<bool> non_head(dc.size(), false);
+    if (grouping) {
+      std::vector<bool> taken(dc.size(), false);
+      for (int x : order) {
+        if (taken[x] || (dc[x].mode != 1 && dc[x].mode != 2)) continue;
+        std::vector<int> mem;
+        for (int y : order)
+          if (!taken[y] && dc[y].mode == dc[x].mode && dc[y].node == dc[x].node && dc[y].dp == dc[x].dp) mem.push_back(y);
+        for (int y : mem) taken[y] = true;
+        std::stable_sort(mem.begin(), mem.end(), [&](int a, int b) { return dc[a].blocks > dc[b].blocks; });
+        std::vector<int> keep{mem[0]};
+        for (size_t i = 1; i < mem.size(); ++i) {
+          auto h = c->share_hint.find(hint_key(dc[mem[i]]));
+          if (group_all || h == c->share_hint.end() || h->second < 0.5) keep.push_back(mem[i]);
         }
+        for (size_t g0 = 0; g0 < keep.size(); g0 += 4) {
+          const size_t nv = std::min<size_t>(4, keep.size() - g0);
+          if (nv < 2) continue;   // a single member stays on the single-candidate path
+          groups.emplace_back(keep.begin() + g0, keep.begin() + g0 + nv);
+          for (size_t i = 0; i < nv; ++i) {
+            if (i) non_head[keep[g0 + i]] = true;
+            dc[keep[g0 + i]].mode += 4;
+          }
+        }
+      }
+    }
+    // per mode: candidate (group head) order and item offsets (the device decodes item ->
+    // (candidate, trial, replica))
+    std::vector<uint32_t> ord_off;   // [mode 0 ord | off] ... [mode 6 ...] [grp mode 5][grp mode 6]
+    size_t ord_at[SAMU_K2_MODES], off_at[SAMU_K2_MODES], grp_at[SAMU_K2_MODES] = {};
+    int64_t n_items[SAMU_K2_MODES], fb_cap[SAMU_K2_MODES] = {};
+    int n_ord[SAMU_K2_MODES];
+    std::vector<uint32_t> grp_words[SAMU_K2_MODES];
+    for (int md = 0; md < SAMU_K2_MODES; ++md) {
+      std::vector<uint32_t> ordm, offm{0};
+      if (md == 5 || md == 6) {
+        for (const auto& G : groups) {
+          if (dc[G[0]].mode != md) continue;
+          ordm.push_back((uint32_t)G[0]);
+          offm.push_back(offm.back() + (uint32_t)(T * dc[G[0]].dp));
+          uint32_t wds[4] = {(uint32_t)G.size(), 0u, 0u, 0u};
+          for (size_t i = 1; i < G.size(); ++i) wds[i] = (uint32_t)G[i];
+          grp_words[md].insert(grp_words[md].end(), wds, wds + 4);
+          fb_cap[md] += (int64_t)(G.size() - 1) * T * dc[G[0]].dp;
+        }
+      } else {
+        for (int x : order)
+          if (dc[x].mode == md) {
+            ordm.push_back((uint32_t)x);
+            offm.push_back(offm.back() + (uint32_t)(T * dc[x].dp));
+          }
+      }
       n_items[md] = offm.back();
       n_ord[md] = (int)ordm.size();
       ord_at[md] = ord_off.size();
       ord_off.insert(ord_off.end(), ordm.begin(), ordm.end());
       off_at[md] = ord_off.size();
       ord_off.insert(ord_off.end(), offm.begin(), offm.end());
+    }
+    for (int md = 5; md <= 6; ++md) {
+      if (grp_words[md].empty()) continue;
+      while (ord_off.size() % 4) ord_off.push_back(0);   // uint4 alignment
+      grp_at[md] = ord_off.size();
+      ord_off.insert(ord_off.end(), grp_words[md].begin(), grp_words[md].end());
     }
 
     SimLaunch L;
@@ -838,37 +926,50 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
     L.fin_t = S.fin_t;
     L.over = S.over;
     L.error = c->d_error.as<int32_t>();
+    const int64_t fb_total = fb_cap[5] + fb_cap[6];
     {
       // persistent grid per mode: resident blocks x SMs, no more warps than items
-      int n_blocks[5];
-      size_t n_warps = SAMU_WARPS_PER_BLOCK;   // scratch rings: modes 0, 2, 4 (LEAN modes 1, 3 use none)
-      for (int md = 0; md < 5; ++md) {
-        const int64_t want = (n_items[md] + SAMU_WARPS_PER_BLOCK - 1) / SAMU_WARPS_PER_BLOCK;
+      int n_blocks[SAMU_K2_MODES];
+      size_t n_warps = SAMU_WARPS_PER_BLOCK;   // scratch rings: modes 0, 2, 4, 6 (the LEAN modes use none)
+      for (int md = 0; md < SAMU_K2_MODES; ++md) {
+        const int64_t want = (n_items[md] + fb_cap[md] + SAMU_WARPS_PER_BLOCK - 1) / SAMU_WARPS_PER_BLOCK;
         n_blocks[md] = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->n_sm * c->sim_blocks_per_sm[md], want));
-        if (md != 1 && md != 3) n_warps = std::max(n_warps, (size_t)n_blocks[md] * SAMU_WARPS_PER_BLOCK);
+        if (md != 1 && md != 3 && md != 5) n_warps = std::max(n_warps, (size_t)n_blocks[md] * SAMU_WARPS_PER_BLOCK);
       }
       CK(c, c->d_scratch_q.ensure(sizeof(uint32_t) * n_warps * max_q));
       CK(c, c->d_scratch_key.ensure(sizeof(uint64_t) * n_warps * 4 * max_p));
       CK(c, c->d_scratch_idx.ensure(sizeof(uint32_t) * n_warps * 4 * max_p));
       CK(c, upload(c->d_cands, dc, s));
       CK(c, upload(c->d_items, ord_off, s));
-      CK(c, c->d_counter.ensure(5 * sizeof(uint32_t)));
-      CK(c, cudaMemsetAsync(c->d_counter.p, 0, 5 * sizeof(uint32_t), s));
+      // item counters [7], fallback counters [2][3] (modes 5, 6), fallbacks per candidate [n]
+      const size_t n_ctr = SAMU_K2_MODES + 6 + idx.size();
+      CK(c, c->d_counter.ensure(n_ctr * sizeof(uint32_t)));
+      CK(c, cudaMemsetAsync(c->d_counter.p, 0, n_ctr * sizeof(uint32_t), s));
+      if (fb_total >= ((int64_t)1 << 31)) FAIL(c, SAMU_E_INVALID, "simulate: too many work items (trials x replicas)");
+      if (fb_total) {
+        CK(c, c->d_fb.ensure(sizeof(uint2) * fb_total));
+        CK(c, cudaMemsetAsync(c->d_fb.p, 0xFF, sizeof(uint2) * fb_total, s));
+      }
       CK(c, c->d_rep_rec.ensure(sizeof(samu_trial_rec) * 16 * idx.size() * T));
       L.cands = c->d_cands.as<DevCand>();
       L.ord = nullptr;
       L.off = nullptr;
       L.n_ord = 0;
       L.next_item = c->d_counter.as<uint32_t>();
+      L.grp = nullptr;
+      L.fb = nullptr;
+      L.fb_ctr = nullptr;
+      L.fb_count = c->d_counter.as<uint32_t>() + SAMU_K2_MODES + 6;
       L.rep_rec = c->d_rep_rec.as<samu_trial_rec>();
       L.scratch_q = c->d_scratch_q.as<uint32_t>();
       L.scratch_key = c->d_scratch_key.as<uint64_t>();
       L.scratch_idx = c->d_scratch_idx.as<uint32_t>();
       L.max_q = (int32_t)max_q;
       L.max_p = (int32_t)max_p;
-      SimLaunch LM[5];
-      int modes[5], nb[5], n_launch = 0;
-      for (int md : {0, 2, 4, 3, 1}) {   // in order on s; the LEAN launch (1) concurrent on the aux stream
+      SimLaunch LM[SAMU_K2_MODES];
+      int modes[SAMU_K2_MODES], nb[SAMU_K2_MODES], n_launch = 0;
+      // in order on s; the LEAN launches (5, 1) concurrent on the aux stream
+      for (int md : {0, 6, 2, 4, 3, 5, 1}) {
         if (n_items[md] == 0) continue;
         SimLaunch& X = LM[n_launch];
         X = L;
@@ -877,6 +978,11 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
         X.n_ord = n_ord[md];
         X.n_items = (int32_t)n_items[md];
         X.next_item = c->d_counter.as<uint32_t>() + md;
+        if (md == 5 || md == 6) {
+          X.grp = reinterpret_cast<const uint4*>(c->d_items.as<uint32_t>() + grp_at[md]);
+          X.fb = c->d_fb.as<uint2>() + (md == 6 ? fb_cap[5] : 0);
+          X.fb_ctr = c->d_counter.as<uint32_t>() + SAMU_K2_MODES + 3 * (md - 5);
+        }
         modes[n_launch] = md;
         nb[n_launch] = n_blocks[md];
         ++n_launch;
@@ -886,10 +992,10 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
         CK(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         CK(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
       }
-      // concurrent LEAN launch only when the other launch is short (a few waves): then its
+      // concurrent LEAN launches only when the others are short (a few waves): then their
       // longest replica-sims are the critical path and the LEAN items fill the idle warps; with
-      // many waves the two kernels only compete for the instruction cache (~2 % slower)
-      const bool overlap = n_items[0] + n_items[2] + n_items[3] + n_items[4] < 8 * (int64_t)c->n_sm * 24;
+      // many waves the kernels only compete for the instruction cache (~2 % slower)
+      const bool overlap = n_items[0] + n_items[2] + n_items[3] + n_items[4] + n_items[6] < 8 * (int64_t)c->n_sm * 24;
       CK(c, launch_simulate(LM, modes, nb, n_launch, dc.data(), (uint32_t)c->eng.block_size, s,
                             overlap ? c->aux_stream : nullptr, c->ev_fork, c->ev_join));
       c->launches += n_launch > 1 ? n_launch - 1 : 0;
@@ -898,8 +1004,25 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
     c->launches += 2;
     c->n_sims += (int64_t)idx.size() * T;
     int32_t herr[2] = {0, 0};
+    std::vector<uint32_t> hfb;
     CK(c, cudaMemcpyAsync(herr, c->d_error.p, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    if (fb_total) {
+      hfb.assign(idx.size(), 0u);
+      CK(c, cudaMemcpyAsync(hfb.data(), c->d_counter.as<uint32_t>() + SAMU_K2_MODES + 6, sizeof(uint32_t) * idx.size(),
+                            cudaMemcpyDeviceToHost, s));
+    }
     CK(c, cudaStreamSynchronize(s));
+    for (const auto& G : groups) {
+      const int64_t items = (int64_t)T * dc[G[0]].dp;
+      c->share[0] += items;
+      c->share[1] += items * (int64_t)(G.size() - 1);
+      for (size_t i = 1; i < G.size(); ++i) {
+        DevCand D = dc[G[i]];
+        D.mode -= 4;
+        c->share[2] += hfb[G[i]];
+        c->share_hint[hint_key(D)] = (double)hfb[G[i]] / (double)items;
+      }
+    }
     if (herr[0]) {
       static const char* sites[] = {"?", "waiting chain successor of a done request", "bad status word",
                                     "scratch overflow", "running/preempted set exceeds the engine slots",
@@ -923,9 +1046,31 @@ static void trial_share(int T, int world, int rank, int* begin, int* count) {
   *begin = rank * base + std::min(rank, rem);
 }
 
-// all-gather per-(job, local trial) records [n][T_local] into rows of `dst` ([*][T]) at `slots`
+// Sharding of a (jobs x trials) product over the ranks: world = Wt x Wc, rank r simulates trial
+// block r % Wt (contiguous split of T over Wt blocks) of the jobs of class r / Wt.  Wc = 1 (pure
+// trial sharding) whenever T >= world: trials are i.i.d., so every rank gets the same work and
+// all of its candidates.  With fewer trials than ranks (C1: T = 1) the candidates are split into
+// Wc = world / Wt classes, Wt the largest divisor of world not above T.  SAMU_SHARD_CLASSES=k
+// forces Wc = k (k | world; tests).
+static void shard_split(const samu_ctx* c, int T, int* Wt, int* Wc) {
+  int wc = 1;
+  const char* e = std::getenv("SAMU_SHARD_CLASSES");
+  const int forced = e ? std::atoi(e) : 0;
+  if (forced > 0 && c->world % forced == 0) wc = forced;
+  else if (T < c->world) {
+    int wt = 1;
+    for (int d = 1; d <= c->world; ++d) if (c->world % d == 0 && d <= std::max(T, 1)) wt = d;
+    wc = c->world / wt;
+  }
+  *Wc = wc;
+  *Wt = c->world / wc;
+}
+
+// all-gather per-(job, local trial) records [n][T_local] into rows of `dst` ([*][T]) at `slots`;
+// job_class[x] = class of job x (all 0 under pure trial sharding), Wt trial blocks
 static samu_status gather_records(samu_ctx* c, const samu_trial_rec* local, int n, int T, samu_trial_rec* dst,
-                                  const std::vector<int>& slots) {
+                                  const std::vector<int>& slots, const std::vector<int>* job_class = nullptr,
+                                  int Wt = 0) {
   cudaStream_t s = c->stream;
   if (n == 0) return SAMU_OK;
   if (!sharded(c)) {
@@ -935,9 +1080,10 @@ static samu_status gather_records(samu_ctx* c, const samu_trial_rec* local, int 
                               cudaMemcpyDeviceToDevice, s));
     return SAMU_OK;
   }
+  if (Wt <= 0) Wt = c->world;
   int b0, cnt0;
-  trial_share(T, c->world, c->rank, &b0, &cnt0);
-  const int Tmax = (T + c->world - 1) / c->world;
+  trial_share(T, Wt, c->rank % Wt, &b0, &cnt0);
+  const int Tmax = (T + Wt - 1) / Wt;
   const size_t row = sizeof(samu_trial_rec) * Tmax;
   CK(c, c->d_gather_send.ensure(row * n));
   CK(c, c->d_gather_recv.ensure(row * n * c->world));
@@ -946,15 +1092,15 @@ static samu_status gather_records(samu_ctx* c, const samu_trial_rec* local, int 
     CK(c, cudaMemcpy2DAsync(c->d_gather_send.p, row, local, sizeof(samu_trial_rec) * cnt0, sizeof(samu_trial_rec) * cnt0,
                             n, cudaMemcpyDeviceToDevice, s));
   RET(comm_allgather(c, c->d_gather_send.p, c->d_gather_recv.p, row * n));
-  for (int w = 0; w < c->world; ++w) {
-    int bw, cw;
-    trial_share(T, c->world, w, &bw, &cw);
-    if (!cw) continue;
-    const samu_trial_rec* src = c->d_gather_recv.as<samu_trial_rec>() + (size_t)w * n * Tmax;
-    for (int x = 0; x < n; ++x)
-      CK(c, cudaMemcpyAsync(dst + (size_t)slots[x] * T + bw, src + (size_t)x * Tmax, sizeof(samu_trial_rec) * cw,
-                            cudaMemcpyDeviceToDevice, s));
+  // one unpack kernel instead of a copy per (job, rank)
+  std::vector<int32_t> meta(2 * (size_t)n);
+  for (int x = 0; x < n; ++x) {
+    meta[x] = slots[x];
+    meta[n + x] = job_class ? (*job_class)[x] : 0;
   }
+  CK(c, upload(c->d_gather_meta, meta, s));
+  CK(c, samu_count(c, launch_unpack_gather(c->d_gather_recv.as<samu_trial_rec>(), c->world, n, Tmax, T, Wt,
+                                           c->d_gather_meta.as<int32_t>(), c->d_gather_meta.as<int32_t>() + n, dst, s)));
   return SAMU_OK;
 }
 
@@ -1015,7 +1161,11 @@ extern "C" samu_status samu_simulate_batch(samu_ctx* c, const samu_candidate* ca
   for (int i = 0; i < n_cands; ++i)
     if (cands[i].dep_src >= 0) jobs[i].src_fin = jobs[cands[i].dep_src].fin_t_out;
   StatePtrs S{st, g, fin_t, overshoot};
-  RET(run_jobs(c, jobs, l_out, l_in_eff, n_trials, S));
+  {
+    samu_status rj = run_jobs(c, jobs, l_out, l_in_eff, n_trials, S);
+    if (out_summary && n_cands) rj = agree(c, rj);   // the summary below is collective
+    RET(rj);
+  }
   if (out_summary && n_cands) {
     int T_total = n_trials;
     const samu_trial_rec* all = out_recs;
@@ -1030,7 +1180,12 @@ extern "C" samu_status samu_simulate_batch(samu_ctx* c, const samu_candidate* ca
       CK(c, cudaStreamSynchronize(c->stream));
       int b, cnt;
       trial_share(Tsum, c->world, c->rank, &b, &cnt);
-      if (cnt != n_trials) FAIL(c, SAMU_E_INVALID, "simulate_batch: local trial count must follow the contiguous split");
+      samu_status split = SAMU_OK;
+      if (cnt != n_trials) {
+        c->err = "simulate_batch: local trial count must follow the contiguous split";
+        split = SAMU_E_INVALID;
+      }
+      RET(agree(c, split));
       T_total = Tsum;
       CK(c, c->d_sum.ensure(sizeof(samu_trial_rec) * (size_t)n_cands * T_total));
       std::vector<int> slots(n_cands);
@@ -1060,6 +1215,11 @@ struct Ent {
 struct Greedy {
   samu_ctx* c;
   int T = 0, Tl = 0, tb = 0;
+  int Wt = 1, Wc = 1, my_class = 0;        // (trial block, job class) sharding, shard_split
+  std::map<int, int> slot_class;           // simulation slot -> job class that ran it
+  std::map<int, SimJob> slot_job;          // full slot -> its job (re-run locally for a commit)
+  std::map<int, int> slot_src;             // slot -> full slot of its dependency source
+  std::set<int> have_fin;                  // full slots whose finish times this rank computed
   size_t n = 0;
   DevBuf lo, li, st, g, fin_t, over;
   StatePtrs S;
@@ -1074,6 +1234,7 @@ struct Greedy {
   std::vector<SimJob> pending;
   std::vector<int> pending_slots;
   std::vector<int> pending_tau;            // f* full slot whose records give tau, or -1
+  std::vector<int> pending_src;            // full slot of the job's dependency source, or -1
   int64_t evals = 0;
   std::vector<bool> is_input;
   std::vector<bool> touched;               // node committed in some stage (its state is no longer FRESH)
@@ -1123,7 +1284,7 @@ struct Greedy {
     auto it = full_slot.find(key);
     if (it != full_slot.end()) { *out_slot = it->second; return SAMU_OK; }
     const double* sf = nullptr;
-    int phase = 0;
+    int phase = 0, src_slot = -1;
     const int src = c->node_input[e.node];
     if (src >= 0)
       for (const Ent& x : E)
@@ -1131,6 +1292,7 @@ struct Greedy {
           int ss;
           RET(ensure_full(x, E, &ss));
           sf = fin_buf.at(ss).as<double>();
+          src_slot = ss;
           auto pp = pending_phase.find(ss);
           if (pp != pending_phase.end()) phase = pp->second + 1;
         }
@@ -1151,7 +1313,10 @@ struct Greedy {
     pending.push_back(J);
     pending_slots.push_back(slot);
     pending_tau.push_back(-1);
+    pending_src.push_back(src_slot);
     pending_phase[slot] = phase;
+    slot_job[slot] = J;
+    slot_src[slot] = src_slot;
     *out_slot = slot;
     return SAMU_OK;
   }
@@ -1163,10 +1328,11 @@ struct Greedy {
     auto it = cut_slot.find(key);
     if (it != cut_slot.end()) { *out_slot = it->second; return SAMU_OK; }
     const double* sf = nullptr;
+    int src_slot = -1;
     const int src = c->node_input[e.node];
     if (src >= 0)
       for (const Ent& x : E)
-        if (x.node == src) { int ss; RET(ensure_full(x, E, &ss)); sf = fin_buf.at(ss).as<double>(); }
+        if (x.node == src) { int ss; RET(ensure_full(x, E, &ss)); sf = fin_buf.at(ss).as<double>(); src_slot = ss; }
     const int slot = n_slots++;
     RET(grow(n_slots));
     cut_slot[key] = slot;
@@ -1178,27 +1344,83 @@ struct Greedy {
     pending.push_back(J);             // tau_k = T_f*^(k) (this rank's trials), resolved at flush
     pending_slots.push_back(slot);
     pending_tau.push_back(fslot);
+    pending_src.push_back(src_slot);
+    slot_src[slot] = src_slot;
     *out_slot = slot;
     return SAMU_OK;
   }
   // run the pending simulations, then all-gather their records into the cache
   samu_status flush() {
     if (pending.empty()) return SAMU_OK;
+    // job classes (Wc > 1: fewer trials than ranks): jobs without a dependency source are spread
+    // over the classes longest-first onto the least loaded (identically on every rank); a
+    // dependent job runs where its source's finish times are
+    std::vector<int> cls(pending.size(), 0);
+    if (Wc > 1) {
+      std::vector<int> free_jobs;
+      for (size_t x = 0; x < pending.size(); ++x) if (pending_src[x] < 0) free_jobs.push_back((int)x);
+      auto work = [&](int x) {
+        const int v = pending[x].cand.node;
+        return (double)(c->node_end[v] - c->node_begin[v]) * c->node_exp_out[v];
+      };
+      std::stable_sort(free_jobs.begin(), free_jobs.end(), [&](int a, int b) { return work(a) > work(b); });
+      std::vector<double> load(Wc, 0.0);
+      for (int x : free_jobs) {
+        int k = 0;
+        for (int q = 1; q < Wc; ++q) if (load[q] < load[k]) k = q;
+        cls[x] = k;
+        load[k] += work(x);
+        slot_class[pending_slots[x]] = k;
+      }
+      for (size_t x = 0; x < pending.size(); ++x)
+        if (pending_src[x] >= 0) {
+          cls[x] = slot_class.at(pending_src[x]);
+          slot_class[pending_slots[x]] = cls[x];
+        }
+    }
     // the cache may have been reallocated after tau_rec pointers were taken: re-point them
     CK(c, local_rec.ensure(sizeof(samu_trial_rec) * pending.size() * std::max(Tl, 1)));
+    std::vector<SimJob> mine;
     for (size_t x = 0; x < pending.size(); ++x) {
       pending[x].out_rec = !sharded(c) ? rec(pending_slots[x]) : local_rec.as<samu_trial_rec>() + x * Tl;
       pending[x].tau_rec = pending_tau[x] >= 0 ? rec(pending_tau[x]) + tb : nullptr;
-      if (pending[x].fin_t_out)
+      if (cls[x] != my_class) continue;
+      if (pending[x].fin_t_out) {
         CK(c, samu_count(c, launch_fill_f64(pending[x].fin_t_out, (int64_t)Tl * n, std::numeric_limits<double>::infinity(),
                                             c->stream)));
+        have_fin.insert(pending_slots[x]);
+      }
+      mine.push_back(pending[x]);
     }
-    RET(run_jobs(c, pending, lo.as<uint16_t>(), li.as<uint16_t>(), Tl, S));
-    if (sharded(c)) RET(gather_records(c, local_rec.as<samu_trial_rec>(), (int)pending.size(), T, cache.as<samu_trial_rec>(), pending_slots));
+    RET(agree(c, run_jobs(c, mine, lo.as<uint16_t>(), li.as<uint16_t>(), Tl, S)));
+    if (sharded(c))
+      RET(gather_records(c, local_rec.as<samu_trial_rec>(), (int)pending.size(), T, cache.as<samu_trial_rec>(), pending_slots,
+                         &cls, Wt));
     pending.clear();
     pending_slots.clear();
     pending_tau.clear();
+    pending_src.clear();
     pending_phase.clear();
+    return SAMU_OK;
+  }
+
+  // finish times of full slot `ss` on this rank (job classes: the slot may have run elsewhere):
+  // re-simulated here, after its own source, for a commit that depends on it
+  samu_status ensure_local_fin(int ss) {
+    if (have_fin.count(ss)) return SAMU_OK;
+    const int src = slot_src.count(ss) ? slot_src.at(ss) : -1;
+    if (src >= 0) RET(ensure_local_fin(src));
+    SimJob J = slot_job.at(ss);
+    J.phase = 0;
+    J.src_fin = src >= 0 ? fin_buf.at(src).as<double>() : nullptr;
+    J.fin_t_out = fin_buf.at(ss).as<double>();
+    J.tau_rec = nullptr;
+    CK(c, local_rec.ensure(sizeof(samu_trial_rec) * std::max(Tl, 1)));
+    J.out_rec = local_rec.as<samu_trial_rec>();
+    CK(c, samu_count(c, launch_fill_f64(J.fin_t_out, (int64_t)Tl * n, std::numeric_limits<double>::infinity(), c->stream)));
+    std::vector<SimJob> one{J};
+    RET(run_jobs(c, one, lo.as<uint16_t>(), li.as<uint16_t>(), Tl, S));
+    have_fin.insert(ss);
     return SAMU_OK;
   }
 
@@ -1445,7 +1667,9 @@ struct Greedy {
     T = T_total;
     if (!borrowed) borrow();
     n = (size_t)c->n_req;
-    trial_share(T, c->world, c->rank, &tb, &Tl);
+    shard_split(c, T, &Wt, &Wc);
+    my_class = c->rank / Wt;
+    trial_share(T, Wt, c->rank % Wt, &tb, &Tl);
     cudaStream_t s = c->stream;
     is_input.assign(c->n_nodes, false);
     touched.assign(c->n_nodes, false);
@@ -1478,6 +1702,7 @@ struct Greedy {
     int fslot = -1;
     RET(ensure_full(Es[f], Es, &fslot));
     std::vector<SimJob> jobs;
+    std::vector<int> src_slots;
     CK(c, local_rec.ensure(sizeof(samu_trial_rec) * Es.size() * std::max(Tl, 1)));
     for (size_t i = 0; i < Es.size(); ++i) {
       const Ent& e = Es[i];
@@ -1491,19 +1716,23 @@ struct Greedy {
           RET(ensure_full(Es[q], Es, &ss));
           J.src_fin = fin_buf.at(ss).as<double>();
           J.phase = 1;
+          src_slots.push_back(ss);
         }
       J.tau_rec = ((int)i == f) ? nullptr : rec(fslot) + tb;
       J.out_rec = local_rec.as<samu_trial_rec>() + i * Tl;
       jobs.push_back(J);
     }
     RET(flush());
+    for (int ss : src_slots) RET(ensure_local_fin(ss));   // job classes: a source may have run elsewhere
+    CK(c, local_rec.ensure(sizeof(samu_trial_rec) * Es.size() * std::max(Tl, 1)));
+    for (size_t i = 0; i < jobs.size(); ++i) jobs[i].out_rec = local_rec.as<samu_trial_rec>() + i * Tl;
     // depth > 1 chains of dependencies commit in topological (node id) order
     for (size_t i = 0; i < jobs.size(); ++i) {
       int d = 0, v = Es[i].node;
       while (c->node_input[v] >= 0) { ++d; v = c->node_input[v]; }
       jobs[i].phase = d;
     }
-    RET(run_jobs(c, jobs, lo.as<uint16_t>(), li.as<uint16_t>(), Tl, S));
+    RET(agree(c, run_jobs(c, jobs, lo.as<uint16_t>(), li.as<uint16_t>(), Tl, S)));
     CK(c, samu_count(c, launch_rebase(st.as<uint32_t>(), fin_t.as<double>(), (int64_t)Tl * n, rec(fslot) + tb, (int32_t)n, s)));
     for (const Ent& e : Es) touched[e.node] = true;
     prev = Es;
@@ -1513,6 +1742,10 @@ struct Greedy {
   void new_stage_caches() {
     full_slot.clear();
     cut_slot.clear();
+    slot_class.clear();
+    slot_job.clear();
+    slot_src.clear();
+    have_fin.clear();
     for (auto& kv : fin_buf) fin_pool.push_back(std::move(kv.second));
     fin_buf.clear();
     n_slots = 0;

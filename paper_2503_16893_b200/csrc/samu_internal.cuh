@@ -38,7 +38,7 @@ struct DevEcdf {
 // One candidate (node, plan) as the simulation kernel sees it.
 struct DevCand {
   int32_t node, dp, tp, resume, commit, has_succ;
-  int32_t mode;                // K2 path: 0 general, 2 FRESH (fresh state, no arrivals / cut / outputs), 1 LEAN (FRESH, no successors), 3 / 4 = LEAN / FRESH cut at tau
+  int32_t mode;                // K2 path: 0 general, 2 FRESH (fresh state, no arrivals / cut / outputs), 1 LEAN (FRESH, no successors), 3 / 4 = LEAN / FRESH cut at tau, 5 / 6 = LEAN / FRESH schedule-sharing groups
   uint32_t max_seqs, bs, budget;
   int32_t blocks;              // KV blocks per replica (c5)
   uint32_t L, h_tp;            // layers, h / tp
@@ -81,6 +81,17 @@ struct SimLaunch {
   uint32_t* scratch_idx;       // [n_warps][4][max_p]
   int32_t max_q, max_p;
   int32_t* error;              // first error code (0 = ok), error site
+  // Schedule sharing (K2 modes 5 / 6 = 1 / 2 with groups: fresh state, no time limit).  Candidates of one (node, dp)
+  // that differ only in tp run one event schedule as long as KV blocks never bind below the
+  // largest variant's count: ord entry x then heads a group, grp[x] = (members, 2nd, 3rd, 4th
+  // candidate; fewer blocks), simulated once with per-lane clocks.  A member whose schedule
+  // would differ in a (trial, replica) item goes to the fallback queue fb (candidate, item
+  // within the candidate) and is simulated on its own in the same launch.  fb_ctr: [0]
+  // allocated, [1] claimed, [2] static items finished.  grp == null: no groups.
+  const uint4* grp;
+  uint2* fb;
+  uint32_t* fb_ctr;
+  uint32_t* fb_count;          // [n_cands] fallback items per member candidate (scheduling hints)
 };
 
 // launchers (return cudaError_t of the launch)
@@ -94,13 +105,17 @@ cudaError_t launch_dense_coeff(const double* bucket_B, int32_t nb, const double*
 cudaError_t launch_simulate(const SimLaunch* Ls, const int* modes, const int32_t* n_blocks, int n_launch,
                             const DevCand* host_cands, uint32_t block_size, cudaStream_t s, cudaStream_t s2,
                             cudaEvent_t ev_fork, cudaEvent_t ev_join);
-cudaError_t simulate_prepare(int blocks_per_sm[5]);   // per K2 mode
+#define SAMU_K2_MODES 7   // 0 general, 1 LEAN, 2 FRESH, 3 / 4 LEAN / FRESH cut, 5 / 6 LEAN / FRESH schedule-sharing groups
+cudaError_t simulate_prepare(int blocks_per_sm[SAMU_K2_MODES]);   // per K2 mode
 
 int32_t simulate_smem_bytes(int mode);
 cudaError_t launch_combine(const samu_trial_rec* rep_rec, const DevCand* cands, int32_t n_cands, int32_t n_trials,
                            double* over, int32_t n_nodes, cudaStream_t s);
 cudaError_t launch_summary(const samu_trial_rec* recs, int32_t n_cands, int32_t n_trials,
                            samu_cand_summary* out, cudaStream_t s);
+cudaError_t launch_unpack_gather(const samu_trial_rec* recv, int32_t world, int32_t n, int32_t Tmax, int32_t T,
+                                 int32_t Wt, const int32_t* slots, const int32_t* job_class, samu_trial_rec* dst,
+                                 cudaStream_t s);
 cudaError_t launch_fill_f64(double* p, int64_t n, double v, cudaStream_t s);
 cudaError_t launch_rebase(uint32_t* st, double* fin_t, int64_t n_total, const samu_trial_rec* fstar_rec,
                           int32_t n_req, cudaStream_t s);
