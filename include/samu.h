@@ -196,6 +196,20 @@ int32_t samu_enumerate_plans(samu_ctx* ctx, int32_t node, int32_t* dp, int32_t* 
 samu_status samu_sample_lengths(samu_ctx* ctx, uint64_t seed, int32_t trial_begin, int32_t n_trials,
                                 uint16_t* out_l_out, uint16_t* out_l_in_eff);
 
+/* Output-length sampling of an arbitrary request set of one model (the §8(b) call shape,
+ * P:431-433 "a set of requests per model"): no application needs to be loaded, only
+ * the model's registration and eCDF.  reqs host [n_req]: l_in_base, cap_y, pred (-1, or the
+ * index within this set of a chained predecessor, which must come earlier and have no other
+ * successor; its generated tokens are added to the successor's prompt), node and chain
+ * ignored.  Draw u of request i in trial k = word ((i + index_base) & 3) of
+ * Philox4x32-10(ctr = ((i + index_base) >> 2, k, stream_id, 0), key = seed): with stream_id =
+ * the node id and index_base = the node's first request index this is exactly what
+ * samu_sample_lengths draws for that node.  Device out_l_out / out_l_in_eff [n_trials][n_req].
+ * SAMU_E_INVALID: unregistered model / no eCDF, l_in_base > l_max, bad pred, stream_id >= 2^31. */
+samu_status samu_sample_requests(samu_ctx* ctx, int32_t model_id, uint32_t stream_id, const samu_request* reqs,
+                                 int32_t n_req, uint32_t index_base, uint64_t seed, int32_t trial_begin,
+                                 int32_t n_trials, uint16_t* out_l_out, uint16_t* out_l_in_eff);
+
 /* Known output lengths in place of the sampler (the §5.5 cost-model ablation):
  * host l_true [n_req] (copied before return) -> device out_l_out / out_l_in_eff [1][n_req] with
  * the sampler's clamps and chained-prompt arithmetic.  Synchronises the context stream. */

@@ -88,7 +88,8 @@ ALGOS = {"greedy": 0, "max": 1, "min": 2}
 EXPORTED = ["samu_ctx_create", "samu_ctx_destroy", "samu_local_group_create", "samu_local_group_destroy",
             "samu_ctx_create_local", "samu_last_error", "samu_launch_count", "samu_share_stats", "samu_nccl_unique_id",
             "samu_model_register",
-            "samu_ecdf_load", "samu_app_load", "samu_enumerate_plans", "samu_sample_lengths", "samu_simulate_batch",
+            "samu_ecdf_load", "samu_app_load", "samu_enumerate_plans", "samu_sample_lengths", "samu_sample_requests",
+            "samu_simulate_batch",
             "samu_plan_greedy", "samu_plan_max_heuristic", "samu_plan_min_heuristic", "samu_plan_run", "samu_known_lengths",
             "samu_replay_plan", "samu_fit_coeffs", "samu_plan_free"]
 
@@ -123,6 +124,8 @@ def lib():
         L.samu_enumerate_plans.argtypes = [P, C.c_int32, P, P, C.c_int32]
         L.samu_enumerate_plans.restype = C.c_int32
         L.samu_sample_lengths.argtypes = [P, C.c_uint64, C.c_int32, C.c_int32, P, P]
+        L.samu_sample_requests.argtypes = [P, C.c_int32, C.c_uint32, P, C.c_int32, C.c_uint32, C.c_uint64, C.c_int32,
+                                           C.c_int32, P, P]
         L.samu_simulate_batch.argtypes = [P, P, C.c_int32, P, P, C.c_int32, P, P, P, P, P, P, P, P, P]
         L.samu_plan_greedy.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(C.POINTER(samu_plan))]
         L.samu_plan_max_heuristic.argtypes = [P, C.c_uint64, C.c_int32, C.POINTER(C.POINTER(samu_plan))]
@@ -278,6 +281,20 @@ class Samu:
         else:
             lo, li = out
         self._check(lib().samu_sample_lengths(self.h, seed, trial_begin, n_trials, _t_ptr(lo), _t_ptr(li)))
+        return lo, li
+
+    def samu_sample_requests(self, model_id: int, stream_id: int, l_in_base, cap_y, pred, index_base: int,
+                             seed: int, trial_begin: int, n_trials: int):
+        """One model's request set with its own Philox stream (include/samu.h); pred indexes the set."""
+        torch = self.torch
+        n = len(l_in_base)
+        req = np.zeros(max(n, 1), dtype=np.dtype([("l_in_base", "<u4"), ("cap_y", "<u4"), ("pred", "<i4"),
+                                                  ("node", "<i4"), ("chain", "<i4")]))
+        req["l_in_base"][:n], req["cap_y"][:n], req["pred"][:n] = l_in_base, cap_y, pred
+        lo = torch.empty((n_trials, n), dtype=torch.int16, device=self.device)
+        li = torch.empty((n_trials, n), dtype=torch.int16, device=self.device)
+        self._check(lib().samu_sample_requests(self.h, model_id, stream_id, _np_ptr(req), n, index_base, seed,
+                                               trial_begin, n_trials, _t_ptr(lo), _t_ptr(li)))
         return lo, li
 
     def samu_known_lengths(self, l_true):

@@ -26,13 +26,21 @@ def _nccl_dir():
 def build(force: bool = False, verbose: bool = False) -> str:
     deps = [os.path.join(CSRC, s) for s in SOURCES] + [os.path.join(CSRC, "samu_internal.cuh"),
                                                        os.path.join(ROOT, "include", "samu.h")]
-    if not force and os.path.exists(SO) and os.path.getmtime(SO) >= max(os.path.getmtime(d) for d in deps):
+    # the flags and defines of a build are part of its identity: a variant / debug build (e.g.
+    # SAMU_DEFINES=SAMU_K2_STATS) is never mistaken for the default one
+    defines = os.environ.get("SAMU_DEFINES", "").split()
+    extra = os.environ.get("SAMU_NVCC_EXTRA", "").split()
+    stamp_txt = " ".join(["defines:"] + defines + ["extra:"] + extra)
+    stamp = SO + ".flags"
+    same_flags = os.path.exists(stamp) and open(stamp).read() == stamp_txt
+    if (not force and same_flags and os.path.exists(SO)
+            and os.path.getmtime(SO) >= max(os.path.getmtime(d) for d in deps)):
         return SO
     nccl = _nccl_dir()
     inc = ["-I", os.path.join(nccl, "include")] if nccl else []
     flags = ARCH + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3"] + inc
-    flags += [f"-D{d}" for d in os.environ.get("SAMU_DEFINES", "").split()]
-    flags += os.environ.get("SAMU_NVCC_EXTRA", "").split()   # experiments (scripts/variants.sh)
+    flags += [f"-D{d}" for d in defines]
+    flags += extra   # experiments (scripts/variants.sh)
     build_dir = os.path.join(HERE, "build")
     os.makedirs(build_dir, exist_ok=True)
 
@@ -57,6 +65,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
     os.replace(SO + ".tmp", SO)
+    with open(stamp, "w") as f:
+        f.write(stamp_txt)
     return SO
 
 

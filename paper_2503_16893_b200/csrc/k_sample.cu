@@ -40,7 +40,8 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __global__ void __launch_bounds__(K1_THREADS) k_sample_lengths(DevApp app, DevEcdf e, const int32_t* __restrict__ seq_head,
                                                                int32_t n_seq, uint32_t k0, uint32_t k1, int32_t trial_begin,
                                                                int32_t n_trials, const uint32_t* __restrict__ known,
-                                                               uint16_t* __restrict__ l_out, uint16_t* __restrict__ l_in) {
+                                                               uint16_t* __restrict__ l_out, uint16_t* __restrict__ l_in,
+                                                               uint32_t r_base, int32_t stream) {
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) unsigned long long bar;
   __shared__ uint32_t s_lib[K1_THREADS], s_cap[K1_THREADS];
@@ -102,7 +103,10 @@ __global__ void __launch_bounds__(K1_THREADS) k_sample_lengths(DevApp app, DevEc
       if (known) {   // known output lengths in place of the draw (reading c30)
         X = __ldg(known + r);
       } else {
-        const uint32_t u = philox_word((uint32_t)r, (uint32_t)(trial_begin + k), (uint32_t)nd, k0, k1);
+        // counter (request id, trial, stream): stream = node id (stream >= 0: a request set's own
+        // stream id, request ids offset by r_base; samu_sample_requests)
+        const uint32_t u = philox_word((uint32_t)r + r_base, (uint32_t)(trial_begin + k),
+                                       stream >= 0 ? (uint32_t)stream : (uint32_t)nd, k0, k1);
         // inverse eCDF (c2): the t-th element of the sorted multiset, t = floor(u n / 2^32)
         const uint32_t t = __umulhi(u, __ldg(e.n_obs + m));
         X = (staged && m == bm) ? (uint32_t)tab[t] : (uint32_t)__ldg(e.tab + __ldg(e.tab_off + m) + t);
@@ -164,13 +168,14 @@ __global__ void k_dense_coeff(const double* __restrict__ bucket_B, int32_t nb, c
 
 cudaError_t launch_sample(const DevApp& app, const DevEcdf& e, const int32_t* seq_head, int32_t n_seq,
                           uint64_t seed, int32_t trial_begin, int32_t n_trials, const uint32_t* known,
-                          uint16_t* l_out, uint16_t* l_in, cudaStream_t s) {
+                          uint16_t* l_out, uint16_t* l_in, cudaStream_t s, uint32_t r_base, int32_t stream) {
   if (n_seq == 0 || n_trials == 0) return cudaSuccess;
   cudaError_t err = cudaFuncSetAttribute(k_sample_lengths, cudaFuncAttributeMaxDynamicSharedMemorySize, e.smem_tab_bytes);
   if (err != cudaSuccess) return err;
   dim3 grid((n_seq + K1_THREADS - 1) / K1_THREADS, (n_trials + K1_TRIALS_PER_BLOCK - 1) / K1_TRIALS_PER_BLOCK);
   k_sample_lengths<<<grid, K1_THREADS, e.smem_tab_bytes, s>>>(app, e, seq_head, n_seq, (uint32_t)seed,
-                                                              (uint32_t)(seed >> 32), trial_begin, n_trials, known, l_out, l_in);
+                                                              (uint32_t)(seed >> 32), trial_begin, n_trials, known, l_out, l_in,
+                                                              r_base, stream);
   return cudaGetLastError();
 }
 

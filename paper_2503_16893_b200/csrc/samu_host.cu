@@ -2,6 +2,7 @@
 // batched simulation launches (K1/K2/K3), NCCL trial sharding and the Algorithm 1 control loop
 // whose scoring runs on the device (K4).  No simulation arithmetic runs here.
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <array>
@@ -97,6 +98,10 @@ struct PlanBufs {
   std::vector<DevBuf> fin_pool;
 };
 
+struct RequestSetBufs {
+  DevBuf tab, knots, tab_off, nobs, mnode, lmax, lib, cap, pred, node, succ, cross, heads;
+};
+
 struct samu_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -137,6 +142,7 @@ struct samu_ctx {
   PlanBufs pb;         // planner buffers (borrowed by Greedy / Replay for the duration of a call)
   DevBuf d_cands, d_items, d_counter, d_rep_rec, d_scratch_q, d_scratch_key, d_scratch_idx, d_error, d_fb;
   DevBuf d_sum, d_gather_send, d_gather_recv, d_gather_meta, d_flag;
+  RequestSetBufs rs;   // samu_sample_requests scratch
   int sim_blocks_per_sm[SAMU_K2_MODES] = {};   // resident K2 blocks per SM, per K2 mode
 
   // stats
@@ -240,6 +246,15 @@ static samu_status agree(samu_ctx* c, samu_status local) {
   if (f[1]) FAIL(c, SAMU_E_STATE, "another rank failed in this collective call");
   return SAMU_OK;
 }
+
+// NVTX ranges around the path's steps (K1 sampling, K2 batches, K3 summaries, planner stages):
+// header-only NVTX v3, free when no profiler is attached (SURVEY §5 tracing)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 static inline cudaError_t samu_count(samu_ctx* c, cudaError_t e) {
   c->launches += 1;
@@ -654,6 +669,7 @@ static samu_status replicas(samu_ctx* c, int node, int dp, const uint32_t** off,
 // ---------------------------------------------------------------------------------------------
 static samu_status sample_or_known(samu_ctx* c, uint64_t seed, int32_t trial_begin, int32_t n_trials,
                                    const uint32_t* known_dev, uint16_t* out_l_out, uint16_t* out_l_in_eff) {
+  NvtxRange nv("samu K1 sample_lengths");
   DevApp a = dev_app(c);
   DevEcdf e;
   e.tab = c->d_tab.as<uint16_t>();
@@ -676,6 +692,85 @@ extern "C" samu_status samu_sample_lengths(samu_ctx* c, uint64_t seed, int32_t t
     FAIL(c, SAMU_E_INVALID, "sample_lengths: bad arguments");
   if (n_trials > 65535) FAIL(c, SAMU_E_INVALID, "sample_lengths: at most 65535 trials per call");
   return sample_or_known(c, seed, trial_begin, n_trials, nullptr, out_l_out, out_l_in_eff);
+}
+
+// one model's request set with its own Philox stream (samu.h): a temporary one-node application
+extern "C" samu_status samu_sample_requests(samu_ctx* c, int32_t model_id, uint32_t stream_id, const samu_request* reqs,
+                                           int32_t n_req, uint32_t index_base, uint64_t seed, int32_t trial_begin,
+                                           int32_t n_trials, uint16_t* out_l_out, uint16_t* out_l_in_eff) {
+  GUARD(c);
+  if (model_id < 0 || model_id >= SAMU_MAX_NODES || !c->models[model_id].spec_set || !c->models[model_id].ecdf_set)
+    FAIL(c, SAMU_E_INVALID, "sample_requests: model not registered or no eCDF");
+  if (n_req < 0 || n_trials < 0 || trial_begin < 0 || stream_id >= (1u << 31) || (n_req && !reqs) ||
+      (n_req && n_trials && (!out_l_out || !out_l_in_eff)))
+    FAIL(c, SAMU_E_INVALID, "sample_requests: bad arguments");
+  if (n_trials > 65535) FAIL(c, SAMU_E_INVALID, "sample_requests: at most 65535 trials per call");
+  if ((uint64_t)n_req * (uint64_t)std::max(n_trials, 1) >= (1ull << 32)) FAIL(c, SAMU_E_INVALID, "sample_requests: too large");
+  if (n_req == 0 || n_trials == 0) return SAMU_OK;
+  const ModelReg& M = c->models[model_id];
+  std::vector<uint32_t> lib(n_req), cap(n_req);
+  std::vector<int32_t> pred(n_req), node(n_req, 0), succ(n_req, -1), heads;
+  std::vector<uint8_t> cross(n_req, 0);
+  for (int32_t i = 0; i < n_req; ++i) {
+    const samu_request& q = reqs[i];
+    if (q.l_in_base > M.spec.l_max) FAIL(c, SAMU_E_INVALID, "sample_requests: l_in_base > l_max");
+    if (q.pred >= i || q.pred < -1) FAIL(c, SAMU_E_INVALID, "sample_requests: pred must be -1 or an earlier request");
+    if (q.pred >= 0) {
+      if (succ[q.pred] >= 0) FAIL(c, SAMU_E_INVALID, "sample_requests: two successors of one request");
+      succ[q.pred] = i;
+    } else {
+      heads.push_back(i);
+    }
+    lib[i] = q.l_in_base;
+    cap[i] = q.cap_y;
+    pred[i] = q.pred;
+  }
+  // the model's sorted-multiset table (reading c2), laid out as the app tables with this model's
+  // entries at offset 0
+  const uint32_t nobs = M.ec.back();
+  const int32_t K = (int32_t)M.ev.size();
+  std::vector<int32_t> toff(SAMU_MAX_NODES + 1, 0), mnode{model_id};
+  for (int m = model_id + 1; m <= SAMU_MAX_NODES; ++m) toff[m] = (int32_t)((nobs + 7u) & ~7u);
+  std::vector<uint32_t> nob(SAMU_MAX_NODES, 0), lmax{M.spec.l_max}, knots;
+  nob[model_id] = nobs;
+  knots.insert(knots.end(), M.ev.begin(), M.ev.end());
+  knots.insert(knots.end(), M.ec.begin(), M.ec.end());
+  RequestSetBufs& B = c->rs;
+  cudaStream_t s = c->stream;
+  CK(c, B.tab.ensure(sizeof(uint16_t) * std::max<uint32_t>((nobs + 7u) & ~7u, 8u)));
+  CK(c, upload(B.knots, knots, s));
+  CK(c, samu_count(c, launch_ecdf_table(B.knots.as<uint32_t>(), B.knots.as<uint32_t>() + K, K, nobs, B.tab.as<uint16_t>(), s)));
+  CK(c, upload(B.tab_off, toff, s));
+  CK(c, upload(B.nobs, nob, s));
+  CK(c, upload(B.mnode, mnode, s));
+  CK(c, upload(B.lmax, lmax, s));
+  CK(c, upload(B.lib, lib, s));
+  CK(c, upload(B.cap, cap, s));
+  CK(c, upload(B.pred, pred, s));
+  CK(c, upload(B.node, node, s));
+  CK(c, upload(B.succ, succ, s));
+  CK(c, upload(B.cross, cross, s));
+  CK(c, upload(B.heads, heads, s));
+  DevApp a;
+  a.n_req = n_req;
+  a.n_nodes = 1;
+  a.l_in_base = B.lib.as<uint32_t>();
+  a.cap_y = B.cap.as<uint32_t>();
+  a.pred = B.pred.as<int32_t>();
+  a.node = B.node.as<int32_t>();
+  a.succ = B.succ.as<int32_t>();
+  a.cross = B.cross.as<uint8_t>();
+  DevEcdf e;
+  e.tab = B.tab.as<uint16_t>();
+  e.tab_off = B.tab_off.as<int32_t>();
+  e.n_obs = B.nobs.as<uint32_t>();
+  e.model_of_node = B.mnode.as<int32_t>();
+  e.l_max_of_node = B.lmax.as<uint32_t>();
+  e.smem_tab_bytes = (int32_t)(sizeof(uint16_t) * ((nobs + 7u) & ~7u));
+  CK(c, samu_count(c, launch_sample(a, e, B.heads.as<int32_t>(), (int32_t)heads.size(), seed, trial_begin, n_trials,
+                                    nullptr, out_l_out, out_l_in_eff, s, index_base, (int32_t)stream_id)));
+  CK(c, cudaStreamSynchronize(s));   // the scratch tables are reused by the next call
+  return SAMU_OK;
 }
 
 // host l_true [n_req] -> device scratch (kept in the context until the next call)
@@ -736,6 +831,7 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
                                  int32_t T, const StatePtrs& S);
 static samu_status run_jobs(samu_ctx* c, std::vector<SimJob>& jobs, const uint16_t* l_out, const uint16_t* l_in,
                             int32_t T, const StatePtrs& S) {
+  NvtxRange nv("samu K2 simulate batch");
   if (!trace_on()) return run_jobs_impl(c, jobs, l_out, l_in, T, S);
   const double t0 = now_s();
   const samu_status r = run_jobs_impl(c, jobs, l_out, l_in, T, S);
@@ -1193,6 +1289,7 @@ extern "C" samu_status samu_simulate_batch(samu_ctx* c, const samu_candidate* ca
       RET(gather_records(c, out_recs, n_cands, T_total, c->d_sum.as<samu_trial_rec>(), slots));
       all = c->d_sum.as<samu_trial_rec>();
     }
+    NvtxRange nv("samu K3 summaries");
     CK(c, c->d_cand_sum.ensure(sizeof(samu_cand_summary) * n_cands));
     CK(c, samu_count(c, launch_summary(all, n_cands, T_total, c->d_cand_sum.as<samu_cand_summary>(), c->stream)));
     CK(c, cudaMemcpyAsync(out_summary, c->d_cand_sum.p, sizeof(samu_cand_summary) * n_cands, cudaMemcpyDeviceToHost,
@@ -1769,6 +1866,7 @@ struct Greedy {
       undone_now = undone;
       if (plan->n_stages >= 64) FAIL(c, SAMU_E_STATE, "plan: too many stages");
       new_stage_caches();
+      NvtxRange nv("samu planner stage");
       std::vector<Ent> Es;
       StageOut chosen{};
       if (algo == 0) RET(choose_greedy(unfinished, undone, Es, chosen));

@@ -97,7 +97,7 @@ struct SimLaunch {
 // launchers (return cudaError_t of the launch)
 cudaError_t launch_sample(const DevApp& app, const DevEcdf& e, const int32_t* seq_head, int32_t n_seq,
                           uint64_t seed, int32_t trial_begin, int32_t n_trials, const uint32_t* known,
-                          uint16_t* l_out, uint16_t* l_in, cudaStream_t s);
+                          uint16_t* l_out, uint16_t* l_in, cudaStream_t s, uint32_t r_base = 0, int32_t stream = -1);
 cudaError_t launch_ecdf_table(const uint32_t* values, const uint32_t* cum, int32_t K, uint32_t n, uint16_t* tab,
                               cudaStream_t s);
 cudaError_t launch_dense_coeff(const double* bucket_B, int32_t nb, const double* coeff_slot,

@@ -1,4 +1,7 @@
-"""Event statistics of K2 per application (needs a SAMU_DEFINES=SAMU_K2_STATS build)."""
+"""Event statistics of K2 per node of the C5 first step (needs a SAMU_DEFINES=SAMU_K2_STATS build).
+
+  python scripts/k2_stats.py [T] [node,node,...]   (default: per application)
+"""
 import ctypes as C
 import os
 import sys
@@ -21,7 +24,11 @@ lo, li = S.samu_sample_lengths(w.seed, 0, T)
 f = lib().samu_debug_k2_stats
 f.argtypes = [C.c_void_p, C.c_int]
 buf = (C.c_ulonglong * 16)()
-for name, nodes in (("ensembling", range(0, 6)), ("routing", range(6, 10)), ("chain", [10])):
+if len(sys.argv) > 2:
+    groups = [(f"node {v}", [int(v)]) for v in sys.argv[2].split(",")]
+else:
+    groups = [("ensembling", range(0, 6)), ("routing", range(6, 10)), ("chain", [10])]
+for name, nodes in groups:
     cands = [(v, dp, tp) for v in nodes for (dp, tp) in S.samu_enumerate_plans(v)]
     f(buf, 1)
     out = S.samu_simulate_batch(cands, lo, li)

@@ -363,3 +363,47 @@ def test_local_8_ranks_replay_one_trial(env):
 
     for rp in _run_ranks(8, fn):
         assert rp == ref
+
+
+# ------------------------------------------------------------------------------------------
+# samu_sample_requests: a model's request set with its own stream (the §8(b) call shape)
+# ------------------------------------------------------------------------------------------
+def test_sample_requests_equals_app_sampler_per_node():
+    """Each node's requests sampled as a standalone set (stream = node id, index_base = the
+    node's first index), on a context with models and eCDFs but no application, equal the app
+    sampler's lengths for that node (and the oracle's), chains included."""
+    from paper_2503_16893_b200 import Samu
+    w = W.make_workload("c5", n_prompts=600, n_docs=120, n_trials=5)
+    P = O.Problem(w)
+    lo, li = P.sample(SEED, 2, 5)
+    S = Samu(0)
+    for m, spec in enumerate(w.models):
+        S.samu_model_register(m, spec, w.coeff_B, w.coeff[m], w.load[m])
+        S.samu_ecdf_load(m, w.ecdf_values[m], w.ecdf_cum[m])
+    checked = 0
+    for v in range(w.n_nodes):
+        a, b = w.node_range(v)
+        pred = w.pred[a:b].astype(np.int64)
+        if np.any((pred >= 0) & (pred < a)):
+            continue   # cross-node predecessors are not part of a one-model set
+        rel = np.where(pred >= 0, pred - a, -1)
+        glo, gli = S.samu_sample_requests(int(w.node_model[v]), v, w.l_in_base[a:b], w.cap_y[a:b], rel, a, SEED, 2, 5)
+        assert np.array_equal(u16(glo), lo[:, a:b]) and np.array_equal(u16(gli), li[:, a:b]), v
+        checked += 1
+    assert checked == w.n_nodes - 1
+
+
+def test_sample_requests_rejects_bad_sets():
+    from paper_2503_16893_b200 import Samu, SamuError
+    w = W.make_workload("c1")
+    S = Samu(0)
+    S.samu_model_register(0, w.models[0], w.coeff_B, w.coeff[0], w.load[0])
+    with pytest.raises(SamuError):   # no eCDF yet
+        S.samu_sample_requests(0, 0, [5], [10], [-1], 0, SEED, 0, 1)
+    S.samu_ecdf_load(0, w.ecdf_values[0], w.ecdf_cum[0])
+    with pytest.raises(SamuError):   # pred must be earlier
+        S.samu_sample_requests(0, 0, [5, 6], [10, 10], [1, -1], 0, SEED, 0, 1)
+    with pytest.raises(SamuError):   # two successors
+        S.samu_sample_requests(0, 0, [5, 6, 7], [10, 10, 10], [-1, 0, 0], 0, SEED, 0, 1)
+    with pytest.raises(SamuError):   # l_in above l_max
+        S.samu_sample_requests(0, 0, [w.models[0]["l_max"] + 1], [10], [-1], 0, SEED, 0, 1)
