@@ -1325,40 +1325,29 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, is_lean(MODE) ? SAM
   constexpr bool GRP = MODE == 5 || MODE == 6;
   const bool groups = GRP && P.grp != nullptr;
   for (;;) {
-    // next work: a queued fallback item first (lane 0 claims it), else a static item; with groups
-    // a warp leaves only once every static item has finished and every fallback is claimed
+    // next work: a queued fallback item first (lane 0 claims it), else a static item.  A warp that
+    // queued fallbacks comes back here after its item, so no queued entry is ever left without a
+    // warp to claim it: nobody waits for the others to finish
     uint32_t kind = 1, item = 0, fb_ci = 0;
     if (lane == 0) {
-      if (!groups) {
+      bool got = false;
+      if (groups) {
+        volatile uint32_t* ctr = P.fb_ctr;
+        uint32_t f = ctr[1];
+        while (f < ctr[0]) {
+          const uint32_t old = atomicCAS(P.fb_ctr + 1, f, f + 1);
+          if (old == f) { got = true; break; }
+          f = old;
+        }
+        if (got) {   // allocated entries are written right after their allocation
+          unsigned long long e;
+          do { e = *reinterpret_cast<volatile unsigned long long*>(P.fb + f); } while ((uint32_t)e == SAMU_EMPTY);
+          kind = 2; fb_ci = (uint32_t)e; item = (uint32_t)(e >> 32);
+        }
+      }
+      if (!got) {
         item = atomicAdd(P.next_item, 1u);
         kind = item < (uint32_t)P.n_items ? 1u : 0u;
-      } else {
-        volatile uint32_t* ctr = P.fb_ctr;
-        for (;;) {
-          uint32_t f = ctr[1];
-          bool got = false;
-          while (f < ctr[0]) {
-            const uint32_t old = atomicCAS(P.fb_ctr + 1, f, f + 1);
-            if (old == f) { got = true; break; }
-            f = old;
-          }
-          if (got) {
-            unsigned long long e;
-            do { e = *reinterpret_cast<volatile unsigned long long*>(P.fb + f); } while ((uint32_t)e == SAMU_EMPTY);
-            kind = 2; fb_ci = (uint32_t)e; item = (uint32_t)(e >> 32);
-            break;
-          }
-          if (*reinterpret_cast<volatile uint32_t*>(P.next_item) < (uint32_t)P.n_items) {
-            item = atomicAdd(P.next_item, 1u);
-            if (item < (uint32_t)P.n_items) { kind = 1; break; }
-          }
-          if (ctr[2] >= (uint32_t)P.n_items) {   // no static item left running: no more pushes
-            __threadfence();
-            if (ctr[1] >= ctr[0]) { kind = 0; break; }
-            continue;
-          }
-          __nanosleep(256);
-        }
       }
     }
     kind = __shfl_sync(FULL, kind, 0);
@@ -1381,10 +1370,6 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, is_lean(MODE) ? SAM
       if (groups) grp = __ldg(P.grp + lo_x);
     }
     sim_item<BSK, CONSTC, MODE>(P, W, lane, q, pkey, pidx, ci, rel, grp);
-    if (groups && kind == 1 && lane == 0) {
-      __threadfence();
-      atomicAdd(P.fb_ctr + 2, 1u);
-    }
   }
 }
 

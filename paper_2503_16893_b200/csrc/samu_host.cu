@@ -123,6 +123,7 @@ struct samu_ctx {
   std::vector<int32_t> node_model, node_begin, node_end, node_input, node_has_succ;
   std::vector<samu_request> req;
   std::vector<double> node_exp_out;   // mean expected output tokens of a node's requests (work-item ordering only)
+  std::vector<double> node_mean_lin;  // mean base prompt tokens of a node's requests (work-item ordering only)
   std::vector<int32_t> succ;
   std::vector<uint8_t> cross;
   std::vector<std::vector<int32_t>> waves;
@@ -597,7 +598,11 @@ extern "C" samu_status samu_app_load(samu_ctx* c, const samu_engine_cfg* engine,
   // expected output length per node, E[min(X, cap, l_max - l_in)] with X ~ the model's eCDF
   // (chain inputs taken at their base length): orders K2's work items longest-first
   c->node_exp_out.assign(n_nodes, 1.0);
+  c->node_mean_lin.assign(n_nodes, 0.0);
   for (int v = 0; v < n_nodes; ++v) {
+    double sl = 0.0;
+    for (int r = c->node_begin[v]; r < c->node_end[v]; ++r) sl += (double)c->req[r].l_in_base;
+    if (c->node_end[v] > c->node_begin[v]) c->node_mean_lin[v] = sl / (double)(c->node_end[v] - c->node_begin[v]);
     const ModelReg& M = c->models[node_model[v]];
     if (!M.ecdf_set || c->node_end[v] <= c->node_begin[v]) continue;
     const size_t K = M.ev.size();
@@ -863,6 +868,7 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
     if (idx.empty()) continue;
     std::vector<DevCand> dc(idx.size());
     std::vector<uint64_t> cost(idx.size());
+    std::vector<double> kvf(idx.size(), 1.0);
     uint32_t max_q = 1, max_p = 1;
     for (size_t x = 0; x < idx.size(); ++x) {
       const SimJob& J = jobs[idx[x]];
@@ -904,8 +910,21 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
       for (int j = 0; j < cd.dp; ++j) mx = std::max(mx, ho[j + 1] - ho[j]);
       max_q = std::max(max_q, mx);
       if (c->node_input[node] >= 0 || S.st) max_p = std::max(max_p, mx);
-      cost[x] = (uint64_t)((double)mx * c->node_exp_out[node]);   // replica requests x expected output
+      // replica requests x expected output, x the KV pressure: a replica whose running set would
+      // need more blocks than it has simulates more iterations (preemption, smaller batches)
+      const double tok_r = c->node_mean_lin[node] + c->node_exp_out[node];
+      const double demand = std::min<double>(c->eng.max_num_seqs, mx) * std::ceil(tok_r / c->eng.block_size);
+      kvf[x] = std::max(1.0, demand / std::max<double>(1.0, (double)blocks));
+      cost[x] = (uint64_t)((double)mx * c->node_exp_out[node]);
     }
+    // small trial shares (e.g. one rank of an 8-GPU run): each launch is a few waves and its
+    // longest replica-sims are the critical path, so their order counts the KV pressure too (and
+    // the single candidates join the group launches below)
+    int64_t items_all = 0;
+    for (const DevCand& D : dc) items_all += (int64_t)T * D.dp;
+    const bool small_share = items_all < 24 * (int64_t)c->n_sm * 24;
+    if (small_share)
+      for (size_t x = 0; x < idx.size(); ++x) cost[x] = (uint64_t)((double)cost[x] * kvf[x]);
     // longest-first work items (cand, trial, replica)
     std::vector<int> order(idx.size());
     for (size_t x = 0; x < idx.size(); ++x) order[x] = (int)x;
@@ -945,6 +964,9 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
     auto hint_key = [&](const DevCand& D) { return std::array<int, 4>{D.node, D.dp, D.tp, D.mode}; };
     std::vector<std::vector<int>> groups;   // member lists, head (most blocks) first
     std::vector<bool> non_head(dc.size(), false);
+    // small trial shares: the single candidates join the group launch (as groups of one) instead
+    // of starting after it: one LEAN and one FRESH launch, longest first
+    const bool fold = grouping && small_share;
     if (grouping) {
       std::vector<bool> taken(dc.size(), false);
       for (int x : order) {
@@ -961,13 +983,19 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
         }
         for (size_t g0 = 0; g0 < keep.size(); g0 += 4) {
           const size_t nv = std::min<size_t>(4, keep.size() - g0);
-          if (nv < 2) continue;   // a single member stays on the single-candidate path
+          if (nv < 2 && !fold) continue;   // a single member stays on the single-candidate path
           groups.emplace_back(keep.begin() + g0, keep.begin() + g0 + nv);
           for (size_t i = 0; i < nv; ++i) {
             if (i) non_head[keep[g0 + i]] = true;
             dc[keep[g0 + i]].mode += 4;
           }
         }
+        if (fold)   // excluded members: groups of one in the same launch
+          for (int y : mem)
+            if (std::find(keep.begin(), keep.end(), y) == keep.end()) {
+              groups.push_back({y});
+              dc[y].mode += 4;
+            }
       }
     }
     // per mode: candidate (group head) order and item offsets (the device decodes item ->
@@ -1029,7 +1057,9 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
       size_t n_warps = SAMU_WARPS_PER_BLOCK;   // scratch rings: modes 0, 2, 4, 6 (the LEAN modes use none)
       for (int md = 0; md < SAMU_K2_MODES; ++md) {
         const int64_t want = (n_items[md] + fb_cap[md] + SAMU_WARPS_PER_BLOCK - 1) / SAMU_WARPS_PER_BLOCK;
-        n_blocks[md] = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->n_sm * c->sim_blocks_per_sm[md], want));
+        static const int bcap = std::getenv("SAMU_K2_BPSM_CAP") ? std::atoi(std::getenv("SAMU_K2_BPSM_CAP")) : 0;
+        const int bpsm = bcap > 0 ? std::min(bcap, c->sim_blocks_per_sm[md]) : c->sim_blocks_per_sm[md];
+        n_blocks[md] = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->n_sm * bpsm, want));
         if (md != 1 && md != 3 && md != 5) n_warps = std::max(n_warps, (size_t)n_blocks[md] * SAMU_WARPS_PER_BLOCK);
       }
       CK(c, c->d_scratch_q.ensure(sizeof(uint32_t) * n_warps * max_q));

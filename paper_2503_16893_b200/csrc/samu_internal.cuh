@@ -87,7 +87,7 @@ struct SimLaunch {
   // candidate; fewer blocks), simulated once with per-lane clocks.  A member whose schedule
   // would differ in a (trial, replica) item goes to the fallback queue fb (candidate, item
   // within the candidate) and is simulated on its own in the same launch.  fb_ctr: [0]
-  // allocated, [1] claimed, [2] static items finished.  grp == null: no groups.
+  // allocated, [1] claimed.  grp == null: no groups.
   const uint4* grp;
   uint2* fb;
   uint32_t* fb_ctr;

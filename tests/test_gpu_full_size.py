@@ -407,3 +407,46 @@ def test_sample_requests_rejects_bad_sets():
         S.samu_sample_requests(0, 0, [5, 6, 7], [10, 10, 10], [-1, 0, 0], 0, SEED, 0, 1)
     with pytest.raises(SamuError):   # l_in above l_max
         S.samu_sample_requests(0, 0, [w.models[0]["l_max"] + 1], [10], [-1], 0, SEED, 0, 1)
+
+
+# ------------------------------------------------------------------------------------------
+# a rank-local failure inside a collective call fails every rank (no rank left waiting)
+# ------------------------------------------------------------------------------------------
+_AGREE_CHILD = r"""
+import os, sys, threading
+sys.path.insert(0, os.environ["SAMU_ROOT"])
+import torch
+import samu_workloads as W
+from paper_2503_16893_b200 import LocalGroup, Samu, SamuError
+w = W.make_workload("c2", n_prompts=40, n_trials=8)
+grp = LocalGroup(3)
+res = [None] * 3
+def work(r):
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        S = Samu(0, rank=r, local_group=grp, stream=st)
+        S.load_workload(w)
+        cnt = [2, 3, 3][r]            # 8 trials in all, but not the contiguous split 3 / 3 / 2
+        lo, li = S.samu_sample_lengths(16893, 0, cnt)
+        try:
+            S.samu_simulate_batch([(0, 1, 1)], lo, li, summary=True)
+            res[r] = "ok"
+        except SamuError as e:
+            res[r] = "err:" + str(e)[:80]
+        st.synchronize()
+th = [threading.Thread(target=work, args=(r,)) for r in range(3)]
+[t.start() for t in th]
+[t.join() for t in th]
+print(res)
+"""
+
+
+def test_rank_local_failure_fails_all_ranks():
+    import subprocess
+    import sys
+    env = dict(os.environ, SAMU_ROOT=ROOT)
+    r = subprocess.run([sys.executable, "-c", _AGREE_CHILD], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = r.stdout.strip().splitlines()[-1]
+    assert out.count("err:") == 3, out          # ranks 0 and 2 fail the split check, rank 1 is told
+    assert "another rank failed" in out
