@@ -66,7 +66,7 @@ struct WarpSmT {
   int2 s_fo[SLOTS];          // (decode index at which it finishes, l - d)
   uint32_t s_meta[SLOTS];    // admission rank << 5 | phase  (phase = (o - 1) mod bs)
   uint32_t stk_req[SLOTS];   // preempted stack, top = front of W
-  uint32_t stk_g[SLOTS];
+  uint32_t stk_pr[SLOTS];    // its prompt tokens p = l_in + g (bits 31..16) and tokens still to generate (15..0)
   uint32_t tmp[SMALL ? 1 : SLOTS];    // finished requests of the current iteration / radix histogram
   uint32_t hist[32];         // running requests per phase
   uint32_t adm_req[32], adm_meta[32];
@@ -587,9 +587,28 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
     // window: register cache of the first wn (<= 32) entries of W, circular over the lanes
     // (position i in lane (wb + i) mod 32, so admitting a prefix just advances wb and the admitted
     // requests enter the running set from their own lanes, spread round-robin over all lanes):
-    // request, prompt tokens p = l_in + g, tokens still to generate incl. the prefill's (L - g)
-    // (raw loads kept unconsumed until needed: the window refill does not wait on them)
-    uint32_t w_r = 0, w_li = 0, w_lo = 0, w_g = 0, wn = 0, wb = 0;
+    // request, prompt tokens p = l_in + g, tokens still to generate incl. the prefill's (L - g).
+    // Entries from the preempted stack carry (p, L - g) from shared memory (no global loads).
+    uint32_t w_r = 0, w_p = 0, w_rem = 0, wn = 0, wb = 0;
+    // load window position pos of W (stack top first, then the queue) into this lane
+#define WIN_LOAD(pos)                                                                          \
+    do {                                                                                       \
+      if ((pos) < m.stack_cnt) {                                                               \
+        const uint32_t si_ = m.stack_cnt - 1 - (pos);                                          \
+        w_r = W.stk_req[si_];                                                                  \
+        const uint32_t pr_ = W.stk_pr[si_];                                                    \
+        w_p = pr_ >> 16;                                                                       \
+        w_rem = pr_ & 0xFFFFu;                                                                 \
+      } else {                                                                                 \
+        const uint32_t qp_ = m.q_head + (pos) - m.stack_cnt;                                   \
+        const uint32_t r_ = qr[qp_];                                                           \
+        /* recompute front (reload) keeps its tokens */                                        \
+        const uint32_t g_ = (!FRESH && qp_ < m.n_front) ? (uint32_t)gst[r_] : 0u;              \
+        w_r = r_;                                                                              \
+        w_p = LI_(r_) + g_;                                                                    \
+        w_rem = max((uint32_t)LO_(r_), 1u) - g_;                                               \
+      }                                                                                        \
+    } while (0)
 
     K2STAT(0, 1);
     // ---- main loop (c25) ----
@@ -629,35 +648,81 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
         const uint32_t want = min(32u, wlen);
         if (wn < want) {
           const uint32_t pos = ((uint32_t)lane - wb) & 31u;
-          if (pos >= wn && pos < want) {
-            uint32_t r, g;
-            if (pos < m.stack_cnt) { r = W.stk_req[m.stack_cnt - 1 - pos]; g = W.stk_g[m.stack_cnt - 1 - pos]; }
-            else {
-              const uint32_t qp = m.q_head + pos - m.stack_cnt;
-              r = qr[qp];
-              g = (!FRESH && qp < m.n_front) ? (uint32_t)gst[r] : 0u;   // recompute front keeps its tokens
-            }
-            w_r = r;
-            w_li = LI_(r);
-            w_lo = LO_(r);
-            w_g = g;
-          }
+          if (pos >= wn && pos < want) WIN_LOAD(pos);
           wn = want;
         }
       }
       // does the head of W fit? (slots, token budget, blocks)
-      const uint32_t hp = __shfl_sync(FULL, w_li + w_g, wb);
+      const uint32_t hp = __shfl_sync(FULL, w_p, wb);
       const bool fits = wlen > 0 && m.B < ms && hp <= C.budget && (int32_t)bs.cdiv(hp) <= m.F;
       uint32_t n_fin = 0;
       if (fits) {
         // ================= prefill iteration (c8): admit a strict FCFS prefix of W =========
         uint32_t k_adm = 0, tok = 0, smaxp = 0, S_add = 0, n_stay = 0;
         int32_t blk = 0, freed = 0;
+        bool reduce_fo = true;   // per-lane finish / offset summaries changed in several lanes
+        // Exactly the head enters when one slot is free, one request waits, or the first two do
+        // not fit together (block-bound prefills, e.g. 2k-token chunks): the head fits (above), so
+        // it is admitted alone with warp-uniform arithmetic, no reductions or scans.
+        const uint32_t nb0 = bs.cdiv(hp);
+        bool single = wn <= 1u || m.B + 1u >= ms;
+        if (!single) {
+          const uint32_t p1 = __shfl_sync(FULL, w_p, (wb + 1u) & 31u);
+          single = hp + p1 > C.budget || (int32_t)(nb0 + bs.cdiv(p1)) > m.F;
+        }
+        if (single) {
+          K2STAT(4, 1);
+          const uint32_t rem0 = __shfl_sync(FULL, w_rem, wb);
+          const uint32_t r0 = __shfl_sync(FULL, w_r, wb);
+          k_adm = 1;
+          tok = hp;
+          smaxp = hp;
+          blk = (int32_t)nb0;
+          if (rem0 <= 1u) {   // done in its prefill
+            n_fin = 1;
+            freed = (int32_t)nb0;
+            if (need_rel && lane == 0) W.tmp[0] = r0;
+          } else {
+            n_stay = 1;
+            S_add = hp + 1;
+            const int32_t s_o = (int32_t)(hp + 1) - (int32_t)m.d;
+            const uint32_t s_fin = m.d + rem0 - 1;
+            const uint32_t s_meta = (m.next_rank << 5) | bs.posmod((int32_t)hp - (int32_t)m.d);
+            // into a free slot of the head's lane, else of the first lane with one (B < 256)
+            const uint32_t fl = __ballot_sync(FULL, occ != 0xFFu);
+            const uint32_t tgt = ((fl >> wb) & 1u) ? wb : (uint32_t)(__ffs(fl) - 1);
+            if ((uint32_t)lane == tgt) {
+              const int jb = __ffs(~occ & 0xFFu) - 1;
+              const int s = lane + 32 * jb;
+              W.s_req[s] = r0;
+              W.s_fo[s] = make_int2((int32_t)s_fin, s_o);
+              W.s_meta[s] = s_meta;
+              W.hist[s_meta & 31u] += 1u;
+              occ |= 1u << jb;
+              lminf = min(lminf, s_fin);
+              lmaxo = max(lmaxo, s_o);
+            }
+            m.next_fin = min(m.next_fin, s_fin);
+            m.maxO = max(m.maxO, s_o);
+            reduce_fo = false;
+            __syncwarp();
+          }
+          const uint32_t take = min(1u, m.stack_cnt);
+          m.stack_cnt -= take;
+          m.q_head += 1u - take;
+          wb = (wb + 1u) & 31u;
+          wn -= 1u;
+          const uint32_t want = min(32u, m.stack_cnt + (m.q_tail - m.q_head));
+          if (wn < want) {
+            const uint32_t pos = ((uint32_t)lane - wb) & 31u;
+            if (pos >= wn && pos < want) WIN_LOAD(pos);
+            wn = want;
+          }
+        } else
         for (;;) {
           const uint32_t pos = ((uint32_t)lane - wb) & 31u;   // window position of this lane
           const bool valid = pos < wn;
-          const uint32_t p = valid ? w_li + w_g : 0u;
-          const uint32_t w_rem = max(w_lo, 1u) - w_g;   // tokens still to generate incl. the prefill's
+          const uint32_t p = valid ? w_p : 0u;
           const uint32_t nb = valid ? bs.cdiv(p) : 0u;
           uint32_t mm, add_tok, add_blk;   // admitted count, tokens, blocks
           K2STAT(4, 1);
@@ -798,19 +863,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
           const uint32_t want = min(32u, wl2);
           if (wn < want) {
             const uint32_t pos = ((uint32_t)lane - wb) & 31u;
-            if (pos >= wn && pos < want) {
-              uint32_t r, g;
-              if (pos < m.stack_cnt) { r = W.stk_req[m.stack_cnt - 1 - pos]; g = W.stk_g[m.stack_cnt - 1 - pos]; }
-              else {
-                const uint32_t qp = m.q_head + pos - m.stack_cnt;
-                r = qr[qp];
-                g = (!FRESH && qp < m.n_front) ? (uint32_t)gst[r] : 0u;
-              }
-              w_r = r;
-              w_li = LI_(r);
-              w_lo = LO_(r);
-              w_g = g;
-            }
+            if (pos >= wn && pos < want) WIN_LOAD(pos);
             wn = want;
           }
           if (mm < 32) break;
@@ -833,7 +886,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
         m.B += n_stay;
         m.S += S_add;
         m.next_rank += k_adm;
-        if (n_stay) {
+        if (n_stay && reduce_fo) {
           m.next_fin = __reduce_min_sync(FULL, lminf);
           m.maxO = __reduce_max_sync(FULL, lmaxo);
         }
@@ -998,10 +1051,12 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
               vs = __shfl_sync(FULL, bslot, ol);
             }
             const uint32_t vr = W.s_req[vs];
-            const int32_t vo = W.s_fo[vs].y;
+            const int2 vfo = W.s_fo[vs];
             const uint32_t vph = vmeta & 31u;
-            const uint32_t l = (uint32_t)(vo + (int32_t)m.d);
-            const uint32_t vg = l - (uint32_t)LI_(vr);
+            // recompute: prompt p = l_in + g = its current length l, still to generate (incl. the
+            // recompute prefill's token) L - g = its finish index - d (> 0: it is not due now)
+            const uint32_t l = (uint32_t)(vfo.y + (int32_t)m.d);
+            const uint32_t vrem = (uint32_t)vfo.x - m.d;
             m.F += (int32_t)bs.cdiv(l - 1);
             if (vph == m.needidx) --need;
             __syncwarp();
@@ -1009,7 +1064,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
               occ &= ~(1u << (vs >> 5));
               W.hist[vph] -= 1;
               W.stk_req[m.stack_cnt] = vr;
-              W.stk_g[m.stack_cnt] = vg;
+              W.stk_pr[m.stack_cnt] = (l << 16) | vrem;
               lminf = FULL;
               lmaxo = INT_MIN;
 #pragma unroll
@@ -1022,12 +1077,9 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
             }
             __syncwarp();
             // the victim is the new front of W: shift the window up by one
-            {
-              const uint32_t Lv = max((uint32_t)LO_(vr), 1u);
-              wb = (wb - 1u) & 31u;   // a full window drops its last entry, the lane now at wb
-              if ((uint32_t)lane == wb) { w_r = vr; w_li = l - vg; w_lo = Lv; w_g = vg; }
-              wn = min(wn + 1, 32u);
-            }
+            wb = (wb - 1u) & 31u;   // a full window drops its last entry, the lane now at wb
+            if ((uint32_t)lane == wb) { w_r = vr; w_p = l; w_rem = vrem; }
+            wn = min(wn + 1, 32u);
             m.stack_cnt += 1;
             K2STAT(9, 1);
             m.B -= 1;
@@ -1245,7 +1297,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
       for (uint32_t i = lane; i < m.stack_cnt; i += 32) {
         const uint32_t rq = W.stk_req[i];
         st[rq] = (SAMU_ST_PREEMPTED << 28) | (m.stack_cnt - 1 - i);
-        gst[rq] = (uint16_t)W.stk_g[i];
+        gst[rq] = (uint16_t)((W.stk_pr[i] >> 16) - (uint32_t)LI_(rq));
       }
       const uint32_t qbase = max(m.q_head, m.n_front + W.n_heads);
       for (uint32_t pos = m.q_head + lane; pos < m.q_tail; pos += 32) {
@@ -1289,6 +1341,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
 }
 #undef LO_
 #undef LI_
+#undef WIN_LOAD
 #undef K1_l
 #undef coef_l
 
