@@ -36,12 +36,12 @@
 #endif
 
 #ifdef SAMU_K2_STATS   // debug build only: event counters (scripts/k2_stats.py)
-__device__ unsigned long long g_k2_stats[16];
+__device__ unsigned long long g_k2_stats[32];
 #define K2STAT(i, v) do { if (lane == 0) atomicAdd(&g_k2_stats[i], (unsigned long long)(v)); } while (0)
 extern "C" int samu_debug_k2_stats(unsigned long long* out, int reset) {
   if (cudaMemcpyFromSymbol(out, g_k2_stats, sizeof(g_k2_stats)) != cudaSuccess) return -1;
   if (reset) {
-    unsigned long long z[16] = {0};
+    unsigned long long z[32] = {0};
     if (cudaMemcpyToSymbol(g_k2_stats, z, sizeof(z)) != cudaSuccess) return -1;
   }
   return 0;
@@ -148,7 +148,9 @@ struct Sim {
   // warp-uniform scalar state
   double t, stop;   // stop = min(tau, next ready time of a pending arrival)
   // FLOPs of the completed iterations = L c * a1 + 2 L (h/tp) * a2 (exact, folded into u128 at
-  // the end): a1 = sum of decode B + prefill B s, a2 = sum of decode S + prefill B s^2
+  // the end): a1 = sum of decode B + prefill B s, a2 = sum of decode S + prefill B s^2.  With the
+  // closed-form request-iterations (REQIT_CF) a1 holds only the prefill terms B (s - 1): the
+  // decode B sum is reqit minus the prefills' B
   uint64_t a1, a2, reqit;
   uint32_t iter, d, needidx, B, S, next_fin, next_rank;
   int32_t F, maxO;
@@ -225,17 +227,27 @@ __device__ __forceinline__ uint32_t run_chunks(double& t, const double* __restri
     // FRESH (chain summariser: long runs of small B): 64 iterations per scan (lane j:
     // iterations 2j and 2j + 1), the same exact binade form (only in that instantiation:
     // elsewhere the extra live values cost more than the saved scans)
-    while ((MODE == 2 || MODE == 4 || MODE == 6) && !stopped && m_run - done_it >= 64u) {
+    // (without a stop time the last pass may be partial: 33..64 iterations, the unused ones cost
+    // exactly 0 and leave every partial sum unchanged)
+#ifdef SAMU_K2_NO_CHUNK64P
+    constexpr uint32_t MIN64 = 64u;
+#else
+    constexpr uint32_t MIN64 = NOSTOP ? 33u : 64u;
+#endif
+    while ((MODE == 2 || MODE == 4 || MODE == 6) && !stopped && m_run - done_it >= MIN64) {
       const uint64_t eb = (uint64_t)__double_as_longlong(t) & 0x7FF0000000000000ull;
       if (!(t > 0.0 && eb >= (64ull << 52) && eb < (0x7F0ull << 52))) break;
+      const uint32_t cnt64 = NOSTOP ? min(64u, m_run - done_it) : 64u;
       const uint32_t ja = done_it + 2u * (uint32_t)lane;
       const uint32_t Sa = S0 + B * ja, Sb = Sa + B;
-      const double c0 = __dadd_rn(__dadd_rn(__fma_rn(ac, __ull2double_rn(K0 + (uint64_t)K1 * Sa), bc),
-                                            __fma_rn(ap, __uint2double_rn(B * (smax0 + ja)), bp)),
-                                  __fma_rn(as_, __uint2double_rn(Sa), bs_));
-      const double c1 = __dadd_rn(__dadd_rn(__fma_rn(ac, __ull2double_rn(K0 + (uint64_t)K1 * Sb), bc),
-                                            __fma_rn(ap, __uint2double_rn(B * (smax0 + ja + 1u)), bp)),
-                                  __fma_rn(as_, __uint2double_rn(Sb), bs_));
+      const double c0v = __dadd_rn(__dadd_rn(__fma_rn(ac, __ull2double_rn(K0 + (uint64_t)K1 * Sa), bc),
+                                             __fma_rn(ap, __uint2double_rn(B * (smax0 + ja)), bp)),
+                                   __fma_rn(as_, __uint2double_rn(Sa), bs_));
+      const double c1v = __dadd_rn(__dadd_rn(__fma_rn(ac, __ull2double_rn(K0 + (uint64_t)K1 * Sb), bc),
+                                             __fma_rn(ap, __uint2double_rn(B * (smax0 + ja + 1u)), bp)),
+                                   __fma_rn(as_, __uint2double_rn(Sb), bs_));
+      const double c0 = (!NOSTOP || 2u * (uint32_t)lane < cnt64) ? c0v : 0.0;
+      const double c1 = (!NOSTOP || 2u * (uint32_t)lane + 1u < cnt64) ? c1v : 0.0;
       const double r0 = __dsub_rn(__dadd_rn(t, c0), t), r1 = __dsub_rn(__dadd_rn(t, c1), t);
       const double e0 = __dsub_rn(c0, r0), e1 = __dsub_rn(c1, r1);
       const double halfu = __longlong_as_double((long long)(eb - (53ull << 52)));
@@ -264,7 +276,7 @@ __device__ __forceinline__ uint32_t run_chunks(double& t, const double* __restri
         stopped = true;
       } else {
         t = __shfl_sync(FULL, acc_b, 31);
-        done_it += 64u;
+        done_it += cnt64;
       }
     }
     while (done_it < m_run && !stopped) {
@@ -360,6 +372,14 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
                                          uint32_t* pidx, const uint32_t ci, const uint32_t rel, const uint4 grp) {
   constexpr bool LEAN = is_lean(MODE), FRESH = MODE != 0, CUT = MODE == 3 || MODE == 4;
   constexpr bool GRP = MODE == 5 || MODE == 6;   // schedule sharing across a (node, dp) group's tp variants
+  // Request-iterations in closed form: without a time limit every request of the replica runs to
+  // completion, and every iteration it takes part in emits one of its tokens (recompute prefills
+  // included, c7), so the sum over iterations of B is the sum of the replica's max(l_out, 1)
+#ifdef SAMU_K2_REQIT_LIVE
+  constexpr bool REQIT_CF = false;
+#else
+  constexpr bool REQIT_CF = MODE == 1 || MODE == 2 || MODE == 5 || MODE == 6;
+#endif
   const DevApp& A = P.app;
   const int n = A.n_req;
     const DevCand& C = CONSTC ? c_cands[ci] : P.cands[ci];
@@ -878,9 +898,9 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
         const uint64_t fl = (LC + (uint64_t)K1_l * smaxp) * Bs32;
         const double lat = iter_cost(coef_l, k_adm, fl, Bs32, tok);
         m.t = __dadd_rn(m.t, lat);
-        m.a1 += Bs32;
+        m.a1 += REQIT_CF ? Bs32 - k_adm : Bs32;   // (closed form: the decode part of a1 is reqit minus the prefills' B)
         m.a2 += (uint64_t)Bs32 * smaxp;
-        m.reqit += k_adm;
+        if (!REQIT_CF) m.reqit += k_adm;
         m.iter += 1;
         m.F += freed;
         m.B += n_stay;
@@ -902,9 +922,9 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
           const uint32_t smax = (uint32_t)((int32_t)m.d + m.maxO);
           const uint64_t fl = LC * B1 + (uint64_t)K1_l * m.S;
           m.t = __dadd_rn(m.t, iter_cost(coef_l, B1, fl, B1 * smax, m.S));
-          m.a1 += B1;
+          if (!REQIT_CF) m.a1 += B1;
           m.a2 += m.S;
-          m.reqit += B1;
+          if (!REQIT_CF) m.reqit += B1;
           m.iter += 1;
           m.F -= (int32_t)need1;
           if (GRP) W.minF = min(W.minF, m.F);
@@ -914,14 +934,25 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
         } else {
         K2STAT(7, 1);
         const uint32_t B = m.B;
-        const double stop_t = m.stop;
+        // no time limit and no arrivals in modes 1, 2, 5, 6: the stop time is a compile-time +inf
+        const double stop_t = (MODE == 1 || MODE == 2 || MODE == 5 || MODE == 6) ? CUDART_INF : m.stop;
         // KV need of the run's decodes: histogram rotated to start at needidx, prefix sums
         const uint32_t hv = (uint32_t)lane < bs.v() ? W.hist[bs.mod(m.needidx + bs.v() - (uint32_t)lane)] : 0u;
         const uint32_t m_fin = m.next_fin - m.d;
         uint32_t i_pre = 0x7fffffffu;   // first run iteration that must preempt
         uint32_t pre = 0;
         // each bs decodes need exactly B blocks: no search (and no scan) when the run cannot run out
-        const bool tight = (uint32_t)m.F < B * (bs.div(m_fin) + 1u);   // <= 256 * (65535 + 1): 32 bits
+        bool tight = (uint32_t)m.F < B * (bs.div(m_fin) + 1u);   // <= 256 * (65535 + 1): 32 bits
+#ifndef SAMU_K2_NO_TIGHT2
+        // (LEAN only: on the chain summariser's FRESH path most runs that fail the first test also
+        // preempt, and the extra reduction measured slower)
+        if (LEAN && tight) {
+          // the exact need of the whole run (full cycles of B blocks + its first m_fin mod bs
+          // phases) is non-decreasing in the decode count: no preemption if it fits
+          const uint32_t rf = bs.mod(m_fin);
+          tight = bs.div(m_fin) * B + __reduce_add_sync(FULL, (uint32_t)lane < rf ? hv : 0u) > (uint32_t)m.F;
+        }
+#endif
         if (tight) {
           pre = warp_incl_scan(hv, lane);
           {
@@ -940,6 +971,11 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
         }
         const uint32_t m_run = min(m_fin, i_pre);
         uint32_t done_it = 0;
+        // run-length histogram (1, 2-4, 5-8, 9-16, 17-32, 33-64, 65-128, > 128), runs ending in a
+        // preemption, runs that took the preemption search
+        K2STAT(16 + (m_run <= 1 ? 0 : m_run <= 4 ? 1 : m_run <= 8 ? 2 : m_run <= 16 ? 3 : m_run <= 32 ? 4 : m_run <= 64 ? 5 : m_run <= 128 ? 6 : 7), 1);
+        K2STAT(24, i_pre < m_fin ? 1 : 0);
+        K2STAT(25, tight ? 1 : 0);
         if (m_run > 0) {
           const uint64_t K0 = LC * B;
           const uint32_t smax0 = (uint32_t)((int32_t)m.d + m.maxO);
@@ -1003,9 +1039,9 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
           // so mm (mm - 1) fits 32 bits and every product is one widening 32 x 32 multiply
           const uint32_t mm = done_it;
           const uint64_t Bmm = (uint64_t)B * mm;
-          m.a1 += Bmm;
+          if (!REQIT_CF) m.a1 += Bmm;
           m.a2 += (uint64_t)mm * m.S + (uint64_t)B * ((mm * (mm - 1u)) >> 1);
-          m.reqit += Bmm;
+          if (!REQIT_CF) m.reqit += Bmm;
           m.iter += done_it;
           const uint32_t rr = bs.mod(done_it);
           const uint32_t need_rr = rr == 0 ? 0u
@@ -1065,15 +1101,22 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
               W.hist[vph] -= 1;
               W.stk_req[m.stack_cnt] = vr;
               W.stk_pr[m.stack_cnt] = (l << 16) | vrem;
-              lminf = FULL;
-              lmaxo = INT_MIN;
+              // the lane's summaries change only if the victim held one of them
+#ifdef SAMU_K2_NO_LAZYV
+              if (true) {
+#else
+              if ((uint32_t)vfo.x == lminf || vfo.y == lmaxo) {
+#endif
+                lminf = FULL;
+                lmaxo = INT_MIN;
 #pragma unroll
-              for (int jj = 0; jj < 8; ++jj)
-                if ((occ >> jj) & 1u) {
-                  const int2 fo = W.s_fo[lane + 32 * jj];
-                  lminf = min(lminf, (uint32_t)fo.x);
-                  lmaxo = max(lmaxo, fo.y);
-                }
+                for (int jj = 0; jj < 8; ++jj)
+                  if ((occ >> jj) & 1u) {
+                    const int2 fo = W.s_fo[lane + 32 * jj];
+                    lminf = min(lminf, (uint32_t)fo.x);
+                    lmaxo = max(lmaxo, fo.y);
+                  }
+              }
             }
             __syncwarp();
             // the victim is the new front of W: shift the window up by one
@@ -1097,9 +1140,9 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
           const uint64_t fl = LC * B2 + (uint64_t)K1_l * m.S;
           const double lat = iter_cost(coef_l, B2, fl, B2 * smax, m.S);
           m.t = __dadd_rn(m.t, lat);
-          m.a1 += B2;
+          if (!REQIT_CF) m.a1 += B2;
           m.a2 += m.S;
-          m.reqit += B2;
+          if (!REQIT_CF) m.reqit += B2;
           m.iter += 1;
           m.S += B2;
           m.d += 1;
@@ -1207,7 +1250,15 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
       // ---- finish records + chain successor release (c19), for this iteration's finishers ----
       if (!LEAN && n_fin && need_rel) {
         const uint32_t itx = m.iter - 1;
-        if (n_fin <= 32) {
+        if (FRESH && n_fin == 1) {
+          // one finisher (FRESH: no outputs): its successor, if any, joins the back of W
+          const int32_t sr = C.has_succ ? __ldg(A.succ + W.tmp[0]) : -1;
+          if (sr >= 0) {
+            if (lane == 0) q[m.q_tail] = (uint32_t)sr;
+            m.q_tail += 1;
+          }
+          __syncwarp();
+        } else if (n_fin <= 32) {
           // one finisher per lane; released successors ranked in registers (index order, c19)
           const bool v = (uint32_t)lane < n_fin;
           const uint32_t r = v ? W.tmp[lane] : 0u;
@@ -1308,6 +1359,15 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
       }
       if (over && lane == 0) over[j] = (done || !cut) ? 0.0 : __dsub_rn(m.t, W.tau);
     }
+    uint64_t reqit_cf = 0;
+    if (REQIT_CF) {
+      uint64_t sl = 0;
+      for (uint32_t i = r0 + (uint32_t)lane; i < r1; i += 32) sl += max((uint32_t)LO_(__ldg(C.rep_req + i)), 1u);
+      // in 24-bit digits (32 lanes x (2^24 - 1) fits a 32-bit reduction)
+      reqit_cf = (uint64_t)__reduce_add_sync(FULL, (uint32_t)(sl & 0xFFFFFFu)) +
+                 ((uint64_t)__reduce_add_sync(FULL, (uint32_t)((sl >> 24) & 0xFFFFFFu)) << 24) +
+                 ((uint64_t)__reduce_add_sync(FULL, (uint32_t)(sl >> 48)) << 48);
+    }
     // lane v < nv writes member v's record (lane 0 alone without groups), or queues the member's
     // item for a simulation of its own when its schedule would have differed from the head's
     const uint32_t nv = GRP ? W.nv : 1u;
@@ -1318,14 +1378,15 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
         samu_trial_rec rec;
         rec.t_end = m.t;
         {   // FLOPs = LC a1 + K1 a2 in u128
-          uint64_t lo = LC * m.a1, hi = __umul64hi(LC, m.a1);
+          const uint64_t a1 = REQIT_CF ? m.a1 + reqit_cf : m.a1;
+          uint64_t lo = LC * a1, hi = __umul64hi(LC, a1);
           const uint64_t plo = (uint64_t)K1_l * m.a2, phi = __umul64hi((uint64_t)K1_l, m.a2);
           lo += plo;
           hi += phi + (lo < plo ? 1ull : 0ull);
           rec.flops_lo = lo;
           rec.flops_hi = hi;
         }
-        rec.req_iters = m.reqit;
+        rec.req_iters = REQIT_CF ? reqit_cf : m.reqit;
         rec.iters = m.iter;
         rec.flags = (done ? 1u : 0u) | (cut ? 2u : 0u) | (all_done ? 4u : 0u);
         P.rep_rec[((size_t)my_ci * P.n_trials + k) * 16 + j] = rec;
