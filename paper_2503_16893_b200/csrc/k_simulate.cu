@@ -590,6 +590,9 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
 #define K1_l (GRP ? W.vK1[lane] : K1)
 #define coef_l (GRP ? W.vcoef[lane] : C.coef)
     const uint64_t LC = C.LC;   // L c
+    // phase whose requests need a new KV block at the next decode: -d mod bs (phase = (l - 1 - d)
+    // mod bs, fixed at admission); kept in a register only for the general block size
+#define NEEDIDX (BSK >= 0 ? ((0u - m.d) & bs.mask()) : m.needidx)
     const bool need_rel = LEAN ? false : FRESH ? (bool)C.has_succ : (fio || fto || commit || C.has_succ);
     bool cut = false;
     // per-lane summaries of this lane's slots: min finish index, max (l - d)
@@ -753,12 +756,11 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
             add_tok = p0;
             add_blk = bs.cdiv(p0);
             mm = (wn > 0 && m.B + k_adm < ms && tok + p0 <= C.budget && (int32_t)(blk + add_blk) <= m.F) ? 1u : 0u;
-          } else if (__reduce_add_sync(FULL, p) + tok <= C.budget &&
-                     (int32_t)(__reduce_add_sync(FULL, nb) + blk) <= m.F) {
-            // the whole window fits the token and block budgets: only the slots bind, no scans
+          } else if ((add_tok = __reduce_add_sync(FULL, pos < slots ? p : 0u)) + tok <= C.budget &&
+                     (int32_t)((add_blk = __reduce_add_sync(FULL, pos < slots ? nb : 0u)) + blk) <= m.F) {
+            // the first `slots` entries fit the token and block budgets together: only the slots
+            // bind (the FCFS prefix is limited by them), no scans
             mm = slots;
-            add_tok = __reduce_add_sync(FULL, pos < mm ? p : 0u);
-            add_blk = __reduce_add_sync(FULL, pos < mm ? nb : 0u);
           } else if (const uint32_t p01 = __shfl_sync(FULL, p, wb) + __shfl_sync(FULL, p, (wb + 1u) & 31u),
                                     b01 = __shfl_sync(FULL, nb, wb) + __shfl_sync(FULL, nb, (wb + 1u) & 31u);
                      tok + p01 > C.budget || (int32_t)(blk + b01) > m.F) {
@@ -913,7 +915,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
       } else {
         if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; if (lane == 0) W.site = 9; break; }
         // ================= decode run (c9): uniform iterations until an event ===============
-        const uint32_t need1 = W.hist[m.needidx];
+        const uint32_t need1 = W.hist[NEEDIDX];
         if (m.next_fin == m.d + 1 && (int32_t)need1 <= m.F) {
           K2STAT(6, 1);
           // one decode that retires requests and needs no preemption: the run below with
@@ -930,14 +932,14 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
           if (GRP) W.minF = min(W.minF, m.F);
           m.S += B1;
           m.d += 1;
-          m.needidx = m.needidx == 0 ? bs.v() - 1 : m.needidx - 1;
+          if (BSK < 0) m.needidx = m.needidx == 0 ? bs.v() - 1 : m.needidx - 1;
         } else {
         K2STAT(7, 1);
         const uint32_t B = m.B;
         // no time limit and no arrivals in modes 1, 2, 5, 6: the stop time is a compile-time +inf
         const double stop_t = (MODE == 1 || MODE == 2 || MODE == 5 || MODE == 6) ? CUDART_INF : m.stop;
         // KV need of the run's decodes: histogram rotated to start at needidx, prefix sums
-        const uint32_t hv = (uint32_t)lane < bs.v() ? W.hist[bs.mod(m.needidx + bs.v() - (uint32_t)lane)] : 0u;
+        const uint32_t hv = (uint32_t)lane < bs.v() ? W.hist[bs.mod(NEEDIDX + bs.v() - (uint32_t)lane)] : 0u;
         const uint32_t m_fin = m.next_fin - m.d;
         uint32_t i_pre = 0x7fffffffu;   // first run iteration that must preempt
         uint32_t pre = 0;
@@ -1052,11 +1054,11 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
           if (GRP) W.minF = min(W.minF, m.F);
           m.S += B * done_it;
           m.d += done_it;
-          m.needidx = bs.mod(m.needidx + bs.v() - rr);
+          if (BSK < 0) m.needidx = bs.mod(m.needidx + bs.v() - rr);
         }
         if (m.d != m.next_fin && done_it == i_pre && !(done_it > 0 && m.t >= stop_t)) {
           // ---- this decode must preempt (c7): recompute the last admitted requests ----
-          uint32_t need = W.hist[m.needidx];
+          uint32_t need = W.hist[NEEDIDX];
           if (GRP && (int32_t)need > m.F) W.minF = INT_MIN;
           while ((int32_t)need > m.F) {
             uint32_t vmeta;
@@ -1094,7 +1096,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
             const uint32_t l = (uint32_t)(vfo.y + (int32_t)m.d);
             const uint32_t vrem = (uint32_t)vfo.x - m.d;
             m.F += (int32_t)bs.cdiv(l - 1);
-            if (vph == m.needidx) --need;
+            if (vph == NEEDIDX) --need;
             __syncwarp();
             if (lane == ol) {
               occ &= ~(1u << (vs >> 5));
@@ -1146,7 +1148,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
           m.iter += 1;
           m.S += B2;
           m.d += 1;
-          m.needidx = m.needidx == 0 ? bs.v() - 1 : m.needidx - 1;
+          if (BSK < 0) m.needidx = m.needidx == 0 ? bs.v() - 1 : m.needidx - 1;
         }
         }
         if (m.d == m.next_fin) {
@@ -1403,6 +1405,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
 #undef LO_
 #undef LI_
 #undef WIN_LOAD
+#undef NEEDIDX
 #undef K1_l
 #undef coef_l
 
