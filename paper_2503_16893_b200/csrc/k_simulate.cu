@@ -635,7 +635,12 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
 
     K2STAT(0, 1);
     // ---- main loop (c25) ----
+    // (every error site inside the loop breaks out of it: the error code is not a loop condition)
+#ifdef SAMU_K2_ERR_LOOP
     while (!m.err) {
+#else
+    if (!m.err) for (;;) {
+#endif
       K2STAT(1, 1);
       if (CUT && m.t >= m.stop) { cut = true; break; }   // no arrivals in these modes: stop = tau
       if (!FRESH && m.t >= m.stop) {   // stop time or a pending arrival reached

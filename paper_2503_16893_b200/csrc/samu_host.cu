@@ -55,6 +55,22 @@ struct ModelReg {
   std::vector<double> coeff;   // [5][3][2][nb]
   std::vector<double> load;    // [5][16]
   std::vector<uint32_t> ev, ec;
+  // FNV-1a fingerprint of the registration and the eCDF (schedule-sharing hints, samu_app_load)
+  uint64_t fingerprint() const {
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&h](uint64_t x) {
+      for (int i = 0; i < 8; ++i) { h ^= (x >> (8 * i)) & 0xFFu; h *= 1099511628211ull; }
+    };
+    mix(spec.n_layers); mix(spec.hidden); mix(spec.c); mix(spec.l_max); mix(spec.tp_mask);
+    mix(spec.weight_bytes); mix(spec.kv_bytes_per_token);
+    auto mixd = [&mix](double x) { uint64_t u; std::memcpy(&u, &x, 8); mix(u); };
+    for (uint32_t b : bucket_B) mix(b);
+    for (double x : coeff) mixd(x);
+    for (double x : load) mixd(x);
+    for (uint32_t x : ev) mix(x);
+    for (uint32_t x : ec) mix(x);
+    return h;
+  }
 };
 
 int log2_exact(uint32_t x) {
@@ -153,6 +169,9 @@ struct samu_ctx {
   // schedule-sharing hints: (node, dp, tp, mode) -> fraction of the member's items that fell out of
   // sync in its last grouped batch (reset by samu_app_load)
   std::map<std::array<int, 4>, double> share_hint;
+  // the hints belong to one application: a fingerprint of the loaded app (engine, node models'
+  // registrations, requests); reloading the same app keeps them
+  uint64_t hint_app = 0;
   uint64_t req_iters = 0;
 };
 
@@ -619,7 +638,25 @@ extern "C" samu_status samu_app_load(samu_ctx* c, const samu_engine_cfg* engine,
     c->node_exp_out[v] = std::max(1.0, acc / (double)(c->node_end[v] - c->node_begin[v]));
   }
   c->app_loaded = true;
-  c->share_hint.clear();
+  {   // FNV-1a over the fields (no struct padding)
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&h](uint64_t x) {
+      for (int i = 0; i < 8; ++i) { h ^= (x >> (8 * i)) & 0xFFu; h *= 1099511628211ull; }
+    };
+    mix(e.max_num_seqs); mix(e.block_size); mix(e.min_batched_tokens); mix(e.mem_util_permille);
+    mix(e.mem_bytes_per_gpu); mix(e.kv_cap_bytes_per_gpu); mix(e.n_gpus);
+    mix((uint64_t)n_nodes);
+    for (int v = 0; v < n_nodes; ++v) {
+      mix((uint64_t)(uint32_t)node_model[v]);
+      mix(c->models[node_model[v]].fingerprint());
+    }
+    mix((uint64_t)n_req);
+    for (const samu_request& q : c->req) {
+      mix(q.l_in_base); mix(q.cap_y); mix((uint32_t)q.pred); mix((uint32_t)q.node); mix((uint32_t)q.chain);
+    }
+    if (h != c->hint_app) c->share_hint.clear();
+    c->hint_app = h;
+  }
   return SAMU_OK;
 }
 
