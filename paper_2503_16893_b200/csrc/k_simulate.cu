@@ -152,7 +152,7 @@ struct Sim {
   // closed-form request-iterations (REQIT_CF) a1 holds only the prefill terms B (s - 1): the
   // decode B sum is reqit minus the prefills' B
   uint64_t a1, a2, reqit;
-  uint32_t iter, d, needidx, B, S, next_fin, next_rank;
+  uint32_t iter, d, needidx, B, S, next_fin, next_rank;   // iter: prefill iterations (decodes: d)
   int32_t F, maxO;
   uint32_t stack_cnt, q_head, q_tail, n_front;
   int32_t err;
@@ -932,7 +932,6 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
           if (!REQIT_CF) m.a1 += B1;
           m.a2 += m.S;
           if (!REQIT_CF) m.reqit += B1;
-          m.iter += 1;
           m.F -= (int32_t)need1;
           if (GRP) W.minF = min(W.minF, m.F);
           m.S += B1;
@@ -966,10 +965,14 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
             const uint32_t F0 = (uint32_t)m.F;
             // q0 = F0 / B from an fp32 estimate corrected by the remainder (F0 < B (l_max / bs + 1)
             // here, so the estimate is within one of the quotient)
-            uint32_t q0 = __float2uint_rz(__fdividef((float)F0, (float)B));
-            int32_t rs = (int32_t)(F0 - q0 * B);
-            while (rs < 0) { --q0; rs += (int32_t)B; }
-            while (rs >= (int32_t)B) { ++q0; rs -= (int32_t)B; }
+            uint32_t q0 = 0;
+            int32_t rs = (int32_t)F0;
+            if (F0 >= B) {   // (KV-bound runs mostly have fewer free blocks than requests)
+              q0 = __float2uint_rz(__fdividef((float)F0, (float)B));
+              rs = (int32_t)(F0 - q0 * B);
+              while (rs < 0) { --q0; rs += (int32_t)B; }
+              while (rs >= (int32_t)B) { ++q0; rs -= (int32_t)B; }
+            }
             const uint32_t rem = (uint32_t)rs;
             const uint32_t bad = __ballot_sync(FULL, (uint32_t)lane < bs.v() && pre > rem);
             const uint64_t ip = (uint64_t)q0 * bs.v() + (uint32_t)(__ffs(bad) - 1);
@@ -1049,7 +1052,6 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
           if (!REQIT_CF) m.a1 += Bmm;
           m.a2 += (uint64_t)mm * m.S + (uint64_t)B * ((mm * (mm - 1u)) >> 1);
           if (!REQIT_CF) m.reqit += Bmm;
-          m.iter += done_it;
           const uint32_t rr = bs.mod(done_it);
           const uint32_t need_rr = rr == 0 ? 0u
                                    : tight ? __shfl_sync(FULL, pre, rr - 1)
@@ -1150,7 +1152,6 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
           if (!REQIT_CF) m.a1 += B2;
           m.a2 += m.S;
           if (!REQIT_CF) m.reqit += B2;
-          m.iter += 1;
           m.S += B2;
           m.d += 1;
           if (BSK < 0) m.needidx = m.needidx == 0 ? bs.v() - 1 : m.needidx - 1;
@@ -1256,7 +1257,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
       }
       // ---- finish records + chain successor release (c19), for this iteration's finishers ----
       if (!LEAN && n_fin && need_rel) {
-        const uint32_t itx = m.iter - 1;
+        const uint32_t itx = m.iter + m.d - 1;   // iterations = prefills + decodes
         if (FRESH && n_fin == 1) {
           // one finisher (FRESH: no outputs): its successor, if any, joins the back of W
           const int32_t sr = C.has_succ ? __ldg(A.succ + W.tmp[0]) : -1;
@@ -1394,7 +1395,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
           rec.flops_hi = hi;
         }
         rec.req_iters = REQIT_CF ? reqit_cf : m.reqit;
-        rec.iters = m.iter;
+        rec.iters = m.iter + m.d;
         rec.flags = (done ? 1u : 0u) | (cut ? 2u : 0u) | (all_done ? 4u : 0u);
         P.rep_rec[((size_t)my_ci * P.n_trials + k) * 16 + j] = rec;
       } else if (GRP) {
@@ -1428,7 +1429,9 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
 // A launch holds only items of one MODE (DevCand::mode); the host issues one launch per mode
 // present (one kernel holding several paths is slower: a multiple of the code footprint).
 template <int BSK, bool CONSTC, int MODE>
-__global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK, is_lean(MODE) ? SAMU_K2_MINB_LEAN : SAMU_K2_MINB)
+// (the minimum block counts are per 4-warp block: the register caps stay the same for any block size)
+__global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK,
+                                  (is_lean(MODE) ? SAMU_K2_MINB_LEAN : SAMU_K2_MINB) * 4 / SAMU_WARPS_PER_BLOCK)
     k_simulate(SimLaunch P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // lane id kept in a register: an opaque copy cannot be rematerialised from SR_TID (an S2R
