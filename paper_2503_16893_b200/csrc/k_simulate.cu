@@ -59,8 +59,9 @@ constexpr int SLOTS = 256;
 // shared block and the LEAN launch bounds
 __host__ __device__ constexpr bool is_lean(int mode) { return mode == 1 || mode == 3 || mode == 5; }
 
-// SMALL (LEAN launches): no finish / release lists, 2 KB less, so 28 warps fit an SM
-template <bool SMALL>
+// SMALL (LEAN launches): no finish / release lists, 2 KB less, so 28 warps fit an SM; GRP
+// (schedule-sharing launches, modes 5 / 6): the group members' tables
+template <bool SMALL, bool GRP>
 struct WarpSmT {
   uint32_t s_req[SLOTS];     // request id of an occupied slot
   int2 s_fo[SLOTS];          // (decode index at which it finishes, l - d)
@@ -69,12 +70,18 @@ struct WarpSmT {
   uint32_t stk_pr[SLOTS];    // its prompt tokens p = l_in + g (bits 31..16) and tokens still to generate (15..0)
   uint32_t tmp[SMALL ? 1 : SLOTS];    // finished requests of the current iteration / radix histogram
   uint32_t hist[32];         // running requests per phase
-  uint32_t adm_req[32], adm_meta[32];
+  // admission exchange / retirement lane tables, and the per-iteration costs of a decode-run
+  // chunk (lane j = iteration j): never live in the same event, so they share their storage
+  union {
+    struct {
+      uint32_t adm_req[32], adm_meta[32];
+    };
+    double cbuf[32];
+  };
   int2 adm_fo[32];
-  double cbuf[32];           // per-iteration costs of a decode-run chunk (lane j = iteration j)
-  const double* vcoef[32];   // schedule sharing: lane v's member's dense coefficients and 2 L (h/tp),
-  uint32_t vK1[32];          // candidate index, and the group size
-  uint32_t vci[32];
+  const double* vcoef[GRP ? 32 : 1];   // schedule sharing: lane v's member's dense coefficients and
+  uint32_t vK1[GRP ? 32 : 1];          // 2 L (h/tp), candidate index, and the group size
+  uint32_t vci[GRP ? 32 : 1];
   uint32_t nv;
   int32_t minF;              // minimum free KV blocks so far (INT_MIN once a preemption happened)
   // warp-uniform state off the hot path (kept out of registers); every lane writes the same
@@ -85,7 +92,6 @@ struct WarpSmT {
   uint32_t pend_ptr, n_pend, n_heads;
   int32_t site;
 };
-using WarpSm = WarpSmT<false>;
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
@@ -368,7 +374,7 @@ __constant__ DevCand c_cands[SAMU_K2_CONST_CANDS];
 // ensembling / routing nodes) — the queue is then the replica's request list itself.  Fewer live
 // registers: ~10 % faster on those items.
 template <int BSK, bool CONSTC, int MODE>
-__device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MODE)>& W, const int lane, uint32_t* q, uint64_t* pkey,
+__device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MODE), (MODE == 5 || MODE == 6)>& W, const int lane, uint32_t* q, uint64_t* pkey,
                                          uint32_t* pidx, const uint32_t ci, const uint32_t rel, const uint4 grp) {
   constexpr bool LEAN = is_lean(MODE), FRESH = MODE != 0, CUT = MODE == 3 || MODE == 4;
   constexpr bool GRP = MODE == 5 || MODE == 6;   // schedule sharing across a (node, dp) group's tp variants
@@ -1422,6 +1428,10 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
 #ifndef SAMU_K2_MINB
 #define SAMU_K2_MINB 6
 #endif
+// FRESH launches without groups (modes 2, 4): their shared block fits 7 blocks too
+#ifndef SAMU_K2_MINB_FRESH
+#define SAMU_K2_MINB_FRESH 6
+#endif
 // LEAN launches: 7 blocks (28 warps, 72 registers; the smaller shared block fits)
 #ifndef SAMU_K2_MINB_LEAN
 #define SAMU_K2_MINB_LEAN 7
@@ -1431,7 +1441,8 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
 template <int BSK, bool CONSTC, int MODE>
 // (the minimum block counts are per 4-warp block: the register caps stay the same for any block size)
 __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK,
-                                  (is_lean(MODE) ? SAMU_K2_MINB_LEAN : SAMU_K2_MINB) * 4 / SAMU_WARPS_PER_BLOCK)
+                                  (is_lean(MODE) ? SAMU_K2_MINB_LEAN : (MODE == 2 || MODE == 4) ? SAMU_K2_MINB_FRESH
+                                                                                    : SAMU_K2_MINB) * 4 / SAMU_WARPS_PER_BLOCK)
     k_simulate(SimLaunch P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // lane id kept in a register: an opaque copy cannot be rematerialised from SR_TID (an S2R
@@ -1442,7 +1453,7 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK,
   int warp_v = threadIdx.x >> 5;   // the same for the warp index, i.e. the warp's shared block (-3.3 %)
   asm volatile("" : "+r"(warp_v));
   const int warp = warp_v;
-  WarpSmT<is_lean(MODE)>& W = reinterpret_cast<WarpSmT<is_lean(MODE)>*>(smem_raw)[warp];
+  WarpSmT<is_lean(MODE), (MODE == 5 || MODE == 6)>& W = reinterpret_cast<WarpSmT<is_lean(MODE), (MODE == 5 || MODE == 6)>*>(smem_raw)[warp];
   const int gw = blockIdx.x * SAMU_WARPS_PER_BLOCK + warp;
   uint32_t* q = P.scratch_q + (size_t)gw * P.max_q;
   uint64_t* pkey = P.scratch_key + (size_t)gw * 4 * P.max_p;
@@ -1499,7 +1510,9 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK,
 }
 
 int32_t simulate_smem_bytes(int mode) {
-  return (int32_t)((is_lean(mode) ? sizeof(WarpSmT<true>) : sizeof(WarpSmT<false>)) * SAMU_WARPS_PER_BLOCK);
+  const size_t b = mode == 5 ? sizeof(WarpSmT<true, true>) : mode == 6 ? sizeof(WarpSmT<false, true>)
+                 : is_lean(mode) ? sizeof(WarpSmT<true, false>) : sizeof(WarpSmT<false, false>);
+  return (int32_t)(b * SAMU_WARPS_PER_BLOCK);
 }
 
 template <int BSK, bool CONSTC, int MODE>
