@@ -386,6 +386,13 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
 #else
   constexpr bool REQIT_CF = MODE == 1 || MODE == 2 || MODE == 5 || MODE == 6;
 #endif
+  // compact small batches (one request per lane: slot 0 only): the chain summariser's KV-bound
+  // FRESH items run at B ~ 10-20; the LEAN launches' batches are large (the checks cost more there)
+#ifdef SAMU_K2_NO_COMPACT
+  constexpr bool COMPACT = false;
+#else
+  constexpr bool COMPACT = !LEAN;
+#endif
   const DevApp& A = P.app;
   const int n = A.n_req;
     const DevCand& C = CONSTC ? c_cands[ci] : P.cands[ci];
@@ -723,7 +730,10 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
             const uint32_t s_fin = m.d + rem0 - 1;
             const uint32_t s_meta = (m.next_rank << 5) | bs.posmod((int32_t)hp - (int32_t)m.d);
             // into a free slot of the head's lane, else of the first lane with one (B < 256)
-            const uint32_t fl = __ballot_sync(FULL, occ != 0xFFu);
+            // (COMPACT: prefer an empty lane, so a small batch keeps one request per lane and
+            // retirement and victim search read one slot per lane)
+            const uint32_t e0 = COMPACT ? __ballot_sync(FULL, occ == 0u) : 0u;
+            const uint32_t fl = e0 ? e0 : __ballot_sync(FULL, occ != 0xFFu);
             const uint32_t tgt = ((fl >> wb) & 1u) ? wb : (uint32_t)(__ffs(fl) - 1);
             if ((uint32_t)lane == tgt) {
               const int jb = __ffs(~occ & 0xFFu) - 1;
@@ -1079,10 +1089,14 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
             if (m.next_rank < (1u << 23)) {
               // ranks are unique: key = (meta << 3 | j) + 1 names the slot of the lane's maximum
               uint32_t key = 0;
+              if (COMPACT && __all_sync(FULL, occ <= 1u)) {   // compact: slot 0 only
+                key = occ ? (W.s_meta[lane] << 3) + 1u : 0u;
+              } else {
 #pragma unroll
-              for (int jj = 0; jj < 8; ++jj) {
-                const uint32_t kj = ((occ >> jj) & 1u) ? ((W.s_meta[lane + 32 * jj] << 3) | (uint32_t)jj) + 1u : 0u;
-                key = max(key, kj);
+                for (int jj = 0; jj < 8; ++jj) {
+                  const uint32_t kj = ((occ >> jj) & 1u) ? ((W.s_meta[lane + 32 * jj] << 3) | (uint32_t)jj) + 1u : 0u;
+                  key = max(key, kj);
+                }
               }
               const uint32_t vkey = __reduce_max_sync(FULL, key);
               ol = __ffs(__ballot_sync(FULL, key == vkey)) - 1;
@@ -1117,11 +1131,10 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
               W.stk_req[m.stack_cnt] = vr;
               W.stk_pr[m.stack_cnt] = (l << 16) | vrem;
               // the lane's summaries change only if the victim held one of them
-#ifdef SAMU_K2_NO_LAZYV
-              if (true) {
-#else
-              if ((uint32_t)vfo.x == lminf || vfo.y == lmaxo) {
-#endif
+              if (occ == 0u) {
+                lminf = FULL;
+                lmaxo = INT_MIN;
+              } else if ((uint32_t)vfo.x == lminf || vfo.y == lmaxo) {
                 lminf = FULL;
                 lmaxo = INT_MIN;
 #pragma unroll
@@ -1171,7 +1184,24 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
           if (ninv <= 4) K2STAT(13, 1);
           uint32_t cnt_l = 0, sfin_l = 0;
           int32_t fr_l = 0;
-          if (ninv <= 4) {
+          if (COMPACT && __all_sync(FULL, occ <= 1u)) {
+            // compact: every lane holds at most its slot 0, whose finish index is lminf
+            const bool fin = lminf == m.d;
+            if (fin) {
+              const uint32_t l_now = (uint32_t)(W.s_fo[lane].y + (int32_t)m.d);
+              fr_l = (int32_t)bs.cdiv(l_now - 1);
+              sfin_l = l_now;
+              cnt_l = 1;
+              atomicSub(&W.hist[W.s_meta[lane] & 31u], 1u);
+              occ = 0;
+              lminf = FULL;
+              lmaxo = INT_MIN;
+            }
+            if (need_rel) {
+              const uint32_t fb = __ballot_sync(FULL, fin);
+              if (fin) W.tmp[__popc(fb & lanemask_lt())] = W.s_req[lane];
+            }
+          } else if (ninv <= 4) {
             // transposed scan: 8-lane group g reads the 8 slots of the g-th involved lane
             const int g = lane >> 3, jj = lane & 7;
             // one involved lane (common): its id is the ballot's only bit, no lane table
