@@ -697,6 +697,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
       const uint32_t hp = __shfl_sync(FULL, w_p, wb);
       const bool fits = wlen > 0 && m.B < ms && hp <= C.budget && (int32_t)bs.cdiv(hp) <= m.F;
       uint32_t n_fin = 0;
+      bool go_decode = !fits;
       if (fits) {
         // ================= prefill iteration (c8): admit a strict FCFS prefix of W =========
         uint32_t k_adm = 0, tok = 0, smaxp = 0, S_add = 0, n_stay = 0;
@@ -933,7 +934,18 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
           m.next_fin = __reduce_min_sync(FULL, lminf);
           m.maxO = __reduce_max_sync(FULL, lmaxo);
         }
-      } else {
+        // Without a stop time or arrivals (modes 1, 2, 5, 6) the next iteration's choice needs
+        // only the refilled window: when the new head does not fit, the decode follows in this
+        // same pass (not when a successor released by this prefill could become the head)
+#ifndef SAMU_K2_NO_MERGE
+        if ((MODE == 1 || MODE == 2 || MODE == 5 || MODE == 6) && (LEAN || n_fin == 0) && m.B > 0) {
+          const uint32_t wl3 = m.stack_cnt + (m.q_tail - m.q_head);
+          const uint32_t hp3 = wl3 ? __shfl_sync(FULL, w_p, wb) : 0u;
+          go_decode = !(wl3 > 0 && m.B < ms && hp3 <= C.budget && (int32_t)bs.cdiv(hp3) <= m.F);
+        }
+#endif
+      }
+      if (go_decode) {
         if (m.B == 0) { m.err = SAMU_E_INFEASIBLE; if (lane == 0) W.site = 9; break; }
         // ================= decode run (c9): uniform iterations until an event ===============
         const uint32_t need1 = W.hist[NEEDIDX];
