@@ -108,6 +108,17 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
   return v;
 }
 
+// inclusive scan within segments of WIDTH lanes (lanes below WIDTH: the first segment)
+template <int WIDTH>
+__device__ __forceinline__ uint32_t seg_incl_scan(uint32_t v, int lane) {
+#pragma unroll
+  for (int o = 1; o < WIDTH; o <<= 1) {
+    const uint32_t n = __shfl_up_sync(FULL, v, o, WIDTH);
+    if ((lane & (WIDTH - 1)) >= o) v += n;
+  }
+  return v;
+}
+
 __device__ __forceinline__ uint64_t dkey(double x) {   // order-preserving double -> u64
   const uint64_t b = (uint64_t)__double_as_longlong(x);
   return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
@@ -988,7 +999,8 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
         }
 #endif
         if (tight) {
-          pre = warp_incl_scan(hv, lane);
+          // (only lanes below bs are read: a block size <= 16 needs a 16-lane scan)
+          pre = (BSK > 0 && BSK <= 16) ? seg_incl_scan<16>(hv, lane) : warp_incl_scan(hv, lane);
           {
             const uint32_t F0 = (uint32_t)m.F;
             // q0 = F0 / B from an fp32 estimate corrected by the remainder (F0 < B (l_max / bs + 1)
