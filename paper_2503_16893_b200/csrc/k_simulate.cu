@@ -982,41 +982,46 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
         // no time limit and no arrivals in modes 1, 2, 5, 6: the stop time is a compile-time +inf
         const double stop_t = (MODE == 1 || MODE == 2 || MODE == 5 || MODE == 6) ? CUDART_INF : m.stop;
         // KV need of the run's decodes: histogram rotated to start at needidx, prefix sums
-        const uint32_t hv = (uint32_t)lane < bs.v() ? W.hist[bs.mod(NEEDIDX + bs.v() - (uint32_t)lane)] : 0u;
         const uint32_t m_fin = m.next_fin - m.d;
         uint32_t i_pre = 0x7fffffffu;   // first run iteration that must preempt
-        uint32_t pre = 0;
-        // each bs decodes need exactly B blocks: no search (and no scan) when the run cannot run out
-        bool tight = (uint32_t)m.F < B * (bs.div(m_fin) + 1u);   // <= 256 * (65535 + 1): 32 bits
+        uint32_t pre = 0, hv = 0;
+        bool tight = true;
+        if ((int32_t)need1 > m.F) {
+          i_pre = 0;   // the first decode already preempts (KV thrash): no run, no search
+        } else {
+          hv = (uint32_t)lane < bs.v() ? W.hist[bs.mod(NEEDIDX + bs.v() - (uint32_t)lane)] : 0u;
+          // each bs decodes need exactly B blocks: no search (and no scan) when the run cannot run out
+          tight = (uint32_t)m.F < B * (bs.div(m_fin) + 1u);   // <= 256 * (65535 + 1): 32 bits
 #ifndef SAMU_K2_NO_TIGHT2
-        // (LEAN only: on the chain summariser's FRESH path most runs that fail the first test also
-        // preempt, and the extra reduction measured slower)
-        if (LEAN && tight) {
-          // the exact need of the whole run (full cycles of B blocks + its first m_fin mod bs
-          // phases) is non-decreasing in the decode count: no preemption if it fits
-          const uint32_t rf = bs.mod(m_fin);
-          tight = bs.div(m_fin) * B + __reduce_add_sync(FULL, (uint32_t)lane < rf ? hv : 0u) > (uint32_t)m.F;
-        }
+          // (LEAN only: on the chain summariser's FRESH path most runs that fail the first test also
+          // preempt, and the extra reduction measured slower)
+          if (LEAN && tight) {
+            // the exact need of the whole run (full cycles of B blocks + its first m_fin mod bs
+            // phases) is non-decreasing in the decode count: no preemption if it fits
+            const uint32_t rf = bs.mod(m_fin);
+            tight = bs.div(m_fin) * B + __reduce_add_sync(FULL, (uint32_t)lane < rf ? hv : 0u) > (uint32_t)m.F;
+          }
 #endif
-        if (tight) {
-          // (only lanes below bs are read: a block size <= 16 needs a 16-lane scan)
-          pre = (BSK > 0 && BSK <= 16) ? seg_incl_scan<16>(hv, lane) : warp_incl_scan(hv, lane);
-          {
-            const uint32_t F0 = (uint32_t)m.F;
-            // q0 = F0 / B from an fp32 estimate corrected by the remainder (F0 < B (l_max / bs + 1)
-            // here, so the estimate is within one of the quotient)
-            uint32_t q0 = 0;
-            int32_t rs = (int32_t)F0;
-            if (F0 >= B) {   // (KV-bound runs mostly have fewer free blocks than requests)
-              q0 = __float2uint_rz(__fdividef((float)F0, (float)B));
-              rs = (int32_t)(F0 - q0 * B);
-              while (rs < 0) { --q0; rs += (int32_t)B; }
-              while (rs >= (int32_t)B) { ++q0; rs -= (int32_t)B; }
+          if (tight) {
+            // (only lanes below bs are read: a block size <= 16 needs a 16-lane scan)
+            pre = (BSK > 0 && BSK <= 16) ? seg_incl_scan<16>(hv, lane) : warp_incl_scan(hv, lane);
+            {
+              const uint32_t F0 = (uint32_t)m.F;
+              // q0 = F0 / B from an fp32 estimate corrected by the remainder (F0 < B (l_max / bs + 1)
+              // here, so the estimate is within one of the quotient)
+              uint32_t q0 = 0;
+              int32_t rs = (int32_t)F0;
+              if (F0 >= B) {   // (KV-bound runs mostly have fewer free blocks than requests)
+                q0 = __float2uint_rz(__fdividef((float)F0, (float)B));
+                rs = (int32_t)(F0 - q0 * B);
+                while (rs < 0) { --q0; rs += (int32_t)B; }
+                while (rs >= (int32_t)B) { ++q0; rs -= (int32_t)B; }
+              }
+              const uint32_t rem = (uint32_t)rs;
+              const uint32_t bad = __ballot_sync(FULL, (uint32_t)lane < bs.v() && pre > rem);
+              const uint64_t ip = (uint64_t)q0 * bs.v() + (uint32_t)(__ffs(bad) - 1);
+              i_pre = ip > 0x7fffffffull ? 0x7fffffffu : (uint32_t)ip;
             }
-            const uint32_t rem = (uint32_t)rs;
-            const uint32_t bad = __ballot_sync(FULL, (uint32_t)lane < bs.v() && pre > rem);
-            const uint64_t ip = (uint64_t)q0 * bs.v() + (uint32_t)(__ffs(bad) - 1);
-            i_pre = ip > 0x7fffffffull ? 0x7fffffffu : (uint32_t)ip;
           }
         }
         const uint32_t m_run = min(m_fin, i_pre);

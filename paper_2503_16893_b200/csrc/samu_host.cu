@@ -236,13 +236,19 @@ static samu_status comm_allreduce_i32(samu_ctx* c, const int32_t* send, int32_t*
   if (c->group) {
     CK(c, cudaStreamSynchronize(s));
     c->group->exchange(c->rank, send);
+    // Every copy runs on the context's stream and is waited for: a plain cudaMemcpy from pageable
+    // host memory may return before its DMA lands and is not ordered with a non-blocking stream,
+    // so a later read of `recv` on the stream could see the previous call's value — ranks then
+    // disagree on a flag (e.g. an unfinished node) and one of them waits alone in a collective.
     std::vector<int32_t> acc(n, 0), tmp(n);
     for (int w = 0; w < c->world; ++w) {
-      CK(c, cudaMemcpy(tmp.data(), c->group->ptrs[w], sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+      CK(c, cudaMemcpyAsync(tmp.data(), c->group->ptrs[w], sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+      CK(c, cudaStreamSynchronize(s));
       for (int i = 0; i < n; ++i) acc[i] = (w == 0) ? tmp[i] : (op == 0 ? std::max(acc[i], tmp[i]) : acc[i] + tmp[i]);
     }
     c->group->barrier(c->rank);
-    CK(c, cudaMemcpy(recv, acc.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+    CK(c, cudaMemcpyAsync(recv, acc.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    CK(c, cudaStreamSynchronize(s));
     return SAMU_OK;
   }
   CKN(c, ncclAllReduce(send, recv, n, ncclInt32, op == 0 ? ncclMax : ncclSum, c->comm, s));
