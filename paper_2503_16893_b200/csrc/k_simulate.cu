@@ -404,6 +404,12 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
 #else
   constexpr bool COMPACT = !LEAN;
 #endif
+  // lazy window refills (see the loop top)
+#ifdef SAMU_K2_EAGER_WIN
+  constexpr bool LAZYW = false;
+#else
+  constexpr bool LAZYW = true;
+#endif
   const DevApp& A = P.app;
   const int n = A.n_req;
     const DevCand& C = CONSTC ? c_cands[ci] : P.cands[ci];
@@ -695,10 +701,12 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
         if (!FRESH && W.pend_ptr < W.n_pend && W.next_ready != CUDART_INF) { m.t = W.next_ready; continue; }
         break;
       }
-      // refill the window so it holds min(32, |W|) entries
+      // refill the window so it holds min(32, |W|) entries (LAZYW: only once it holds fewer than
+      // min(2, |W|): the head checks read its first two entries, the multi-request admission below
+      // refills it in full first; a refill loads all missing entries in one pass)
       {
         const uint32_t want = min(32u, wlen);
-        if (wn < want) {
+        if (wn < (LAZYW ? min(2u, wlen) : want)) {
           const uint32_t pos = ((uint32_t)lane - wb) & 31u;
           if (pos >= wn && pos < want) WIN_LOAD(pos);
           wn = want;
@@ -769,13 +777,22 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
           wb = (wb + 1u) & 31u;
           wn -= 1u;
           const uint32_t want = min(32u, m.stack_cnt + (m.q_tail - m.q_head));
-          if (wn < want) {
+          // (LAZYW: the merged decode check below reads the new head)
+          if (wn < (LAZYW ? min(1u, want) : want)) {
             const uint32_t pos = ((uint32_t)lane - wb) & 31u;
             if (pos >= wn && pos < want) WIN_LOAD(pos);
             wn = want;
           }
         } else
         for (;;) {
+          if (LAZYW) {   // the FCFS prefix may extend over the whole window: fill it
+            const uint32_t want = min(32u, m.stack_cnt + (m.q_tail - m.q_head));
+            if (wn < want) {
+              const uint32_t pos = ((uint32_t)lane - wb) & 31u;
+              if (pos >= wn && pos < want) WIN_LOAD(pos);
+              wn = want;
+            }
+          }
           const uint32_t pos = ((uint32_t)lane - wb) & 31u;   // window position of this lane
           const bool valid = pos < wn;
           const uint32_t p = valid ? w_p : 0u;

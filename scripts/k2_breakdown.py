@@ -26,3 +26,12 @@ for name, nodes in groups.items():
         e0.record(); o2 = S.samu_simulate_batch(cs, lo, li); e1.record(); torch.cuda.synchronize()
         g2 = recs_to_numpy(o2["recs"])
         print(f"    dp={dp}: cands={len(cs)} ms={e0.elapsed_time(e1):7.1f} iters={g2['iters'].sum():.3e} mean_B={g2['req_iters'].astype(float).sum()/g2['iters'].sum():.1f}")
+# the whole first-step candidate set (the bench step's K2 work): median of 5 timed calls
+allc = [(v, dp, tp) for nodes in groups.values() for v in nodes for (dp, tp) in S.samu_enumerate_plans(v)]
+S.samu_simulate_batch(allc, lo, li)
+ts = []
+for _ in range(5):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(); S.samu_simulate_batch(allc, lo, li); e1.record(); torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1))
+print(f"all {len(allc)} candidates: median {np.median(ts):.2f} ms min {min(ts):.2f} max {max(ts):.2f}")

@@ -59,8 +59,9 @@ for r in data:
     samp[line] += s
     tot_i += i
     tot_s += s
-src = open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2503_16893_b200", "csrc",
-                        "k_simulate.cu")).read().splitlines()
+# SAMU_SRC: the k_simulate.cu the .so was built from (default: the working tree's)
+src = open(os.environ.get("SAMU_SRC") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "..",
+                                                      "paper_2503_16893_b200", "csrc", "k_simulate.cu")).read().splitlines()
 print(f"total warp instructions {tot_i:.4e}, stall samples {tot_s}")
 for line, i in inst.most_common(top):
     if isinstance(line, tuple):
