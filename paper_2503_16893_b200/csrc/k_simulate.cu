@@ -31,6 +31,9 @@
 
 #include <mutex>
 
+#ifndef SAMU_K2_MULTI_EAGER   // 1: refill the window after every multi-request admission round
+#define SAMU_K2_MULTI_EAGER 0
+#endif
 #ifndef SAMU_K2_CHUNK_MIN
 #define SAMU_K2_CHUNK_MIN 4   // decode runs longer than this take the lane-parallel chunk sums
 #endif
@@ -404,6 +407,9 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
 #else
   constexpr bool COMPACT = !LEAN;
 #endif
+  // the host runs a candidate on the FRESH paths (modes 2, 4, 6) only when its node has chain
+  // successors (DevCand::has_succ): no constant-bank read for it there
+  constexpr bool SUCC = MODE == 2 || MODE == 4 || MODE == 6;
   // lazy window refills (see the loop top)
 #ifdef SAMU_K2_EAGER_WIN
   constexpr bool LAZYW = false;
@@ -623,7 +629,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
     // phase whose requests need a new KV block at the next decode: -d mod bs (phase = (l - 1 - d)
     // mod bs, fixed at admission); kept in a register only for the general block size
 #define NEEDIDX (BSK >= 0 ? ((0u - m.d) & bs.mask()) : m.needidx)
-    const bool need_rel = LEAN ? false : FRESH ? (bool)C.has_succ : (fio || fto || commit || C.has_succ);
+    const bool need_rel = LEAN ? false : FRESH ? (SUCC || (bool)C.has_succ) : (fio || fto || commit || C.has_succ);
     bool cut = false;
     // per-lane summaries of this lane's slots: min finish index, max (l - d)
     uint32_t lminf = FULL;
@@ -716,6 +722,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
       const uint32_t hp = __shfl_sync(FULL, w_p, wb);
       const bool fits = wlen > 0 && m.B < ms && hp <= C.budget && (int32_t)bs.cdiv(hp) <= m.F;
       uint32_t n_fin = 0;
+      bool rel_done = false;   // the retirement released the successors itself
       bool go_decode = !fits;
       if (fits) {
         // ================= prefill iteration (c8): admit a strict FCFS prefix of W =========
@@ -928,12 +935,13 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
           const uint32_t take = min(mm, m.stack_cnt);
           m.stack_cnt -= take;
           m.q_head += mm - take;
-          // advance the window by mm and refill it
+          // advance the window by mm and refill it (LAZYW: the next round fills it first; after the
+          // last round the merged decode check reads the new head)
           wb = (wb + mm) & 31u;
           wn -= mm;
           const uint32_t wl2 = m.stack_cnt + (m.q_tail - m.q_head);
           const uint32_t want = min(32u, wl2);
-          if (wn < want) {
+          if (wn < ((LAZYW && !SAMU_K2_MULTI_EAGER) ? min(1u, want) : want)) {
             const uint32_t pos = ((uint32_t)lane - wb) & 31u;
             if (pos >= wn && pos < want) WIN_LOAD(pos);
             wn = want;
@@ -1244,8 +1252,24 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
               lmaxo = INT_MIN;
             }
             if (need_rel) {
-              const uint32_t fb = __ballot_sync(FULL, fin);
-              if (fin) W.tmp[__popc(fb & lanemask_lt())] = W.s_req[lane];
+#ifdef SAMU_K2_FOLD_REL
+              if (FRESH && ninv == 1) {
+                // one finisher (FRESH: no outputs): it appends its successor, if any, to the back of
+                // W itself (the release below is skipped; the __syncwarp closing the retirement
+                // orders the store before any window refill)
+                int32_t sr = -1;
+                if (fin) {
+                  sr = (SUCC || C.has_succ) ? __ldg(A.succ + W.s_req[lane]) : -1;
+                  if (sr >= 0) q[m.q_tail] = (uint32_t)sr;
+                }
+                m.q_tail += __popc(__ballot_sync(FULL, sr >= 0));
+                rel_done = true;
+              } else
+#endif
+              {
+                const uint32_t fb = __ballot_sync(FULL, fin);
+                if (fin) W.tmp[__popc(fb & lanemask_lt())] = W.s_req[lane];
+              }
             }
           } else if (ninv <= 4) {
             // transposed scan: 8-lane group g reads the 8 slots of the g-th involved lane
@@ -1338,11 +1362,11 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
         }
       }
       // ---- finish records + chain successor release (c19), for this iteration's finishers ----
-      if (!LEAN && n_fin && need_rel) {
+      if (!LEAN && n_fin && need_rel && !rel_done) {
         const uint32_t itx = m.iter + m.d - 1;   // iterations = prefills + decodes
         if (FRESH && n_fin == 1) {
           // one finisher (FRESH: no outputs): its successor, if any, joins the back of W
-          const int32_t sr = C.has_succ ? __ldg(A.succ + W.tmp[0]) : -1;
+          const int32_t sr = (SUCC || C.has_succ) ? __ldg(A.succ + W.tmp[0]) : -1;
           if (sr >= 0) {
             if (lane == 0) q[m.q_tail] = (uint32_t)sr;
             m.q_tail += 1;
@@ -1361,7 +1385,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
                 if (commit) { st[r] = SAMU_ST_DONE << 28; ft[r] = m.t; }
               }
             }
-            if (C.has_succ) sr = __ldg(A.succ + r);
+            if (SUCC || C.has_succ) sr = __ldg(A.succ + r);
           }
           const uint32_t br = __ballot_sync(FULL, sr >= 0);
           if (br) {
@@ -1387,7 +1411,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
                 if (fto) fto[r] = m.t;
                 if (commit) { st[r] = SAMU_ST_DONE << 28; ft[r] = m.t; }
               }
-              if (C.has_succ) sr = __ldg(A.succ + r);
+              if (SUCC || C.has_succ) sr = __ldg(A.succ + r);
             }
             // compacted in place: the k-th successor overwrites finisher slot <= k, already read
             // by every lane of this pass (the __syncwarp orders those reads before the writes)
@@ -1504,9 +1528,10 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
 #ifndef SAMU_K2_MINB
 #define SAMU_K2_MINB 6
 #endif
-// FRESH launches without groups (modes 2, 4): their shared block fits 7 blocks too
+// FRESH launches without groups (modes 2, 4): their shared block fits 7 blocks too (28 warps at
+// 72 registers: equal to 6 x 80 in round 1, -2 ms per C5 step once the window refills went lazy)
 #ifndef SAMU_K2_MINB_FRESH
-#define SAMU_K2_MINB_FRESH 6
+#define SAMU_K2_MINB_FRESH 7
 #endif
 // LEAN launches: 7 blocks (28 warps, 72 registers; the smaller shared block fits)
 #ifndef SAMU_K2_MINB_LEAN
