@@ -722,7 +722,6 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
       const uint32_t hp = __shfl_sync(FULL, w_p, wb);
       const bool fits = wlen > 0 && m.B < ms && hp <= C.budget && (int32_t)bs.cdiv(hp) <= m.F;
       uint32_t n_fin = 0;
-      bool rel_done = false;   // the retirement released the successors itself
       bool go_decode = !fits;
       if (fits) {
         // ================= prefill iteration (c8): admit a strict FCFS prefix of W =========
@@ -1252,24 +1251,8 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
               lmaxo = INT_MIN;
             }
             if (need_rel) {
-#ifdef SAMU_K2_FOLD_REL
-              if (FRESH && ninv == 1) {
-                // one finisher (FRESH: no outputs): it appends its successor, if any, to the back of
-                // W itself (the release below is skipped; the __syncwarp closing the retirement
-                // orders the store before any window refill)
-                int32_t sr = -1;
-                if (fin) {
-                  sr = (SUCC || C.has_succ) ? __ldg(A.succ + W.s_req[lane]) : -1;
-                  if (sr >= 0) q[m.q_tail] = (uint32_t)sr;
-                }
-                m.q_tail += __popc(__ballot_sync(FULL, sr >= 0));
-                rel_done = true;
-              } else
-#endif
-              {
-                const uint32_t fb = __ballot_sync(FULL, fin);
-                if (fin) W.tmp[__popc(fb & lanemask_lt())] = W.s_req[lane];
-              }
+              const uint32_t fb = __ballot_sync(FULL, fin);
+              if (fin) W.tmp[__popc(fb & lanemask_lt())] = W.s_req[lane];
             }
           } else if (ninv <= 4) {
             // transposed scan: 8-lane group g reads the 8 slots of the g-th involved lane
@@ -1362,7 +1345,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
         }
       }
       // ---- finish records + chain successor release (c19), for this iteration's finishers ----
-      if (!LEAN && n_fin && need_rel && !rel_done) {
+      if (!LEAN && n_fin && need_rel) {
         const uint32_t itx = m.iter + m.d - 1;   // iterations = prefills + decodes
         if (FRESH && n_fin == 1) {
           // one finisher (FRESH: no outputs): its successor, if any, joins the back of W
