@@ -29,6 +29,7 @@
 
 #include <math_constants.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #ifndef SAMU_K2_MULTI_EAGER   // 1: refill the window after every multi-request admission round
@@ -1591,6 +1592,14 @@ __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK,
     }
     sim_item<BSK, CONSTC, MODE>(P, W, lane, q, pkey, pidx, ci, rel, grp);
   }
+  // Programmatic dependent launch (launches of one batch in one stream): this warp has no more
+  // work, so the next K2 launch may start its blocks on the SM resources this launch frees while
+  // its last items run; that launch does not read this one's results.  Before exiting, a block
+  // waits for the previous launch of the chain to complete, so the completion of the last launch
+  // implies the completion of them all (the combine kernel after them is an ordinary launch).
+  // Both are no-ops for a launch without the programmatic-serialization attribute.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 int32_t simulate_smem_bytes(int mode) {
@@ -1635,19 +1644,33 @@ cudaError_t simulate_prepare(int blocks_per_sm[SAMU_K2_MODES]) {
   return prepare_one<-1, false, 0>(blocks_per_sm);
 }
 
+template <int BSK, bool CONSTC, int MODE>
+static cudaError_t launch_one(const SimLaunch& L, int32_t n_blocks, int smem, cudaStream_t s, bool pdl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)n_blocks);
+  cfg.blockDim = dim3(32 * SAMU_WARPS_PER_BLOCK);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k_simulate<BSK, CONSTC, MODE>, L);
+}
+
 template <bool CONSTC>
-static void launch_variant(const SimLaunch& L, uint32_t block_size, int mode, int32_t n_blocks, int smem,
-                           cudaStream_t s) {
-  const dim3 blk(32 * SAMU_WARPS_PER_BLOCK);
-  if (block_size == 16 && mode == 1) k_simulate<16, CONSTC, 1><<<n_blocks, blk, smem, s>>>(L);
-  else if (block_size == 16 && mode == 2) k_simulate<16, CONSTC, 2><<<n_blocks, blk, smem, s>>>(L);
-  else if (block_size == 16 && mode == 3) k_simulate<16, CONSTC, 3><<<n_blocks, blk, smem, s>>>(L);
-  else if (block_size == 16 && mode == 4) k_simulate<16, CONSTC, 4><<<n_blocks, blk, smem, s>>>(L);
-  else if (block_size == 16 && mode == 5) k_simulate<16, CONSTC, 5><<<n_blocks, blk, smem, s>>>(L);
-  else if (block_size == 16 && mode == 6) k_simulate<16, CONSTC, 6><<<n_blocks, blk, smem, s>>>(L);
-  else if (block_size == 16) k_simulate<16, CONSTC, 0><<<n_blocks, blk, smem, s>>>(L);
-  else if ((block_size & (block_size - 1)) == 0) k_simulate<0, CONSTC, 0><<<n_blocks, blk, smem, s>>>(L);
-  else k_simulate<-1, CONSTC, 0><<<n_blocks, blk, smem, s>>>(L);
+static cudaError_t launch_variant(const SimLaunch& L, uint32_t block_size, int mode, int32_t n_blocks, int smem,
+                                  cudaStream_t s, bool pdl) {
+  if (block_size == 16 && mode == 1) return launch_one<16, CONSTC, 1>(L, n_blocks, smem, s, pdl);
+  if (block_size == 16 && mode == 2) return launch_one<16, CONSTC, 2>(L, n_blocks, smem, s, pdl);
+  if (block_size == 16 && mode == 3) return launch_one<16, CONSTC, 3>(L, n_blocks, smem, s, pdl);
+  if (block_size == 16 && mode == 4) return launch_one<16, CONSTC, 4>(L, n_blocks, smem, s, pdl);
+  if (block_size == 16 && mode == 5) return launch_one<16, CONSTC, 5>(L, n_blocks, smem, s, pdl);
+  if (block_size == 16 && mode == 6) return launch_one<16, CONSTC, 6>(L, n_blocks, smem, s, pdl);
+  if (block_size == 16) return launch_one<16, CONSTC, 0>(L, n_blocks, smem, s, pdl);
+  if ((block_size & (block_size - 1)) == 0) return launch_one<0, CONSTC, 0>(L, n_blocks, smem, s, pdl);
+  return launch_one<-1, CONSTC, 0>(L, n_blocks, smem, s, pdl);
 }
 
 // Launch the K2 kernels of one simulate batch, one per mode present (Ls[i] / modes[i] / n_blocks[i]).
@@ -1685,12 +1708,19 @@ cudaError_t launch_simulate(const SimLaunch* Ls, const int* modes, const int32_t
     if ((e = cudaEventRecord(ev_fork, s)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(s2, ev_fork, 0)) != cudaSuccess) return e;
   }
+  // serialized launches (one stream): a launch may start beside the tail of the previous one
+  // (programmatic dependent launch) unless both use the per-warp scratch rings, which are indexed
+  // by the warp's position in its grid (the general / FRESH modes 0, 2, 4, 6)
+  static const bool pdl_on = !std::getenv("SAMU_K2_PDL") || std::atoi(std::getenv("SAMU_K2_PDL")) != 0;
+  auto scratch = [](int md) { return md == 0 || md == 2 || md == 4 || md == 6; };
   for (int i = 0; i < n_launch; ++i) {
     const bool on_aux = fork && (modes[i] == 1 || modes[i] == 5);
     const int smem = simulate_smem_bytes(modes[i]);
     cudaStream_t st = on_aux ? s2 : s;
-    if (constc) launch_variant<true>(Ls[i], block_size, modes[i], n_blocks[i], smem, st);
-    else launch_variant<false>(Ls[i], block_size, modes[i], n_blocks[i], smem, st);
+    const bool pdl = pdl_on && !fork && i > 0 && !(scratch(modes[i]) && scratch(modes[i - 1]));
+    e = constc ? launch_variant<true>(Ls[i], block_size, modes[i], n_blocks[i], smem, st, pdl)
+               : launch_variant<false>(Ls[i], block_size, modes[i], n_blocks[i], smem, st, pdl);
+    if (e != cudaSuccess) return e;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   if (fork) {
