@@ -966,7 +966,8 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
     int64_t items_all = 0;
     for (const DevCand& D : dc) items_all += (int64_t)T * D.dp;
     const bool small_share = items_all < 24 * (int64_t)c->n_sm * 24;
-    if (small_share)
+    static const int kvf_order = std::getenv("SAMU_K2_KVF_ORDER") ? std::atoi(std::getenv("SAMU_K2_KVF_ORDER")) : 0;
+    if (small_share || kvf_order == 1)
       for (size_t x = 0; x < idx.size(); ++x) cost[x] = (uint64_t)((double)cost[x] * kvf[x]);
     // longest-first work items (cand, trial, replica)
     std::vector<int> order(idx.size());
@@ -1138,7 +1139,24 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
       SimLaunch LM[SAMU_K2_MODES];
       int modes[SAMU_K2_MODES], nb[SAMU_K2_MODES], n_launch = 0;
       // in order on s; the LEAN launches (5, 1) concurrent on the aux stream
-      for (int md : {0, 6, 2, 4, 3, 5, 1}) {
+      static int order[SAMU_K2_MODES] = {0, 6, 2, 4, 3, 5, 1};
+      static bool order_read = false;
+      if (!order_read) {   // SAMU_K2_ORDER: launch order of the modes (experiments), e.g. "0,6,2,4,3,1,5"
+        order_read = true;
+        if (const char* o = std::getenv("SAMU_K2_ORDER")) {
+          int v[SAMU_K2_MODES], n = 0;
+          for (const char* p = o; *p && n < SAMU_K2_MODES; ) {
+            v[n++] = std::atoi(p);
+            while (*p && *p != ',') ++p;
+            if (*p == ',') ++p;
+          }
+          int seen = 0;
+          for (int i = 0; i < n; ++i) seen |= (v[i] >= 0 && v[i] < SAMU_K2_MODES) ? 1 << v[i] : 0;
+          if (n == SAMU_K2_MODES && seen == (1 << SAMU_K2_MODES) - 1)   // a permutation of the modes
+            for (int i = 0; i < n; ++i) order[i] = v[i];
+        }
+      }
+      for (int md : order) {
         if (n_items[md] == 0) continue;
         SimLaunch& X = LM[n_launch];
         X = L;
