@@ -39,9 +39,13 @@ N_SM = 148
 
 
 def trial_share(T, world, rank):
-    base, rem = divmod(T, world)
-    cnt = base + (1 if rank < rem else 0)
-    return rank * base + min(rank, rem), cnt
+    """This rank's contiguous trial block from libsamu's own sharding rule (samu_shard_plan, the
+    split its sharded samu_simulate_batch checks): the bench configs have T >= world, i.e. pure
+    trial sharding (every rank simulates every candidate)."""
+    from paper_2503_16893_b200 import samu_shard_plan
+    p = samu_shard_plan(T, world, rank)
+    assert p["job_classes"] == 1, "bench configs shard trials only (T >= world)"
+    return p["trial_begin"], p["trial_count"]
 
 
 def first_step_candidates(nodes_ready, plans_of):

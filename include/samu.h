@@ -188,6 +188,30 @@ samu_status samu_app_load(samu_ctx* ctx, const samu_engine_cfg* engine, int32_t 
  * their total count (>= 0), or a negative samu_status. */
 int32_t samu_enumerate_plans(samu_ctx* ctx, int32_t node, int32_t* dp, int32_t* tp, int32_t cap);
 
+/* ---- sharding over ranks (north star: "candidates and Monte Carlo trials shard
+ * naturally across the 8 GPUs") ---------------------------------------------------------------
+ * Host-only: no context, no GPU.  These are the rules the sharded calls apply internally, so a
+ * caller (bench.py, tests) can place its local trials / jobs the same way. */
+
+/* A (jobs x trials) product over `world` ranks: world = trial_blocks x job_classes; rank r
+ * simulates the contiguous trial block r % trial_blocks of n_trials (block sizes differ by at
+ * most one, the lower blocks larger) for the jobs of class r / trial_blocks.  job_classes = 1
+ * whenever n_trials >= world (pure trial sharding: trials are i.i.d., every rank holds every
+ * candidate); with fewer trials than ranks, trial_blocks = the largest divisor of world not above
+ * max(n_trials, 1).  forced_classes > 0 that divides world fixes job_classes (tests; the
+ * SAMU_SHARD_CLASSES variable of the sharded calls).  Any output pointer may be NULL.
+ * SAMU_E_INVALID: n_trials < 0, world < 1 or rank outside [0, world). */
+samu_status samu_shard_plan(int32_t n_trials, int32_t world, int32_t rank, int32_t forced_classes,
+                            int32_t* trial_blocks, int32_t* job_classes, int32_t* trial_begin,
+                            int32_t* trial_count, int32_t* my_class);
+
+/* Job classes of one batch: jobs (host work[n_jobs] >= 0, e.g. replica requests x expected
+ * output) are placed longest-first (stable on ties) onto the least loaded class (lowest index
+ * on ties); host out_class[n_jobs].  The greedy applies this to the jobs without a dependency
+ * source (a dependent job runs in its source's class).  SAMU_E_INVALID: n_jobs < 0,
+ * job_classes < 1, a negative or NaN work, or NULL arrays with n_jobs > 0. */
+samu_status samu_shard_classes(int32_t n_jobs, const double* work, int32_t job_classes, int32_t* out_class);
+
 /* ---- the hot path ---------------------------------------------------------------------- */
 
 /* Output-length sampling (c1-c3) for every app request and trials

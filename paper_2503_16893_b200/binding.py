@@ -91,7 +91,7 @@ EXPORTED = ["samu_ctx_create", "samu_ctx_destroy", "samu_local_group_create", "s
             "samu_ecdf_load", "samu_app_load", "samu_enumerate_plans", "samu_sample_lengths", "samu_sample_requests",
             "samu_simulate_batch",
             "samu_plan_greedy", "samu_plan_max_heuristic", "samu_plan_min_heuristic", "samu_plan_run", "samu_known_lengths",
-            "samu_replay_plan", "samu_fit_coeffs", "samu_plan_free"]
+            "samu_replay_plan", "samu_fit_coeffs", "samu_plan_free", "samu_shard_plan", "samu_shard_classes"]
 
 _lib = None
 
@@ -137,6 +137,8 @@ def lib():
         L.samu_fit_coeffs.argtypes = [P, C.c_int32, P, P, P, C.c_int32, P, P, P, P]
         L.samu_plan_free.argtypes = [C.POINTER(samu_plan)]
         L.samu_plan_free.restype = None
+        L.samu_shard_plan.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, P, P, P, P, P]
+        L.samu_shard_classes.argtypes = [C.c_int32, P, C.c_int32, P]
         _lib = L
     return _lib
 
@@ -161,6 +163,26 @@ def samu_nccl_unique_id() -> bytes:
     if rc:
         raise SamuError(rc, "ncclGetUniqueId failed")
     return bytes(buf)
+
+
+def samu_shard_plan(n_trials: int, world: int, rank: int, forced_classes: int = 0) -> Dict[str, int]:
+    """libsamu's (trial block, job class) sharding of `rank` (host-only, no GPU needed)."""
+    out = [C.c_int32() for _ in range(5)]
+    rc = lib().samu_shard_plan(n_trials, world, rank, forced_classes, *[C.byref(o) for o in out])
+    if rc:
+        raise SamuError(rc, "samu_shard_plan: invalid arguments")
+    keys = ("trial_blocks", "job_classes", "trial_begin", "trial_count", "my_class")
+    return {k: o.value for k, o in zip(keys, out)}
+
+
+def samu_shard_classes(work, job_classes: int) -> np.ndarray:
+    """libsamu's job -> class assignment of one batch (longest-first onto the least loaded)."""
+    w = np.ascontiguousarray(work, dtype=np.float64)
+    cls = np.zeros(len(w), np.int32)
+    rc = lib().samu_shard_classes(len(w), _np_ptr(w), job_classes, _np_ptr(cls))
+    if rc:
+        raise SamuError(rc, "samu_shard_classes: invalid arguments")
+    return cls
 
 
 class LocalGroup:

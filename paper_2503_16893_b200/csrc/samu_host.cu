@@ -1239,18 +1239,64 @@ static void trial_share(int T, int world, int rank, int* begin, int* count) {
 // all of its candidates.  With fewer trials than ranks (C1: T = 1) the candidates are split into
 // Wc = world / Wt classes, Wt the largest divisor of world not above T.  SAMU_SHARD_CLASSES=k
 // forces Wc = k (k | world; tests).
-static void shard_split(const samu_ctx* c, int T, int* Wt, int* Wc) {
+static void shard_split_w(int world, int T, int forced, int* Wt, int* Wc) {
   int wc = 1;
-  const char* e = std::getenv("SAMU_SHARD_CLASSES");
-  const int forced = e ? std::atoi(e) : 0;
-  if (forced > 0 && c->world % forced == 0) wc = forced;
-  else if (T < c->world) {
+  if (forced > 0 && world % forced == 0) wc = forced;
+  else if (T < world) {
     int wt = 1;
-    for (int d = 1; d <= c->world; ++d) if (c->world % d == 0 && d <= std::max(T, 1)) wt = d;
-    wc = c->world / wt;
+    for (int d = 1; d <= world; ++d) if (world % d == 0 && d <= std::max(T, 1)) wt = d;
+    wc = world / wt;
   }
   *Wc = wc;
-  *Wt = c->world / wc;
+  *Wt = world / wc;
+}
+
+static void shard_split(const samu_ctx* c, int T, int* Wt, int* Wc) {
+  const char* e = std::getenv("SAMU_SHARD_CLASSES");
+  shard_split_w(c->world, T, e ? std::atoi(e) : 0, Wt, Wc);
+}
+
+// Job classes of one batch (Wc > 1): jobs longest-first (stable on ties) onto the least loaded
+// class (lowest index on ties); identical on every rank.
+static void assign_classes(const std::vector<int>& jobs, const std::vector<double>& work, int Wc, std::vector<int>& cls) {
+  std::vector<int> order(jobs);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return work[a] > work[b]; });
+  std::vector<double> load(Wc, 0.0);
+  for (int x : order) {
+    int k = 0;
+    for (int q = 1; q < Wc; ++q) if (load[q] < load[k]) k = q;
+    cls[x] = k;
+    load[k] += work[x];
+  }
+}
+
+extern "C" samu_status samu_shard_plan(int32_t n_trials, int32_t world, int32_t rank, int32_t forced_classes,
+                                       int32_t* trial_blocks, int32_t* job_classes, int32_t* trial_begin,
+                                       int32_t* trial_count, int32_t* my_class) {
+  if (n_trials < 0 || world < 1 || rank < 0 || rank >= world) return SAMU_E_INVALID;
+  int Wt = 1, Wc = 1, b = 0, cnt = 0;
+  shard_split_w(world, n_trials, forced_classes, &Wt, &Wc);
+  trial_share(n_trials, Wt, rank % Wt, &b, &cnt);
+  if (trial_blocks) *trial_blocks = Wt;
+  if (job_classes) *job_classes = Wc;
+  if (trial_begin) *trial_begin = b;
+  if (trial_count) *trial_count = cnt;
+  if (my_class) *my_class = rank / Wt;
+  return SAMU_OK;
+}
+
+extern "C" samu_status samu_shard_classes(int32_t n_jobs, const double* work, int32_t job_classes, int32_t* out_class) {
+  if (n_jobs < 0 || job_classes < 1 || (n_jobs > 0 && (!work || !out_class))) return SAMU_E_INVALID;
+  std::vector<int> jobs(n_jobs), cls(n_jobs, 0);
+  std::vector<double> w(n_jobs);
+  for (int x = 0; x < n_jobs; ++x) {
+    if (!(work[x] >= 0.0)) return SAMU_E_INVALID;   // also rejects NaN
+    jobs[x] = x;
+    w[x] = work[x];
+  }
+  assign_classes(jobs, w, job_classes, cls);
+  for (int x = 0; x < n_jobs; ++x) out_class[x] = cls[x];
+  return SAMU_OK;
 }
 
 // all-gather per-(job, local trial) records [n][T_local] into rows of `dst` ([*][T]) at `slots`;
@@ -1546,20 +1592,14 @@ struct Greedy {
     std::vector<int> cls(pending.size(), 0);
     if (Wc > 1) {
       std::vector<int> free_jobs;
-      for (size_t x = 0; x < pending.size(); ++x) if (pending_src[x] < 0) free_jobs.push_back((int)x);
-      auto work = [&](int x) {
+      std::vector<double> work(pending.size(), 0.0);
+      for (size_t x = 0; x < pending.size(); ++x) {
         const int v = pending[x].cand.node;
-        return (double)(c->node_end[v] - c->node_begin[v]) * c->node_exp_out[v];
-      };
-      std::stable_sort(free_jobs.begin(), free_jobs.end(), [&](int a, int b) { return work(a) > work(b); });
-      std::vector<double> load(Wc, 0.0);
-      for (int x : free_jobs) {
-        int k = 0;
-        for (int q = 1; q < Wc; ++q) if (load[q] < load[k]) k = q;
-        cls[x] = k;
-        load[k] += work(x);
-        slot_class[pending_slots[x]] = k;
+        work[x] = (double)(c->node_end[v] - c->node_begin[v]) * c->node_exp_out[v];
+        if (pending_src[x] < 0) free_jobs.push_back((int)x);
       }
+      assign_classes(free_jobs, work, Wc, cls);
+      for (int x : free_jobs) slot_class[pending_slots[x]] = cls[x];
       for (size_t x = 0; x < pending.size(); ++x)
         if (pending_src[x] >= 0) {
           cls[x] = slot_class.at(pending_src[x]);

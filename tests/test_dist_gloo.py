@@ -1,9 +1,11 @@
-"""N>1 host logic on CPU (gloo, world size 2): trials are sharded in contiguous blocks, every rank
-simulates only its share, per-(candidate, trial) records are all-gathered in rank = trial order
-and reduced in trial order.  The result must be bit-identical to the single-process run, for the
-per-candidate means (c17) and for the greedy's stage score inputs.  The simulator here is the
-oracle (no GPU); libsamu's NCCL path follows the same plan (samu_host.cu: trial_share,
-gather_records) and bench.py uses the same split.
+"""N>1 host logic on CPU (gloo, world sizes 2 and 4): every rank takes its share from libsamu's
+own sharding rules (samu_shard_plan / samu_shard_classes, the host-only entry points the sharded
+calls apply internally): contiguous trial blocks, and job classes when there are fewer trials
+than ranks.  Each rank simulates only its (class, trial block), the per-(candidate, trial)
+records are all-gathered in rank order and placed by the same plan.  The result must be
+bit-identical to the single-process run, for the records and the trial-ordered means (c17).
+The simulator here is the oracle (no GPU); libsamu's NCCL path gathers with the same plan
+(samu_host.cu: gather_records, the unpack kernel) and bench.py uses the same split.
 """
 import os
 import socket
@@ -20,9 +22,24 @@ SEED = W.SAMPLING_SEED
 
 
 def trial_share(T, world, rank):
+    """the contiguous split written out (the reference for libsamu's plan in the tests below)"""
     base, rem = divmod(T, world)
     cnt = base + (1 if rank < rem else 0)
     return rank * base + min(rank, rem), cnt
+
+
+def _libsamu():
+    import __graft_entry__  # noqa: F401
+    from paper_2503_16893_b200 import build
+    build.build()
+    import paper_2503_16893_b200 as S
+    return S
+
+
+def _work(w):
+    # per-candidate work for the class assignment: replica requests x mean prompt (any fixed,
+    # rank-independent value does; the greedy uses replica requests x expected output)
+    return [float(np.sum(w.node == n)) / d * (1 + t) for (n, d, t) in CANDS]
 
 
 def _free_port():
@@ -41,30 +58,42 @@ def _worker(rank, world, port, T, out_path):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    S = _libsamu()
     w = W.make_workload("c2", n_prompts=120, n_trials=T)
     P = O.Problem(w)
-    tb, cnt = trial_share(T, world, rank)
-    lo, li = P.sample(SEED, tb, cnt)          # counter-based: only this rank's trials
-    recs = np.stack([P.simulate(n, d, t, lo, li)[0] for (n, d, t) in CANDS])   # [cand][local trial]
-    tmax = -(-T // world)
+    plans = [S.samu_shard_plan(T, world, r) for r in range(world)]
+    me = plans[rank]
+    Wt, Wc = me["trial_blocks"], me["job_classes"]
+    cls = S.samu_shard_classes(_work(w), Wc)
+    tb, cnt = me["trial_begin"], me["trial_count"]
+    tmax = -(-T // Wt)
     buf = np.zeros((len(CANDS), tmax), O.REC_DTYPE)
-    buf[:, :cnt] = recs
+    if cnt:
+        lo, li = P.sample(SEED, tb, cnt)      # counter-based: only this rank's trials
+        for x, (n, d, t) in enumerate(CANDS):
+            if cls[x] == me["my_class"]:      # only this rank's job class
+                buf[x, :cnt] = P.simulate(n, d, t, lo, li)[0]
     send = torch.from_numpy(buf.view(np.uint8).copy())
     gathered = [torch.zeros_like(send) for _ in range(world)]
     dist.all_gather(gathered, send)
     full = np.zeros((len(CANDS), T), O.REC_DTYPE)
+    filled = np.zeros((len(CANDS), T), np.int32)
     for r in range(world):
-        b, c = trial_share(T, world, r)
-        full[:, b:b + c] = gathered[r].numpy().view(O.REC_DTYPE).reshape(len(CANDS), tmax)[:, :c]
+        b, c, k = plans[r]["trial_begin"], plans[r]["trial_count"], plans[r]["my_class"]
+        g = gathered[r].numpy().view(O.REC_DTYPE).reshape(len(CANDS), tmax)
+        for x in range(len(CANDS)):
+            if cls[x] == k:
+                full[x, b:b + c] = g[x, :c]
+                filled[x, b:b + c] += 1
+    assert (filled == 1).all()                # every (candidate, trial) from exactly one rank
     if rank == 0:
         np.save(out_path, full.view(np.uint8))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("T", [5, 8])
-def test_sharded_records_equal_single_process(tmp_path, T):
-    world = 2
+@pytest.mark.parametrize("world,T", [(2, 5), (2, 8), (4, 3), (4, 1)])
+def test_sharded_records_equal_single_process(tmp_path, world, T):
     out = str(tmp_path / "full.npy")
     mp.spawn(_worker, args=(world, _free_port(), T, out), nprocs=world, join=True)
     full = np.load(out).view(O.REC_DTYPE).reshape(len(CANDS), T)
@@ -85,10 +114,14 @@ def test_sharded_records_equal_single_process(tmp_path, T):
 
 
 def test_trial_share_partitions():
+    S = _libsamu()
     for T in (1, 7, 64, 1024):
         for world in (1, 2, 3, 4, 8):
             seen = []
             for r in range(world):
                 b, c = trial_share(T, world, r)
                 seen.extend(range(b, b + c))
+                if T >= world:                # libsamu's pure trial sharding is this split
+                    p = S.samu_shard_plan(T, world, r)
+                    assert (p["trial_begin"], p["trial_count"]) == (b, c)
             assert seen == list(range(T))
