@@ -35,6 +35,9 @@
 #ifndef SAMU_K2_MULTI_EAGER   // 1: refill the window after every multi-request admission round
 #define SAMU_K2_MULTI_EAGER 0
 #endif
+#ifndef SAMU_K2_CHUNK_GRP   // schedule-sharing launches: chunk runs longer than this x the group size
+#define SAMU_K2_CHUNK_GRP 5
+#endif
 #ifndef SAMU_K2_CHUNK_MIN
 #define SAMU_K2_CHUNK_MIN 4   // decode runs longer than this take the lane-parallel chunk sums
 #endif
@@ -1059,7 +1062,11 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
         if (m_run > 0) {
           const uint64_t K0 = LC * B;
           const uint32_t smax0 = (uint32_t)((int32_t)m.d + m.maxO);
-          if (m_run > SAMU_K2_CHUNK_MIN) {
+          // (schedule sharing: the chunked sums run once per member while the iteration-by-
+          // iteration path evaluates every member in its own lane at once, so the chunks pay off
+          // only for runs ~nv times longer)
+          const uint32_t chunk_min = GRP ? (uint32_t)SAMU_K2_CHUNK_GRP * W.nv : (uint32_t)SAMU_K2_CHUNK_MIN;
+          if (m_run > chunk_min) {
             if (GRP) {
               // the chunked exact sums once per group member (lane v keeps member v's clock)
               const uint32_t nv = W.nv;
@@ -1113,7 +1120,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
             m.t = t;
           }
           K2STAT(8, done_it);
-          if (m_run > SAMU_K2_CHUNK_MIN) K2STAT(14, 1);
+          if (m_run > chunk_min) K2STAT(14, 1);
           // closed-form exact updates for the done_it iterations of the run
           // sum_j (K0 + K1 (S + B j)) = L c (B mm) + K1 (mm S + B mm (mm - 1) / 2); mm <= l_max < 2^16,
           // so mm (mm - 1) fits 32 bits and every product is one widening 32 x 32 multiply
