@@ -1182,7 +1182,10 @@ static samu_status run_jobs_impl(samu_ctx* c, std::vector<SimJob>& jobs, const u
       // concurrent LEAN launches only when the others are short (a few waves): then their
       // longest replica-sims are the critical path and the LEAN items fill the idle warps; with
       // many waves the kernels only compete for the instruction cache (~2 % slower)
-      const bool overlap = n_items[0] + n_items[2] + n_items[3] + n_items[4] + n_items[6] < 8 * (int64_t)c->n_sm * 24;
+      // (SAMU_K2_OVERLAP=0 / 1 overrides the rule: tests and sanitizer runs of the chained launches)
+      const int ov_env = std::getenv("SAMU_K2_OVERLAP") ? std::atoi(std::getenv("SAMU_K2_OVERLAP")) : -1;
+      const bool overlap = ov_env >= 0 ? ov_env != 0
+                                       : n_items[0] + n_items[2] + n_items[3] + n_items[4] + n_items[6] < 8 * (int64_t)c->n_sm * 24;
       CK(c, launch_simulate(LM, modes, nb, n_launch, dc.data(), (uint32_t)c->eng.block_size, s,
                             overlap ? c->aux_stream : nullptr, c->ev_fork, c->ev_join));
       c->launches += n_launch > 1 ? n_launch - 1 : 0;

@@ -15,6 +15,8 @@ for name, kw in [("c2", dict(n_prompts=60)), ("c4", dict(n_docs=20)), ("c5", dic
     S.samu_simulate_batch(cands, lo, li, summary=True, want_fin_iter=True, want_fin_t=True)
     os.environ["SAMU_K2_MODES"] = "always"   # the LEAN / FRESH paths on this small batch too
     S.samu_simulate_batch(cands, lo, li, summary=True)
+    os.environ["SAMU_K2_OVERLAP"] = "0"      # ... as launches chained in one stream (PDL)
+    S.samu_simulate_batch(cands, lo, li, summary=True)
     del os.environ["SAMU_K2_MODES"]
     st = S.fresh_state(2)
     S.samu_simulate_batch([cands[0][:3] + (0, -1, 1)], lo, li, state=st, time_limit=np.array([[5.0, 7.0]]))

@@ -32,17 +32,23 @@ def gpu(w):
 
 
 @contextlib.contextmanager
-def k2_modes(policy):
-    """SAMU_K2_MODES: "always" runs K2's LEAN / FRESH paths even on batches below the size rule."""
-    old = os.environ.get("SAMU_K2_MODES")
-    os.environ["SAMU_K2_MODES"] = policy
+def k2_modes(policy, overlap=None):
+    """SAMU_K2_MODES: "always" runs K2's LEAN / FRESH paths even on batches below the size rule;
+    SAMU_K2_OVERLAP="0": their launches run chained in one stream (programmatic dependent launch,
+    the large-batch configuration) instead of LEAN beside the others on a second stream."""
+    env = {"SAMU_K2_MODES": policy, "SAMU_K2_OVERLAP": overlap}
+    old = {k: os.environ.get(k) for k in env}
+    for k, v in env.items():
+        if v is not None:
+            os.environ[k] = v
     try:
         yield
     finally:
-        if old is None:
-            del os.environ["SAMU_K2_MODES"]
-        else:
-            os.environ["SAMU_K2_MODES"] = old
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
 
 
 def u16(t):
@@ -109,11 +115,14 @@ def _sim_parity(w, cands, T, tb=0, tau=None):
     # K2's LEAN path (k_simulate<16, ., 1>), the rest on the general one
     with k2_modes("always"):
         g_lean = recs(S.samu_simulate_batch(cands, glo, gli, time_limit=tau))
+    with k2_modes("always", overlap="0"):
+        g_chain = recs(S.samu_simulate_batch(cands, glo, gli, time_limit=tau))
     for ci, cd in enumerate(cands):
         node, dp, tp = cd[:3]
         o, ofi, oft = P.simulate(node, dp, tp, lo, li, tau=None if tau is None else tau[ci], want_fin=True)
         assert_rec_equal(g[ci], o, f"cand {cd}")
         assert_rec_equal(g_lean[ci], o, f"cand {cd} without per-request outputs")
+        assert_rec_equal(g_chain[ci], o, f"cand {cd} with the K2 launches chained in one stream")
         a, b = w.node_range(node)
         assert np.array_equal(fi[ci][:, a:b], ofi[:, a:b]), f"finish iterations differ for {cd}"
         assert np.array_equal(ft[ci][:, a:b], oft[:, a:b]), f"finish times differ for {cd}"
@@ -415,6 +424,10 @@ def test_planner_all_k2_paths(preemption):
         pg = gpu(w).samu_plan_greedy(SEED, 3, "greedy", preemption=preemption)
     pg.pop("n_sims")
     assert pg == po
+    with k2_modes("always", overlap="0"):   # the K2 launches of every batch chained in one stream
+        pc = gpu(w).samu_plan_greedy(SEED, 3, "greedy", preemption=preemption)
+    pc.pop("n_sims")
+    assert pc == po
 
 
 def test_known_lengths_bit_exact():
