@@ -55,12 +55,11 @@ struct ModelReg {
   std::vector<double> coeff;   // [5][3][2][nb]
   std::vector<double> load;    // [5][16]
   std::vector<uint32_t> ev, ec;
-  // FNV-1a fingerprint of the registration and the eCDF (schedule-sharing hints, samu_app_load)
+  // fingerprint of the registration and the eCDF (schedule-sharing hints, samu_app_load): one
+  // multiply-xor step per field (a hint key only: records never depend on it)
   uint64_t fingerprint() const {
     uint64_t h = 1469598103934665603ull;
-    auto mix = [&h](uint64_t x) {
-      for (int i = 0; i < 8; ++i) { h ^= (x >> (8 * i)) & 0xFFu; h *= 1099511628211ull; }
-    };
+    auto mix = [&h](uint64_t x) { h = (h ^ (x + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2))) * 1099511628211ull; };
     mix(spec.n_layers); mix(spec.hidden); mix(spec.c); mix(spec.l_max); mix(spec.tp_mask);
     mix(spec.weight_bytes); mix(spec.kv_bytes_per_token);
     auto mixd = [&mix](double x) { uint64_t u; std::memcpy(&u, &x, 8); mix(u); };
@@ -150,6 +149,11 @@ struct samu_ctx {
   std::map<std::pair<int, int>, DevBuf> coef;                      // (model, tp slot) -> dense table
   struct RepLists { DevBuf off, req; uint64_t gen = 0; };
   std::map<std::pair<int, int>, RepLists> rep;    // (node, dp) -> replica CSR, built for app load `gen`
+  // every (node, dp) of the nodes' valid plans, built at the first use after an app load into
+  // one arena (one upload instead of two synchronous ones per pair): key -> (off, req) offsets
+  DevBuf rep_arena;
+  uint64_t rep_arena_gen = 0;
+  std::map<std::pair<int, int>, std::pair<size_t, size_t>> rep_at;
   uint64_t app_gen = 1;                            // bumped by every samu_app_load (buffers are reused)
   std::map<std::pair<int, int>, std::vector<uint32_t>> rep_off_host;
 
@@ -545,8 +549,8 @@ extern "C" samu_status samu_app_load(samu_ctx* c, const samu_engine_cfg* engine,
   CK(c, upload(c->d_node, nd, s));
   CK(c, upload(c->d_succ, c->succ, s));
   CK(c, upload(c->d_cross, c->cross, s));
-  c->d_waves.clear();
-  for (auto& w : c->waves) { c->d_waves.emplace_back(); CK(c, upload(c->d_waves.back(), w, s)); }
+  if (c->d_waves.size() < c->waves.size()) c->d_waves.resize(c->waves.size());   // buffers kept across loads
+  for (size_t i = 0; i < c->waves.size(); ++i) CK(c, upload(c->d_waves[i], c->waves[i], s));
   // eCDF tables: each registered model's sorted multiset expanded on the device (reading c2)
   {
     std::vector<int32_t> toff(SAMU_MAX_NODES + 1, 0);
@@ -644,17 +648,18 @@ extern "C" samu_status samu_app_load(samu_ctx* c, const samu_engine_cfg* engine,
     c->node_exp_out[v] = std::max(1.0, acc / (double)(c->node_end[v] - c->node_begin[v]));
   }
   c->app_loaded = true;
-  {   // FNV-1a over the fields (no struct padding)
+  {   // one multiply-xor step per field (no struct padding); each model's fingerprint once
     uint64_t h = 1469598103934665603ull;
-    auto mix = [&h](uint64_t x) {
-      for (int i = 0; i < 8; ++i) { h ^= (x >> (8 * i)) & 0xFFu; h *= 1099511628211ull; }
-    };
+    auto mix = [&h](uint64_t x) { h = (h ^ (x + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2))) * 1099511628211ull; };
+    std::map<int, uint64_t> model_fp;
     mix(e.max_num_seqs); mix(e.block_size); mix(e.min_batched_tokens); mix(e.mem_util_permille);
     mix(e.mem_bytes_per_gpu); mix(e.kv_cap_bytes_per_gpu); mix(e.n_gpus);
     mix((uint64_t)n_nodes);
     for (int v = 0; v < n_nodes; ++v) {
       mix((uint64_t)(uint32_t)node_model[v]);
-      mix(c->models[node_model[v]].fingerprint());
+      auto f = model_fp.find(node_model[v]);
+      if (f == model_fp.end()) f = model_fp.emplace(node_model[v], c->models[node_model[v]].fingerprint()).first;
+      mix(f->second);
     }
     mix((uint64_t)n_req);
     for (const samu_request& q : c->req) {
@@ -689,17 +694,47 @@ static DevApp dev_app(const samu_ctx* c) {
 }
 
 // requests of `node` grouped by dp replica (c13): key = chain id if >= 0 else index within node
+static void replica_lists(const samu_ctx* c, int node, int dp, std::vector<uint32_t>& o, std::vector<uint32_t>& l) {
+  // counting sort by replica, stable in request order
+  const int b = c->node_begin[node], e = c->node_end[node];
+  auto rep_of = [&](int r) { return (c->req[r].chain >= 0 ? c->req[r].chain : r - b) % dp; };
+  o.assign(dp + 1, 0);
+  for (int r = b; r < e; ++r) o[rep_of(r) + 1] += 1;
+  for (int j = 0; j < dp; ++j) o[j + 1] += o[j];
+  l.resize((size_t)(e - b));
+  std::vector<uint32_t> at(o.begin(), o.end() - 1);
+  for (int r = b; r < e; ++r) l[at[rep_of(r)]++] = (uint32_t)r;
+}
+
 static samu_status replicas(samu_ctx* c, int node, int dp, const uint32_t** off, const uint32_t** lst) {
   auto key = std::make_pair(node, dp);
-  auto it = c->rep.find(key);
-  if (it == c->rep.end() || it->second.gen != c->app_gen) {
-    std::vector<std::vector<uint32_t>> L(dp);
-    for (int r = c->node_begin[node]; r < c->node_end[node]; ++r) {
-      const int kk = c->req[r].chain >= 0 ? c->req[r].chain : r - c->node_begin[node];
-      L[kk % dp].push_back((uint32_t)r);
+  if (c->rep_arena_gen != c->app_gen) {   // first use after an app load: every plan's lists at once
+    c->rep_at.clear();
+    std::vector<uint32_t> all, o, l;
+    for (int v = 0; v < c->n_nodes; ++v) {
+      std::set<int> dps;
+      for (const auto& pl : plans_of(c, c->node_model[v])) dps.insert(pl.first);
+      for (int d : dps) {
+        replica_lists(c, v, d, o, l);
+        c->rep_at[{v, d}] = {all.size(), all.size() + o.size()};
+        all.insert(all.end(), o.begin(), o.end());
+        all.insert(all.end(), l.begin(), l.end());
+        c->rep_off_host[{v, d}] = o;
+      }
     }
-    std::vector<uint32_t> o(dp + 1, 0), l;
-    for (int j = 0; j < dp; ++j) { o[j + 1] = o[j] + (uint32_t)L[j].size(); l.insert(l.end(), L[j].begin(), L[j].end()); }
+    CK(c, upload(c->rep_arena, all, c->stream));
+    c->rep_arena_gen = c->app_gen;
+  }
+  auto at = c->rep_at.find(key);
+  if (at != c->rep_at.end()) {
+    *off = c->rep_arena.as<uint32_t>() + at->second.first;
+    *lst = c->rep_arena.as<uint32_t>() + at->second.second;
+    return SAMU_OK;
+  }
+  auto it = c->rep.find(key);
+  if (it == c->rep.end() || it->second.gen != c->app_gen) {   // a (node, dp) outside the plans
+    std::vector<uint32_t> o, l;
+    replica_lists(c, node, dp, o, l);
     auto& pr = c->rep[key];
     CK(c, upload(pr.off, o, c->stream));
     CK(c, upload(pr.req, l, c->stream));
