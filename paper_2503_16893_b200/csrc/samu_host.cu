@@ -539,6 +539,11 @@ extern "C" samu_status samu_app_load(samu_ctx* c, const samu_engine_cfg* engine,
     if (q.pred < 0) c->waves[0].push_back(r);
     else if (c->cross[r]) c->waves[depth[q.node]].push_back(r);
   }
+  // K1 walks a chain serially in one thread: chain roots first (stable), so the blocks holding
+  // them start at the front of each trial group's row of the grid instead of forming its tail
+  // (sampled values are keyed by request id: the order changes nothing else)
+  if (!std::getenv("SAMU_K1_INDEX_ORDER"))
+    std::stable_partition(c->waves[0].begin(), c->waves[0].end(), [&](int r) { return c->succ[r] >= 0; });
   cudaStream_t s = c->stream;
   std::vector<uint32_t> lib(n_req), cap(n_req);
   std::vector<int32_t> pred(n_req), nd(n_req);
