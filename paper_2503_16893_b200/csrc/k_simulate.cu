@@ -1528,12 +1528,16 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
 #ifndef SAMU_K2_MINB_LEAN
 #define SAMU_K2_MINB_LEAN 7
 #endif
+// LEAN schedule-sharing launches (mode 5): the LEAN count unless overridden (experiments)
+#ifndef SAMU_K2_MINB_GRP
+#define SAMU_K2_MINB_GRP SAMU_K2_MINB_LEAN
+#endif
 // A launch holds only items of one MODE (DevCand::mode); the host issues one launch per mode
 // present (one kernel holding several paths is slower: a multiple of the code footprint).
 template <int BSK, bool CONSTC, int MODE>
 // (the minimum block counts are per 4-warp block: the register caps stay the same for any block size)
 __global__ void __launch_bounds__(32 * SAMU_WARPS_PER_BLOCK,
-                                  (is_lean(MODE) ? SAMU_K2_MINB_LEAN : (MODE == 2 || MODE == 4) ? SAMU_K2_MINB_FRESH
+                                  (MODE == 5 ? SAMU_K2_MINB_GRP : is_lean(MODE) ? SAMU_K2_MINB_LEAN : (MODE == 2 || MODE == 4) ? SAMU_K2_MINB_FRESH
                                                                                     : SAMU_K2_MINB) * 4 / SAMU_WARPS_PER_BLOCK)
     k_simulate(SimLaunch P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
