@@ -414,6 +414,15 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
   // the host runs a candidate on the FRESH paths (modes 2, 4, 6) only when its node has chain
   // successors (DevCand::has_succ): no constant-bank read for it there
   constexpr bool SUCC = MODE == 2 || MODE == 4 || MODE == 6;
+  // ... and without per-request outputs a running request's id is needed only to find its chain
+  // successor when it finishes: on those paths the window, the slots, the preempted stack and the
+  // finisher list carry the successor's id (-1: none) instead, loaded beside the request's lengths
+  // when it enters the window, so a finish releases its successor without a dependent global load
+#ifdef SAMU_K2_NO_SUCC_SLOT
+  constexpr bool SUCC_SLOT = false;
+#else
+  constexpr bool SUCC_SLOT = SUCC;
+#endif
   // lazy window refills (see the loop top)
 #ifdef SAMU_K2_EAGER_WIN
   constexpr bool LAZYW = false;
@@ -667,7 +676,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
         const uint32_t r_ = qr[qp_];                                                           \
         /* recompute front (reload) keeps its tokens */                                        \
         const uint32_t g_ = (!FRESH && qp_ < m.n_front) ? (uint32_t)gst[r_] : 0u;              \
-        w_r = r_;                                                                              \
+        w_r = SUCC_SLOT ? (uint32_t)__ldg(A.succ + r_) : r_;                                   \
         w_p = LI_(r_) + g_;                                                                    \
         w_rem = max((uint32_t)LO_(r_), 1u) - g_;                                               \
       }                                                                                        \
@@ -1357,7 +1366,7 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
         const uint32_t itx = m.iter + m.d - 1;   // iterations = prefills + decodes
         if (FRESH && n_fin == 1) {
           // one finisher (FRESH: no outputs): its successor, if any, joins the back of W
-          const int32_t sr = (SUCC || C.has_succ) ? __ldg(A.succ + W.tmp[0]) : -1;
+          const int32_t sr = SUCC_SLOT ? (int32_t)W.tmp[0] : (SUCC || C.has_succ) ? __ldg(A.succ + W.tmp[0]) : -1;
           if (sr >= 0) {
             if (lane == 0) q[m.q_tail] = (uint32_t)sr;
             m.q_tail += 1;
@@ -1376,7 +1385,8 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
                 if (commit) { st[r] = SAMU_ST_DONE << 28; ft[r] = m.t; }
               }
             }
-            if (SUCC || C.has_succ) sr = __ldg(A.succ + r);
+            if (SUCC_SLOT) sr = (int32_t)r;
+            else if (SUCC || C.has_succ) sr = __ldg(A.succ + r);
           }
           const uint32_t br = __ballot_sync(FULL, sr >= 0);
           if (br) {
@@ -1402,7 +1412,8 @@ __device__ __forceinline__ void sim_item(const SimLaunch& P, WarpSmT<is_lean(MOD
                 if (fto) fto[r] = m.t;
                 if (commit) { st[r] = SAMU_ST_DONE << 28; ft[r] = m.t; }
               }
-              if (SUCC || C.has_succ) sr = __ldg(A.succ + r);
+              if (SUCC_SLOT) sr = (int32_t)r;
+              else if (SUCC || C.has_succ) sr = __ldg(A.succ + r);
             }
             // compacted in place: the k-th successor overwrites finisher slot <= k, already read
             // by every lane of this pass (the __syncwarp orders those reads before the writes)
